@@ -1,0 +1,367 @@
+"""Benchmark of the solve phase (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+One STEP = one full AMG-PCG solve (every SURVEY §8(a) row: outer SpMV+dot, CG update, V-cycle with
+Chebyshev-ℓ1-Jacobi pre/post smoothing on every level, restriction, coarsest solve, prolongation,
+direction update) of the workload's system K u = F from u0 = 0 to rtol 1e-6, with K's hierarchy and F
+already resident in HBM.  The hierarchy setup (host) is built once before timing and reported apart.
+
+value = solve seconds per step (the paper's "solve s"), lower is better.  At N > 1 this
+version runs one independent replica of the workload per GPU ("replicas", weak: per-GPU work fixed);
+the distributed row-block solve is future work.
+
+--impl reference times the ORACLE (plain single-threaded C, oracle/) on a bounded sample of the same
+workload, scaled by the byte model to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import amg_inputs  # noqa: E402
+
+METRIC = "AMG-PCG solve s & s/iter, iters, V-cycle HBM GB/s (% peak) at 1/2/4/8 B200"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload_desc(cfg: str) -> dict:
+    c = amg_inputs.CONFIGS[cfg]
+    return dict(c, name=cfg, m=amg_inputs.CHEB_DEGREE[c["p"]])
+
+
+def byte_model(info: dict, m: int) -> dict:
+    """Algorithmic bytes of one PCG iteration: 12 B per stored non-zero read
+    (fp64 value + int32 column), 8 B row pointer + vector traffic per row per sweep."""
+    nnz, N, nnzP, L = info["nnz"], info["N"], info["nnz_P"], info["levels"]
+    b = 12.0 * (2 * m + 1) * nnz[0] + 64.0 * (2 * m + 1) * N[0]
+    for l in range(1, L - 1):
+        b += 12.0 * 2 * m * nnz[l] + 64.0 * 2 * m * N[l]
+    for l in range(L - 1):
+        b += 2 * (12.0 * nnzP[l]) + 8.0 * (N[l] + N[l + 1]) * 2
+    b += 12.0 * nnz[L - 1] * 30 if L > 1 else 0.0
+    b += 100.0 * N[0]  # outer CG vector updates and dots
+    sweep0 = 12.0 * nnz[0] + 64.0 * N[0]
+    return dict(iter_bytes=b, sweep0_bytes=sweep0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 5 + k and s[5 + k] == "Active"})
+        under_load = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(under_load) if under_load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+def ncu_traffic(cfg: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_dominant.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if d.get("workload") == cfg:
+            return d.get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def run_gpu(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_21268_b200 as amg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = workload_desc(args.config)
+    dim, p, n, m = wl["dim"], wl["p"], wl["n"], wl["m"]
+    t0 = time.perf_counter()
+    K, F = amg.iga_poisson(dim, p, n)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    H = amg.Hierarchy(K, amg.params(p))
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    info = H.info()
+    N = K.shape[0]
+    del K
+    stream = torch.cuda.current_stream()
+    Fd = torch.from_numpy(F).cuda()
+    u = torch.zeros_like(Fd)
+
+    def step():
+        u.zero_()
+        return H.solve(Fd, u=u, rtol=args.rtol, maxit=args.maxit, stream=stream, history=False)
+
+    for _ in range(args.warmup):
+        _, iters, relres, _, st = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    H.set_profiling(True)
+    iters_seen = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, iters, relres, _, st = step()
+            iters_seen.append(iters)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ks = H.kernel_stats()
+    H.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+
+    # end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
+    Fh = torch.from_numpy(F).pin_memory()
+    uh = torch.zeros_like(Fh).pin_memory()
+    for _ in range(max(1, args.warmup // 2)):
+        uh.zero_()
+        H.solve_host_ptr(Fh.data_ptr(), uh.data_ptr(), rtol=args.rtol, maxit=args.maxit, stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        uh.zero_()
+        H.solve_host_ptr(Fh.data_ptr(), uh.data_ptr(), rtol=args.rtol, maxit=args.maxit, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = t.item()
+
+    peak, peak_src = load_peaks()
+    bm = byte_model(info, m)
+    iters = iters_seen[-1]
+    solve_s = ms / 1e3
+    per_launch_ms = ks["total_ms"] / max(ks["launches"], 1)
+    achieved = ks["bytes_per_launch"] / (per_launch_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.config)
+    vcyc_gbs = bm["iter_bytes"] * iters / solve_s / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, iters, info, m, reps=2)
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(solve_s, 6),
+            "unit": "s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 4),
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (generated IgA Poisson system, manufactured-solution RHS)",
+            "config": {
+                "workload": f"{args.config}: {dim}-D Poisson, B-spline p={p}, n={n} elements/dir, "
+                            f"{N} free DOFs, AMG-PCG rtol {args.rtol}",
+                "dofs": N, "nnz_K0": info["nnz"][0], "levels": info["levels"], "level_N": info["N"],
+                "opc": round(info["opc"], 4), "cheb_degree": m, "coarse_sweeps": 30,
+                "parallelism": "replicas" if world > 1 else "single",
+                "l2": "inputs exceed L2 (K0 = %.2f GB >> 126 MB); no flush needed" % (12e-9 * info["nnz"][0]),
+            },
+            "iters": iters,
+            "s_per_iter": round(solve_s / max(iters, 1), 7),
+            "relres": relres,
+            "setup_s": round(t_setup, 3),
+            "generator_s": round(t_gen, 3),
+            "vcycle_GBps": round(vcyc_gbs, 1),
+            "vcycle_frac_of_peak": round(vcyc_gbs / peak, 4),
+            "gpu_launches": ks["kernels_launched"],
+            "roofline": {
+                "kernel": "k_csr2<32, EpiCheb> (fused Chebyshev-ℓ1-Jacobi step on level 0)",
+                "bound": "hbm",
+                "achieved": round(achieved, 1),
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": traffic,
+                "algorithmic_bytes_per_launch": ks["bytes_per_launch"],
+                "launch_ms": round(per_launch_ms, 5),
+                "launches_timed": ks["launches"],
+            },
+            "e2e": {
+                "value": round(ms_e2e / 1e3, 6), "unit": "s",
+                "h2d_bytes_per_step": 2 * 8 * N, "d2h_bytes_per_step": 8 * N,
+                "api": "amg_pcg_solve_host (pinned host F,u)",
+            },
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------------
+# oracle arm (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------------
+def _oracle_sample(cfg: str):
+    """Assemble the workload's K with the oracle (exact tables + plain C Kronecker sum)."""
+    import oracle
+    wl = workload_desc(cfg)
+    return oracle.assemble(wl["dim"], wl["p"], wl["n"])
+
+
+def cpu_baseline(cfg: str, iters: int, info: dict, m: int, reps: int = 2, K=None) -> dict:
+    """The oracle, as it stands, single-threaded: `reps` of its level-0 sweeps (or_spmv over the
+    workload's own K_0) timed, scaled by the byte model to one PCG iteration and by the iteration
+    count to a solve.  (A full oracle solve of C3 needs a ~10 min single-threaded setup.)"""
+    import oracle
+    if K is None:
+        K = _oracle_sample(cfg)
+    x = amg_inputs.uniform_pm1(K.shape[0], seed=5)
+    oracle.spmv(K, x)  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.spmv(K, x)
+    t_sweep = (time.perf_counter() - t0) / reps
+    bm = byte_model(info, m)
+    s_iter = t_sweep * bm["iter_bytes"] / bm["sweep0_bytes"]
+    return {"value": round(s_iter * iters, 4), "unit": "s", "cores": 1, "kind": "oracle",
+            "s_per_iter": round(s_iter, 4), "iters_used": iters,
+            "sample": f"{reps} oracle level-0 SpMV sweeps over the {cfg} K0 ({K.nnz} nnz, "
+                      f"{t_sweep:.3f} s each), scaled by the byte model (x{bm['iter_bytes'] / bm['sweep0_bytes']:.1f}) "
+                      f"to one PCG iteration and by {iters} iterations to a solve"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = workload_desc(args.config)
+    # hierarchy sizes for the byte model come from the oracle's own setup, precomputed by the
+    # committed oracle-only script oracle/scripts/hierarchy_sizes.py (a C3 oracle setup takes minutes)
+    path = os.path.join(ROOT, "oracle", f"sizes_{args.config}.json")
+    if not os.path.exists(path):
+        print(json.dumps({"impl": "reference", "unavailable": f"{path} missing (run oracle/scripts/hierarchy_sizes.py)"}))
+        return
+    with open(path) as f:
+        info = json.load(f)
+    K = _oracle_sample(args.config)
+    iters = int(info.get("oracle_iters", args.ref_iters))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(args.config, iters, info, wl["m"], reps=1, K=K)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 2),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated IgA Poisson system)",
+        "config": {"workload": f"{args.config}: {wl['dim']}-D Poisson, B-spline p={wl['p']}, n={wl['n']}"},
+        "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "oracle", "sample": r["sample"]},
+        "e2e": {"value": round(v, 4), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(amg_inputs.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rtol", type=float, default=1e-6)
+    ap.add_argument("--maxit", type=int, default=200)
+    ap.add_argument("--ref-iters", type=int, default=15, help="iteration count the reference arm scales to")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

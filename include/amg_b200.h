@@ -1,0 +1,180 @@
+/*
+ * amg_b200.h — C ABI of the B200-native solve path of arXiv 2511.21268 (D'Ambra, Durastante,
+ * Filippone, "Parallel matching-based AMG preconditioners for elliptic equations discretized by
+ * IgA"): fp64 PCG on the IgA Poisson stiffness system K u = F, preconditioned by one V-cycle of a
+ * compatible-weighted-matching AMG hierarchy with Chebyshev-accelerated ℓ1-Jacobi smoothing.
+ *
+ * Citations "P:Lnnn" are lines of the paper text; "c.N" are the readings listed in
+ * DESIGN.md §3 (taken from SURVEY.md §8(c)).
+ *
+ * Conventions for every entry point:
+ *   - All functions return amg_status.  No C++ exception crosses the ABI.  On a non-OK status the
+ *     thread-local message from amg_last_error() says what failed; output arguments are then
+ *     unspecified unless stated otherwise.
+ *   - Input arrays are BORROWED for the duration of the call (copied when kept).  Every output the
+ *     library allocates is released by the matching amg_*_free / amg_free.
+ *   - Matrices are CSR, 0-based, int64 row pointers, int32 columns sorted strictly ascending in each
+ *     row, fp64 values (amg_csr).
+ *   - A hierarchy handle may be used by one host thread at a time.
+ *   - There is no CPU fallback: solve-phase entry points need a CUDA device (sm_100a) and return
+ *     AMG_ENODEV / AMG_ECUDA without one.
+ */
+#ifndef AMG_B200_H
+#define AMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AMG_OK = 0,
+    AMG_NOT_CONVERGED = 1, /* outputs valid; iters == maxit and relres > rtol                  */
+    AMG_EINVAL = -1,       /* bad argument (NULL, size mismatch, unsupported option)            */
+    AMG_ENOMEM = -2,       /* host or device allocation failed                                  */
+    AMG_ECUDA = -3,        /* CUDA runtime error (message has the CUDA error string)            */
+    AMG_ENCCL = -4,        /* NCCL error (multi-GPU)                                            */
+    AMG_ENOTSPD = -5,      /* d̂_i <= 0, missing diagonal, pᵀKp <= 0 or rᵀz <= 0 (CG breakdown)  */
+    AMG_ENODEV = -6        /* no usable CUDA device                                             */
+} amg_status;
+
+/* Host CSR matrix (n_rows x n_cols, nnz entries). */
+typedef struct {
+    int64_t n_rows, n_cols, nnz;
+    int64_t *row_ptr; /* n_rows + 1 */
+    int32_t *col;     /* nnz, strictly ascending within a row */
+    double *val;      /* nnz */
+} amg_csr;
+
+/* ---------------------------------------------------------------------------------------------
+ * Problem generator: tensor-product B-spline Poisson stiffness (eq:matrix_and_vector_
+ * values P:L646-650) on the unit square (dim 2) or cube (dim 3) with n_elem uniform elements per
+ * direction, degree `degree`, maximal regularity C^{p-1}.
+ *
+ * DOFs on Dirichlet sides are eliminated.  Side s (1..2*dim) is Dirichlet iff bit s-1
+ * of dirichlet_sides is set; sides are 1:x=0 2:x=1 3:y=0 4:y=1 5:z=0 6:z=1; the paper's cube uses
+ * sides 1,2,3 = 0x7.  Free DOFs are numbered lexicographically, x fastest (c.1).
+ * K is assembled as the Kronecker sum of 1-D tables computed by (p+1)-point Gauss quadrature in
+ * binary128 and rounded once (c.3, Remark P:L570-573), in the canonical order of DESIGN.md §3 (c.4).
+ *
+ * rhs = 0: F = load of the manufactured solution u* = sin(πx) sin(πy/2) [cos(πz)] (c.5);
+ * rhs = 1: F = 0.
+ * Outputs: *K (free with amg_csr_free) and *F (length K->n_rows, free with amg_free).
+ * Errors: AMG_EINVAL for dim ∉ {2,3}, degree ∉ [1,8], n_elem < 1, sides out of range, or more
+ * than 2^31-1 free DOFs; AMG_ENOMEM.
+ */
+typedef struct {
+    int dim;
+    int degree;
+    int n_elem;
+    uint32_t dirichlet_sides;
+    int rhs;
+} amg_iga_desc;
+
+amg_status amg_iga_poisson(const amg_iga_desc *desc, amg_csr **K, double **F);
+
+/* The rounded integer-knot (h = 1) 1-D tables M̂_ab = ∫N_aN_b, K̂_ab = ∫N'_aN'_b (c.3) in band
+ * storage: mhat[a*(2p+1) + (b-a+p)], a = 0..n+p-1 (caller allocates (n+p)*(2p+1) doubles each;
+ * entries with b outside 0..n+p-1 are 0).  For bitwise checks against exact rationals. */
+amg_status amg_iga_tables(int degree, int n_elem, double *mhat, double *khat);
+
+void amg_csr_free(amg_csr *K);
+void amg_free(void *p);
+
+/* ---------------------------------------------------------------------------------------------
+ * Hierarchy parameters (defaults from amg_params_default; meaning in DESIGN.md §3).
+ */
+typedef struct {
+    int agg_steps;          /* pairwise matchings per level: 3 -> aggregates of size <= 8 */
+    int smooth_prolong;     /* 1: P̄ = (I − ω D_f⁻¹K_f) P; 0: tentative P            */
+    double match_threshold; /* edge eligible iff c_ij > threshold (1.0, c.8)                          */
+    double filter_theta;    /* strength filter for the prolongator smoothing matrix (0.01, c.12);
+                               0 = literal (I − ωD⁻¹K)P                                                */
+    int cheb_degree;        /* Chebyshev degree m = SpMVs per smoothing (p=3→8, 4→12, 5→14, 6→16; p=2→4) */
+    int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30)                */
+    int64_t coarse_size;    /* coarsest when N_l <= coarse_size (50)                 */
+    int max_levels;         /* 20                                                                 */
+    int format;             /* device matrix format: 0 auto, 1 CSR warp-per-row, 2 SELL-32 (row per lane) */
+    int host_only;          /* 1: build the hierarchy on the host only (export/inspection; no CUDA call) */
+    int num_threads;        /* host setup threads (OpenMP); 0 = runtime default                     */
+} amg_params;
+
+/* Defaults for spline degree p (sets cheb_degree from the table above). EINVAL for p ∉ [1,8]. */
+amg_status amg_params_default(amg_params *prm, int spline_degree);
+
+/* Device allocator hook (e.g. PyTorch's caching allocator).  Unset -> cudaMalloc/cudaFree.
+ * alloc returns NULL on failure.  Must be set before amg_setup; applies to hierarchies created after. */
+typedef void *(*amg_alloc_fn)(size_t bytes, int device, void *cuda_stream);
+typedef void (*amg_free_fn)(void *ptr, size_t bytes, int device, void *cuda_stream);
+amg_status amg_set_allocator(amg_alloc_fn alloc, amg_free_fn free_fn);
+
+/* Multi-GPU descriptor: one process per GPU.  NULL or nranks == 1 -> single GPU `device`
+ * (NULL -> the current device). */
+typedef struct {
+    int rank, nranks;
+    unsigned char nccl_id[128]; /* ncclUniqueId from rank 0, broadcast by the caller */
+    int device;
+} amg_dist;
+
+typedef struct amg_hierarchy amg_hierarchy; /* opaque, library-owned */
+
+/* Builds the hierarchy of K on the host (deterministic; bitwise reproducible; c.6-c.15) and, unless
+ * prm->host_only, uploads it to the device.  K is borrowed (copied).  K must be square, symmetric
+ * and have a positive diagonal (else AMG_ENOTSPD).  prm NULL -> amg_params_default(·, 2).
+ * *H is released with amg_hierarchy_free. */
+amg_status amg_setup(const amg_csr *K, const amg_params *prm, const amg_dist *dist, amg_hierarchy **H);
+
+/* PCG (c.19) preconditioned by one V-cycle per iteration (c.18).
+ * F, u: DEVICE pointers (fp64, N = K->n_rows); u holds the initial guess on entry and the solution on
+ * exit.  Stops when ‖r_k‖₂ <= rtol·‖F‖₂ (recurrence residual) or k == maxit; iteration count = number
+ * of K·p products.  F == 0 -> u = 0, *iters = 0.  cuda_stream: cudaStream_t (NULL = legacy default).
+ * resid_history: nullable host array of length maxit+1, receives ‖r_k‖/‖F‖.
+ * Returns AMG_OK, AMG_NOT_CONVERGED, AMG_ENOTSPD (breakdown), AMG_ECUDA, AMG_EINVAL. */
+amg_status amg_pcg_solve(amg_hierarchy *H, const double *F, double *u, double rtol, int maxit,
+                         void *cuda_stream, int *iters, double *relres, double *resid_history);
+
+/* Same as amg_pcg_solve with HOST F and u (copied to / from the device inside the call). */
+amg_status amg_pcg_solve_host(amg_hierarchy *H, const double *F, double *u, double rtol, int maxit,
+                              void *cuda_stream, int *iters, double *relres, double *resid_history);
+
+/* One V-cycle z = V(r) (c.18) on DEVICE vectors of length N_0. */
+amg_status amg_vcycle(amg_hierarchy *H, const double *r, double *z, void *cuda_stream);
+
+/* y = A x on the device for A = K_l (op 0), P̄_l (op 1, x has N_{l+1} entries) or R_l = P̄_lᵀ (op 2). */
+amg_status amg_level_apply(amg_hierarchy *H, int level, int op, const double *x, double *y,
+                           void *cuda_stream);
+
+/* Hierarchy summary; arrays sized >= max_levels (nullable).  nnz_P[l] = nnz(P̄_l) (0 on the
+ * coarsest).  opc = Σ nnz(K_l)/nnz(K_0). */
+amg_status amg_hierarchy_info(const amg_hierarchy *H, int64_t *n_levels, int64_t *N, int64_t *nnz,
+                              int64_t *nnz_P, double *opc);
+
+/* Host copies of level l's K_l, P̄_l (NULL on the coarsest), composite aggregate map (fine row ->
+ * coarse index; NULL on the coarsest), ℓ1 diagonal d̂_l and ω_l.  Any output pointer may be NULL.
+ * Free with amg_csr_free / amg_free. */
+amg_status amg_hierarchy_export(const amg_hierarchy *H, int level, amg_csr **K_l, amg_csr **P_l,
+                                int32_t **aggregate_of, double **dhat, double *omega);
+
+/* Kernel timing of the dominant kernel (the fused Chebyshev step on level 0), recorded with CUDA
+ * events on the launching stream while enabled.  bytes_per_launch is the ALGORITHMIC byte count
+ * 12·nnz(K_0) + 64·N_0. */
+typedef struct {
+    int64_t launches;
+    double total_ms;
+    double bytes_per_launch;
+    int64_t kernels_launched; /* all library kernels launched since the counter was reset */
+} amg_kernel_stats;
+amg_status amg_set_profiling(amg_hierarchy *H, int enable); /* enable resets the counters */
+amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
+
+void amg_hierarchy_free(amg_hierarchy *H);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+const char *amg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMG_B200_H */

@@ -1,0 +1,237 @@
+"""paper_2511_21268_b200 — B200-native solve path of arXiv 2511.21268.
+
+fp64 PCG on the IgA Poisson stiffness system K u = F, preconditioned by one V-cycle of a
+compatible-weighted-matching AMG hierarchy (Chebyshev-accelerated ℓ1-Jacobi smoothing), behind the
+C ABI of ``include/amg_b200.h``.  This module is a thin binding: argument marshalling only.  PyTorch
+provides device memory (caching allocator hook) and streams.
+
+    K, F = iga_poisson(dim=3, p=3, n=96)          # generator (host, library)
+    H = Hierarchy(K, params(p=3))                 # host setup + upload
+    u, iters, relres, hist = H.solve(F_cuda)      # device PCG
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import AmgError, check, lib
+
+__all__ = ["AmgError", "Hierarchy", "iga_poisson", "iga_tables", "params", "use_torch_allocator", "HostCsr"]
+
+
+@dataclass
+class HostCsr:
+    indptr: np.ndarray
+    indices: np.ndarray
+    data: np.ndarray
+    shape: tuple
+
+    @property
+    def nnz(self) -> int:
+        return int(self.indptr[-1])
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        A = sp.csr_matrix((self.data, self.indices, self.indptr), shape=self.shape)
+        A.has_sorted_indices = True
+        return A
+
+
+def _from_c(ptr) -> HostCsr:
+    rp, ci, v, shape = _lib.csr_to_numpy(ptr.contents)
+    lib().amg_csr_free(ptr)
+    return HostCsr(rp, ci, v, shape)
+
+
+def iga_poisson(dim: int, p: int, n: int, dirichlet_sides: int = 0b000111, rhs: int = 0):
+    """amg_iga_poisson: (K as HostCsr, F as numpy fp64)."""
+    d = _lib.amg_iga_desc(dim, p, n, dirichlet_sides, rhs)
+    Kp = C.POINTER(_lib.amg_csr)()
+    Fp = C.POINTER(C.c_double)()
+    check(lib().amg_iga_poisson(C.byref(d), C.byref(Kp), C.byref(Fp)))
+    K = _from_c(Kp)
+    F = np.ctypeslib.as_array(Fp, shape=(K.shape[0],)).copy()
+    lib().amg_free(Fp)
+    return K, F
+
+
+def iga_tables(p: int, n: int):
+    """amg_iga_tables: rounded h=1 1-D tables (M̂, K̂) in band storage (n+p, 2p+1)."""
+    m = n + p
+    M = np.zeros((m, 2 * p + 1))
+    K = np.zeros((m, 2 * p + 1))
+    dp = C.POINTER(C.c_double)
+    check(lib().amg_iga_tables(p, n, M.ctypes.data_as(dp), K.ctypes.data_as(dp)))
+    return M, K
+
+
+def params(p: int, **overrides) -> _lib.amg_params:
+    prm = _lib.amg_params()
+    check(lib().amg_params_default(C.byref(prm), p))
+    for k, v in overrides.items():
+        if not hasattr(prm, k):
+            raise AttributeError(k)
+        setattr(prm, k, v)
+    return prm
+
+
+_ALLOC_REFS = None
+
+
+def use_torch_allocator() -> None:
+    """Route the library's device allocations through PyTorch's caching allocator."""
+    global _ALLOC_REFS
+    if _ALLOC_REFS is not None:
+        return
+    import torch
+
+    ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+    FREE = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+
+    def _alloc(nbytes, device, stream):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device=int(device))
+        except Exception:  # noqa: BLE001 — the C side reports AMG_ENOMEM
+            return None
+
+    def _free(ptr, nbytes, device, stream):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    refs = (ALLOC(_alloc), FREE(_free))
+    check(lib().amg_set_allocator(C.cast(refs[0], C.c_void_p), C.cast(refs[1], C.c_void_p)))
+    _ALLOC_REFS = refs
+
+
+def _borrow(K) -> tuple:
+    """View a HostCsr / scipy CSR as an amg_csr (arrays kept alive by the returned tuple)."""
+    indptr = np.ascontiguousarray(K.indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(K.indices, dtype=np.int32)
+    data = np.ascontiguousarray(K.data, dtype=np.float64)
+    c = _lib.amg_csr(K.shape[0], K.shape[1], int(indptr[-1]), indptr.ctypes.data_as(C.POINTER(C.c_int64)),
+                     indices.ctypes.data_as(C.POINTER(C.c_int32)), data.ctypes.data_as(C.POINTER(C.c_double)))
+    return c, (indptr, indices, data)
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        import torch
+        if torch.cuda.is_available():
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return C.c_void_p(None)
+    return C.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+class Hierarchy:
+    """amg_setup / amg_pcg_solve / amg_vcycle / amg_level_apply / export / info on one handle."""
+
+    def __init__(self, K, prm: _lib.amg_params | None = None, dist: _lib.amg_dist | None = None):
+        c, keep = _borrow(K)
+        self._h = C.c_void_p()
+        if prm is None:
+            prm = params(2)
+        if not prm.host_only:
+            use_torch_allocator()
+        check(lib().amg_setup(C.byref(c), C.byref(prm), C.byref(dist) if dist is not None else None,
+                              C.byref(self._h)))
+        self.prm = prm
+        del keep
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            lib().amg_hierarchy_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # --- inspection ---------------------------------------------------------------------------
+    def info(self) -> dict:
+        nl = C.c_int64()
+        N = (C.c_int64 * 32)()
+        nnz = (C.c_int64 * 32)()
+        nnzP = (C.c_int64 * 32)()
+        opc = C.c_double()
+        check(lib().amg_hierarchy_info(self._h, C.byref(nl), N, nnz, nnzP, C.byref(opc)))
+        L = nl.value
+        return dict(levels=L, N=list(N[:L]), nnz=list(nnz[:L]), nnz_P=list(nnzP[:L]), opc=opc.value)
+
+    def export(self, level: int) -> dict:
+        Kp, Pp = C.POINTER(_lib.amg_csr)(), C.POINTER(_lib.amg_csr)()
+        ag = C.POINTER(C.c_int32)()
+        dh = C.POINTER(C.c_double)()
+        om = C.c_double()
+        check(lib().amg_hierarchy_export(self._h, level, C.byref(Kp), C.byref(Pp), C.byref(ag), C.byref(dh),
+                                         C.byref(om)))
+        K = _from_c(Kp)
+        n = K.shape[0]
+        out = dict(K=K, P=_from_c(Pp) if Pp else None, omega=om.value)
+        if ag:
+            out["agg"] = np.ctypeslib.as_array(ag, shape=(n,)).copy()
+            lib().amg_free(ag)
+        else:
+            out["agg"] = None
+        out["dhat"] = np.ctypeslib.as_array(dh, shape=(n,)).copy()
+        lib().amg_free(dh)
+        return out
+
+    # --- device solve path ----------------------------------------------------------------------
+    def solve(self, F, u=None, rtol: float = 1e-6, maxit: int = 200, stream=None, history: bool = True):
+        """amg_pcg_solve on device tensors (torch.float64, CUDA).  u: initial guess (updated in place)."""
+        import torch
+        if u is None:
+            u = torch.zeros_like(F)
+        it = C.c_int()
+        rr = C.c_double()
+        hist = np.full(maxit + 1, np.nan) if history else None
+        st = check(lib().amg_pcg_solve(self._h, C.c_void_p(F.data_ptr()), C.c_void_p(u.data_ptr()), rtol, maxit,
+                                       _stream_ptr(stream), C.byref(it), C.byref(rr),
+                                       hist.ctypes.data_as(C.POINTER(C.c_double)) if history else None))
+        return u, it.value, rr.value, (hist[: it.value + 1] if history else None), st
+
+    def solve_host(self, F: np.ndarray, u: np.ndarray | None = None, rtol: float = 1e-6, maxit: int = 200,
+                   stream=None):
+        """amg_pcg_solve_host on host arrays (copies inside the call)."""
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        u = np.zeros_like(F) if u is None else np.ascontiguousarray(u, dtype=np.float64)
+        it = C.c_int()
+        rr = C.c_double()
+        dp = C.POINTER(C.c_double)
+        st = check(lib().amg_pcg_solve_host(self._h, F.ctypes.data_as(dp), u.ctypes.data_as(dp), rtol, maxit,
+                                            _stream_ptr(stream), C.byref(it), C.byref(rr), None))
+        return u, it.value, rr.value, st
+
+    def solve_host_ptr(self, F_ptr: int, u_ptr: int, rtol: float = 1e-6, maxit: int = 200, stream=None):
+        """amg_pcg_solve_host on raw host pointers (e.g. pinned torch tensors)."""
+        it = C.c_int()
+        rr = C.c_double()
+        dp = C.POINTER(C.c_double)
+        st = check(lib().amg_pcg_solve_host(self._h, C.cast(F_ptr, dp), C.cast(u_ptr, dp), rtol, maxit,
+                                            _stream_ptr(stream), C.byref(it), C.byref(rr), None))
+        return it.value, rr.value, st
+
+    def vcycle(self, r, z=None, stream=None):
+        import torch
+        if z is None:
+            z = torch.empty_like(r)
+        check(lib().amg_vcycle(self._h, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), _stream_ptr(stream)))
+        return z
+
+    def apply(self, level: int, op: int, x, y, stream=None):
+        check(lib().amg_level_apply(self._h, level, op, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                    _stream_ptr(stream)))
+        return y
+
+    def set_profiling(self, enable: bool) -> None:
+        check(lib().amg_set_profiling(self._h, int(enable)))
+
+    def kernel_stats(self) -> dict:
+        s = _lib.amg_kernel_stats()
+        check(lib().amg_get_kernel_stats(self._h, C.byref(s)))
+        return dict(launches=s.launches, total_ms=s.total_ms, bytes_per_launch=s.bytes_per_launch,
+                    kernels_launched=s.kernels_launched)

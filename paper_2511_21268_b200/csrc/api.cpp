@@ -1,0 +1,196 @@
+// api.cpp — host-side C-ABI entry points (generator, parameters, setup, export, errors).
+#include <omp.h>
+
+#include <cstdio>
+#include <string>
+
+#include "common.hpp"
+
+namespace amgb {
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+const char *get_error() { return g_err.c_str(); }
+}  // namespace amgb
+
+using namespace amgb;
+
+#define API_BEGIN \
+    try {         \
+        set_error("");
+#define API_END                                                  \
+    }                                                            \
+    catch (const Error &e) {                                     \
+        set_error(e.msg);                                        \
+        return e.st;                                             \
+    }                                                            \
+    catch (const std::bad_alloc &) {                             \
+        set_error("out of host memory");                         \
+        return AMG_ENOMEM;                                       \
+    }                                                            \
+    catch (...) {                                                \
+        set_error("unknown internal error");                     \
+        return AMG_EINVAL;                                       \
+    }
+
+namespace {
+amg_csr *export_csr(const HCsr &A) {
+    amg_csr *c = static_cast<amg_csr *>(std::calloc(1, sizeof(amg_csr)));
+    if (!c) throw Error{AMG_ENOMEM, "host allocation failed"};
+    const int64_t nnz = A.nnz();
+    c->n_rows = A.nrows;
+    c->n_cols = A.ncols;
+    c->nnz = nnz;
+    c->row_ptr = static_cast<int64_t *>(std::malloc(sizeof(int64_t) * (A.nrows + 1)));
+    c->col = static_cast<int32_t *>(std::malloc(sizeof(int32_t) * (nnz > 0 ? nnz : 1)));
+    c->val = static_cast<double *>(std::malloc(sizeof(double) * (nnz > 0 ? nnz : 1)));
+    if (!c->row_ptr || !c->col || !c->val) {
+        amg_csr_free(c);
+        throw Error{AMG_ENOMEM, "host allocation failed"};
+    }
+    std::memcpy(c->row_ptr, A.rp.data(), sizeof(int64_t) * (A.nrows + 1));
+    std::memcpy(c->col, A.ci.data(), sizeof(int32_t) * nnz);
+    std::memcpy(c->val, A.v.data(), sizeof(double) * nnz);
+    return c;
+}
+}  // namespace
+
+extern "C" {
+
+const char *amg_last_error(void) { return get_error(); }
+
+void amg_free(void *p) { std::free(p); }
+
+void amg_csr_free(amg_csr *K) {
+    if (!K) return;
+    std::free(K->row_ptr);
+    std::free(K->col);
+    std::free(K->val);
+    std::free(K);
+}
+
+amg_status amg_iga_tables(int degree, int n_elem, double *mhat, double *khat) {
+    API_BEGIN
+    if (degree < 1 || degree > 8 || n_elem < 1 || !mhat || !khat) throw Error{AMG_EINVAL, "bad argument"};
+    iga_tables_hat(degree, n_elem, mhat, khat);
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_iga_poisson(const amg_iga_desc *d, amg_csr **K, double **F) {
+    API_BEGIN
+    if (!d || !K || !F) throw Error{AMG_EINVAL, "NULL argument"};
+    if (d->dim != 2 && d->dim != 3) throw Error{AMG_EINVAL, "dim must be 2 or 3"};
+    if (d->degree < 1 || d->degree > 8) throw Error{AMG_EINVAL, "degree must be in [1, 8]"};
+    if (d->n_elem < 1) throw Error{AMG_EINVAL, "n_elem must be >= 1"};
+    if (d->dirichlet_sides >> (2 * d->dim)) throw Error{AMG_EINVAL, "dirichlet_sides names a side > 2*dim"};
+    if (d->rhs != 0 && d->rhs != 1) throw Error{AMG_EINVAL, "rhs must be 0 or 1"};
+    HCsr A;
+    Buf<double> f;
+    iga_assemble(*d, A, f);
+    amg_csr *c = export_csr(A);
+    double *fo = static_cast<double *>(std::malloc(sizeof(double) * (A.nrows > 0 ? A.nrows : 1)));
+    if (!fo) {
+        amg_csr_free(c);
+        throw Error{AMG_ENOMEM, "host allocation failed"};
+    }
+    std::memcpy(fo, f.data(), sizeof(double) * A.nrows);
+    *K = c;
+    *F = fo;
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_params_default(amg_params *prm, int p) {
+    API_BEGIN
+    if (!prm || p < 1 || p > 8) throw Error{AMG_EINVAL, "bad argument"};
+    static const int cheb[9] = {0, 2, 4, 8, 12, 14, 16, 16, 16};  // P:L1117 (p>=3); p=2 -> 4 (c.16)
+    prm->agg_steps = 3;
+    prm->smooth_prolong = 1;
+    prm->match_threshold = 1.0;
+    prm->filter_theta = 0.01;
+    prm->cheb_degree = cheb[p];
+    prm->coarse_sweeps = 30;
+    prm->coarse_size = 50;
+    prm->max_levels = 20;
+    prm->format = 0;
+    prm->host_only = 0;
+    prm->num_threads = 0;
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist *dist, amg_hierarchy **Hout) {
+    API_BEGIN
+    if (!K || !Hout || !K->row_ptr || (K->nnz && (!K->col || !K->val))) throw Error{AMG_EINVAL, "NULL argument"};
+    if (K->n_rows < 1 || K->n_rows > INT32_MAX) throw Error{AMG_EINVAL, "n_rows out of range"};
+    amg_params prm;
+    if (prm_in) prm = *prm_in;
+    else amg_params_default(&prm, 2);
+    if (prm.agg_steps < 1 || prm.cheb_degree < 1 || prm.coarse_sweeps < 0 || prm.max_levels < 1 ||
+        prm.coarse_size < 1 || !(prm.filter_theta >= 0.0))
+        throw Error{AMG_EINVAL, "bad parameter"};
+    amg_hierarchy *H = new amg_hierarchy();
+    try {
+        build_hierarchy(*K, prm, H->host);
+        if (!prm.host_only) H->dev = dev_create(H->host, dist);
+    } catch (...) {
+        delete H;
+        throw;
+    }
+    *Hout = H;
+    return AMG_OK;
+    API_END
+}
+
+void amg_hierarchy_free(amg_hierarchy *H) {
+    if (!H) return;
+    if (H->dev) dev_destroy(H->dev);
+    delete H;
+}
+
+amg_status amg_hierarchy_info(const amg_hierarchy *H, int64_t *n_levels, int64_t *N, int64_t *nnz, int64_t *nnz_P,
+                              double *opc) {
+    API_BEGIN
+    if (!H) throw Error{AMG_EINVAL, "NULL hierarchy"};
+    const HHierarchy &h = H->host;
+    if (n_levels) *n_levels = h.nlevels;
+    double tot = 0.0;
+    for (int l = 0; l < h.nlevels; l++) {
+        if (N) N[l] = h.lev[l].N;
+        if (nnz) nnz[l] = h.lev[l].K.nnz();
+        if (nnz_P) nnz_P[l] = (l + 1 < h.nlevels) ? h.lev[l].P.nnz() : 0;
+        tot += (double)h.lev[l].K.nnz();
+    }
+    if (opc) *opc = tot / (double)h.lev[0].K.nnz();
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_hierarchy_export(const amg_hierarchy *H, int level, amg_csr **K_l, amg_csr **P_l,
+                                int32_t **aggregate_of, double **dhat, double *omega) {
+    API_BEGIN
+    if (!H || level < 0 || level >= H->host.nlevels) throw Error{AMG_EINVAL, "bad level"};
+    const HLevel &L = H->host.lev[level];
+    const bool last = level == H->host.nlevels - 1;
+    if (K_l) *K_l = export_csr(L.K);
+    if (P_l) *P_l = last ? nullptr : export_csr(L.P);
+    if (aggregate_of) {
+        if (last) {
+            *aggregate_of = nullptr;
+        } else {
+            *aggregate_of = static_cast<int32_t *>(std::malloc(sizeof(int32_t) * L.N));
+            if (!*aggregate_of) throw Error{AMG_ENOMEM, "host allocation failed"};
+            std::memcpy(*aggregate_of, L.agg.data(), sizeof(int32_t) * L.N);
+        }
+    }
+    if (dhat) {
+        *dhat = static_cast<double *>(std::malloc(sizeof(double) * L.N));
+        if (!*dhat) throw Error{AMG_ENOMEM, "host allocation failed"};
+        std::memcpy(*dhat, L.dhat.data(), sizeof(double) * L.N);
+    }
+    if (omega) *omega = L.omega;
+    return AMG_OK;
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,283 @@
+// iga_gen.cpp — tensor-product B-spline Poisson stiffness generator (the problem source).
+//
+// Paper: P:L69-78 (B-spline basis, open knot vectors, C^{p-1}), P:L551-568 (single-patch Galerkin
+// assembly, k_ij = ∫∇φ_j·∇φ_i), Remark P:L570-573 ((p+1)-point Gauss is exact)
+// (Dirichlet DOFs eliminated), P:L1061-1072 (cube: Dirichlet on sides 1,2,3).
+//
+// Route (c.3/c.4): on the unit square/cube J_F = I, so the stiffness is the Kronecker
+// sum K = K1⊗M1⊗M1 + M1⊗K1⊗M1 + M1⊗M1⊗K1 of 1-D mass/stiffness tables.  The 1-D tables are
+// integrated on the integer-knot vector (h = 1) with (p+1)-point Gauss–Legendre in IEEE binary128
+// (__float128: nodes by Newton on P_{p+1}, basis by the Cox–de Boor triangle) and rounded ONCE to
+// fp64; the binary128 error (~1e-32 relative) is far below half an fp64 ulp, so the rounded tables are
+// the correctly-rounded exact values.  Then M1 = fl(M̂/n), K1 = fl(K̂·n) and every 3-D entry is
+// evaluated as ((K·M)·M + (M·K)·M) + (M·M)·K in that order, without FMA (-ffp-contract=off).
+#include <quadmath.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.hpp"
+
+namespace amgb {
+namespace {
+
+using q128 = __float128;
+
+// Gauss–Legendre nodes/weights on [0,1] in binary128.
+void gauss_legendre_q(int npts, std::vector<q128> &x, std::vector<q128> &w) {
+    x.assign(npts, 0);
+    w.assign(npts, 0);
+    for (int i = 0; i < npts; i++) {
+        q128 z = cosq(M_PIq * (i + 0.75Q) / (npts + 0.5Q));
+        q128 dp = 1;
+        for (int it = 0; it < 100; it++) {
+            q128 p0 = 1, p1 = z;
+            for (int k = 2; k <= npts; k++) {
+                q128 pk = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k;
+                p0 = p1;
+                p1 = pk;
+            }
+            if (npts == 1) { p0 = 1; p1 = z; }
+            dp = npts * (z * p1 - p0) / (z * z - 1);
+            q128 dz = p1 / dp;
+            z -= dz;
+            if (fabsq(dz) < 1e-33Q) break;
+        }
+        // recompute derivative at the converged node
+        q128 p0 = 1, p1 = z;
+        for (int k = 2; k <= npts; k++) {
+            q128 pk = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k;
+            p0 = p1;
+            p1 = pk;
+        }
+        if (npts == 1) { p0 = 1; p1 = z; }
+        dp = npts * (z * p1 - p0) / (z * z - 1);
+        x[i] = (z + 1) / 2;                    // map [-1,1] -> [0,1]
+        w[i] = 1 / ((1 - z * z) * dp * dp);    // 2/((1-z^2)P'^2) halved
+    }
+}
+
+// Knot t_k of the open integer-knot vector on [0, n] (degree p).
+inline int knot(int k, int p, int n) { return std::min(std::max(k - p, 0), n); }
+
+// Non-zero basis functions N_{s-deg..s, deg} at x in span s (The NURBS Book A2.2), binary128.
+void basis_funs(int s, q128 x, int deg, int p, int n, q128 *N) {
+    q128 left[16], right[16];
+    N[0] = 1;
+    for (int j = 1; j <= deg; j++) {
+        left[j] = x - knot(s + 1 - j, p, n);
+        right[j] = knot(s + j, p, n) - x;
+        q128 saved = 0;
+        for (int r = 0; r < j; r++) {
+            q128 tmp = N[r] / (right[r + 1] + left[j - r]);
+            N[r] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        N[j] = saved;
+    }
+}
+
+// Values and first derivatives of the p+1 functions a = s-p..s at x.
+void basis_and_derivs(int s, q128 x, int p, int n, q128 *val, q128 *der) {
+    basis_funs(s, x, p, p, n, val);
+    q128 low[16];
+    if (p == 0) { der[0] = 0; return; }
+    basis_funs(s, x, p - 1, p, n, low);  // N_{s-p+1..s, p-1}
+    for (int k = 0; k <= p; k++) {
+        int a = s - p + k;
+        q128 d = 0;
+        if (k >= 1) {  // N_{a,p-1} is low[k-1]
+            int den = knot(a + p, p, n) - knot(a, p, n);
+            if (den) d += p * low[k - 1] / den;
+        }
+        if (k <= p - 1) {  // N_{a+1,p-1} is low[k]
+            int den = knot(a + p + 1, p, n) - knot(a + 1, p, n);
+            if (den) d -= p * low[k] / den;
+        }
+        der[k] = d;
+    }
+}
+
+struct Tables1D {
+    int p = 0, n = 0, m = 0;
+    std::vector<double> M, K;  // band (m x (2p+1)), physical (scaled) tables
+};
+
+void hat_tables_q(int p, int n, std::vector<q128> &Mq, std::vector<q128> &Kq) {
+    const int m = n + p, bw = 2 * p + 1;
+    Mq.assign((size_t)m * bw, 0);
+    Kq.assign((size_t)m * bw, 0);
+    std::vector<q128> gx, gw;
+    gauss_legendre_q(p + 1, gx, gw);
+    q128 val[16], der[16];
+    for (int e = 0; e < n; e++) {
+        int s = e + p;
+        for (int g = 0; g <= p; g++) {
+            basis_and_derivs(s, e + gx[g], p, n, val, der);
+            for (int i = 0; i <= p; i++)
+                for (int j = 0; j <= p; j++) {
+                    int a = e + i, b = e + j;
+                    Mq[(size_t)a * bw + (b - a + p)] += gw[g] * val[i] * val[j];
+                    Kq[(size_t)a * bw + (b - a + p)] += gw[g] * der[i] * der[j];
+                }
+        }
+    }
+}
+
+// Round to fp64; values that are zero up to the binary128 integration error become exactly 0
+// (exact non-zero entries are rationals of magnitude >> 1e-25 for p <= 8).
+double round_q(q128 v, q128 scale) {
+    if (fabsq(v) < 1e-25Q * scale) return 0.0;
+    return (double)v;
+}
+
+void hat_tables(int p, int n, double *mhat, double *khat) {
+    std::vector<q128> Mq, Kq;
+    hat_tables_q(p, n, Mq, Kq);
+    q128 sm = 0, sk = 0;
+    for (auto v : Mq) sm = fmaxq(sm, fabsq(v));
+    for (auto v : Kq) sk = fmaxq(sk, fabsq(v));
+    for (size_t i = 0; i < Mq.size(); i++) {
+        mhat[i] = round_q(Mq[i], sm);
+        khat[i] = round_q(Kq[i], sk);
+    }
+}
+
+Tables1D physical_tables(int p, int n) {
+    Tables1D t;
+    t.p = p; t.n = n; t.m = n + p;
+    const size_t sz = (size_t)t.m * (2 * p + 1);
+    std::vector<double> mh(sz), kh(sz);
+    hat_tables(p, n, mh.data(), kh.data());
+    t.M.resize(sz);
+    t.K.resize(sz);
+    const double dn = (double)n;
+    for (size_t i = 0; i < sz; i++) {
+        t.M[i] = mh[i] / dn;  // M1 = fl(M̂/n)
+        t.K[i] = kh[i] * dn;  // K1 = fl(K̂·n)
+    }
+    return t;
+}
+
+// 1-D load factors F_ax[a] = ∫_0^1 g_ax(x) N_a(x) dx, g = sin(πx), sin(πy/2), cos(πz) (c.5).
+std::vector<double> load_factor(int ax, int p, int n) {
+    const int m = n + p;
+    std::vector<q128> F(m, 0);
+    std::vector<q128> gx, gw;
+    gauss_legendre_q(p + 1, gx, gw);
+    q128 val[16], der[16];
+    for (int e = 0; e < n; e++) {
+        for (int g = 0; g <= p; g++) {
+            basis_and_derivs(e + p, e + gx[g], p, n, val, der);
+            q128 x = (e + gx[g]) / n;
+            q128 f = ax == 0 ? sinq(M_PIq * x) : ax == 1 ? sinq(M_PIq * x / 2) : cosq(M_PIq * x);
+            for (int i = 0; i <= p; i++) F[e + i] += gw[g] / n * f * val[i];
+        }
+    }
+    std::vector<double> out(m);
+    for (int a = 0; a < m; a++) out[a] = (double)F[a];
+    return out;
+}
+
+}  // namespace
+
+void iga_tables_hat(int p, int n, double *mhat, double *khat) { hat_tables(p, n, mhat, khat); }
+
+void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
+    const int dim = d.dim, p = d.degree, n = d.n_elem, m = n + p, bw = 2 * p + 1;
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, nf[3] = {1, 1, 1};
+    for (int ax = 0; ax < dim; ax++) {
+        lo[ax] = (d.dirichlet_sides >> (2 * ax)) & 1u ? 1 : 0;
+        hi[ax] = m - 1 - ((d.dirichlet_sides >> (2 * ax + 1)) & 1u ? 1 : 0);
+        nf[ax] = hi[ax] - lo[ax] + 1;
+        if (nf[ax] < 1) throw Error{AMG_EINVAL, "no free DOFs along an axis"};
+    }
+    const int64_t N = (int64_t)nf[0] * nf[1] * nf[2];
+    if (N > INT32_MAX) throw Error{AMG_EINVAL, "more than 2^31-1 free DOFs (int32 columns)"};
+    const Tables1D T = physical_tables(p, n);
+    const double *M1 = T.M.data(), *K1 = T.K.data();
+
+    // per-axis column window [l, h] of function x
+    auto win = [&](int ax, int x, int &l, int &h) {
+        l = std::max(x - p, lo[ax]);
+        h = std::min(x + p, hi[ax]);
+    };
+    K.nrows = K.ncols = N;
+    K.rp.alloc(N + 1);
+    K.rp[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < N; row++) {
+        int a = lo[0] + (int)(row % nf[0]);
+        int b = lo[1] + (int)((row / nf[0]) % nf[1]);
+        int c = lo[2] + (int)(row / ((int64_t)nf[0] * nf[1]));
+        int l, h;
+        int64_t cnt = 1;
+        win(0, a, l, h); cnt *= h - l + 1;
+        win(1, b, l, h); cnt *= h - l + 1;
+        if (dim == 3) { win(2, c, l, h); cnt *= h - l + 1; }
+        K.rp[row + 1] = cnt;
+    }
+    for (int64_t r = 0; r < N; r++) K.rp[r + 1] += K.rp[r];
+    const int64_t nnz = K.rp[N];
+    K.ci.alloc(nnz);
+    K.v.alloc(nnz);
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < N; row++) {
+        const int a = lo[0] + (int)(row % nf[0]);
+        const int b = lo[1] + (int)((row / nf[0]) % nf[1]);
+        const int c = lo[2] + (int)(row / ((int64_t)nf[0] * nf[1]));
+        int al, ah, bl, bh, cl = c, ch = c;
+        win(0, a, al, ah);
+        win(1, b, bl, bh);
+        if (dim == 3) win(2, c, cl, ch);
+        int64_t k = K.rp[row];
+        for (int c2 = cl; c2 <= ch; c2++) {
+            const double Mc = dim == 3 ? M1[(size_t)c * bw + (c2 - c + p)] : 1.0;
+            const double Kc = dim == 3 ? K1[(size_t)c * bw + (c2 - c + p)] : 0.0;
+            for (int b2 = bl; b2 <= bh; b2++) {
+                const double Mb = M1[(size_t)b * bw + (b2 - b + p)];
+                const double Kb = K1[(size_t)b * bw + (b2 - b + p)];
+                const int64_t base = (int64_t)nf[0] * ((b2 - lo[1]) + (int64_t)nf[1] * (c2 - lo[2])) - lo[0];
+                for (int a2 = al; a2 <= ah; a2++) {
+                    const double Ma = M1[(size_t)a * bw + (a2 - a + p)];
+                    const double Ka = K1[(size_t)a * bw + (a2 - a + p)];
+                    double val;
+                    if (dim == 3) {
+                        const double t1 = (Ka * Mb) * Mc;
+                        const double t2 = (Ma * Kb) * Mc;
+                        const double t3 = (Ma * Mb) * Kc;
+                        val = (t1 + t2) + t3;
+                    } else {
+                        const double t1 = Ka * Mb;
+                        const double t2 = Ma * Kb;
+                        val = t1 + t2;
+                    }
+                    K.ci[k] = (int32_t)(base + a2);
+                    K.v[k] = val;
+                    k++;
+                }
+            }
+        }
+    }
+    // load vector (c.5)
+    F.alloc(N);
+    if (d.rhs == 1) {
+        std::memset(F.data(), 0, sizeof(double) * N);
+        return;
+    }
+    std::vector<double> f1[3];
+    for (int ax = 0; ax < dim; ax++) f1[ax] = load_factor(ax, p, n);
+    const double cfac = (dim == 2 ? 5.0 : 9.0) * M_PI * M_PI / 4.0;
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < N; row++) {
+        int a = lo[0] + (int)(row % nf[0]);
+        int b = lo[1] + (int)((row / nf[0]) % nf[1]);
+        int c = lo[2] + (int)(row / ((int64_t)nf[0] * nf[1]));
+        double v = f1[0][a] * f1[1][b];
+        if (dim == 3) v *= f1[2][c];
+        F[row] = cfac * v;
+    }
+}
+
+}  // namespace amgb

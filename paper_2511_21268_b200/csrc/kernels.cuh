@@ -1,0 +1,328 @@
+// kernels.cuh — hand-written sm_100a fp64 kernels of the solve phase.
+//
+// The whole solve phase is HBM-bandwidth bound (≈0.17 flop/B): every kernel below is a streaming
+// kernel; no tensor cores (nothing here is a dense contraction).  Matrix streams (values + column
+// indices) are ≈99% of the algorithmic bytes, so the design goal is full-rate, coalesced, 128-bit
+// streaming of the CSR arrays with the x-gathers served from L1/L2, and every vector update fused
+// into the epilogue of the SpMV that produces it.
+//
+// Matrix layout on the device ("CSR2"): each row padded to an even length with (col = a valid column,
+// val = 0.0), so that every row starts 16-byte aligned and is read as double2 values + int2 columns.
+// One warp owns a group of G consecutive rows: it reduces one row at a time across its 32 lanes
+// (warp-shuffle tree) and parks row t's sum in lane t; the epilogue then runs on G lanes at once, so
+// epilogue vector traffic is coalesced (G = 32 on the large levels).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace amgb {
+namespace dev {
+
+constexpr int kBlock = 256;
+
+struct Scalars {
+    double ff;       // F·F
+    double rr;       // r·r (after the CG update)
+    double pq;       // pᵀKp
+    double rho;      // rᵀz (current)
+    double rho_new;  // rᵀz (new)
+    double alpha;    // ρ/(pᵀq)
+    double beta;     // ρ_new/ρ
+    int flags;       // bit0: pᵀq <= 0, bit1: rᵀz <= 0
+    int pad;
+};
+
+enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ_INIT, DOT_RZ };
+
+struct DotCtx {
+    double *partials;    // >= gridDim.x
+    unsigned *counter;   // zero between launches
+    Scalars *S;
+    int kind;
+};
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// Deterministic block reduction + "last block finalises" (fixed partial order ⇒ run-to-run
+// identical scalars; no atomics on values).
+__device__ __forceinline__ void block_dot_finalize(double v, const DotCtx &dc) {
+    __shared__ double red[kBlock / 32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < kBlock / 32 ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) {
+            dc.partials[blockIdx.x] = t;
+            __threadfence();
+            unsigned ticket = atomicAdd(dc.counter, 1u);
+            last = (ticket == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += kBlock) t += __ldcg(dc.partials + i);
+    t = warp_sum(t);
+    if (lane == 0) red[wid] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kBlock / 32; w++) s += red[w];
+        Scalars *S = dc.S;
+        switch (dc.kind) {
+            case DOT_FF: S->ff = s; break;
+            case DOT_RR: S->rr = s; break;
+            case DOT_PQ:
+                S->pq = s;
+                S->alpha = S->rho / s;
+                if (!(s > 0.0)) S->flags |= 1;
+                break;
+            case DOT_RZ_INIT:
+                S->rho = s;
+                if (!(s > 0.0)) S->flags |= 2;
+                break;
+            case DOT_RZ:
+                S->rho_new = s;
+                S->beta = s / S->rho;
+                S->rho = s;
+                if (!(s > 0.0)) S->flags |= 2;
+                break;
+            default: break;
+        }
+        *dc.counter = 0u;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Epilogues.  operator()(row, s) consumes the row sum s = (A·g)_row and returns the row's
+// contribution to the fused dot product (ignored unless kDot).
+// ------------------------------------------------------------------------------------------------
+struct EpiStore {  // y = A x
+    static constexpr bool kDot = false;
+    double *y;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const { y[i] = s; return 0.0; }
+};
+
+struct EpiSpmvDot {  // a1: q = K p, pᵀq
+    static constexpr bool kDot = true;
+    const double *p;
+    double *q;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        q[i] = s;
+        return p[i] * s;
+    }
+};
+
+struct EpiResidualFrom {  // r = b − K x  (also: r −= K d with b == r);  optionally x = dpend
+    static constexpr bool kDot = false;
+    const double *b;
+    double *r;
+    const double *dpend;  // nullable: x = dpend (degree-1 pre-smoothing)
+    double *x;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        r[i] = b[i] - s;
+        if (dpend) x[i] = dpend[i];
+        return 0.0;
+    }
+};
+
+// a4/a10: fused Chebyshev step (Lottes 4th kind, ρ = 1; SURVEY c.16):
+//   r = rin − K d_old;  d_new = a·d_old + bc·(r·invd);  x = ((xin or 0) + dpend) + d_new.
+template <bool kDotRZ>
+struct EpiCheb {
+    static constexpr bool kDot = kDotRZ;
+    const double *rin;
+    double *rout;
+    const double *dold;
+    double *dnew;
+    const double *invd;
+    const double *xin;    // nullable (x = 0 on entry)
+    const double *dpend;  // nullable (pending d_0 not yet added to x)
+    double *xout;
+    const double *bdot;   // kDotRZ: returns bdot[i]·x_new[i]
+    double a, bc;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        const double r = rin[i] - s;
+        const double dn = a * dold[i] + bc * (r * invd[i]);
+        double x = xin ? xin[i] : 0.0;
+        if (dpend) x = x + dpend[i];
+        x = x + dn;
+        rout[i] = r;
+        dnew[i] = dn;
+        xout[i] = x;
+        return kDotRZ ? bdot[i] * x : 0.0;
+    }
+};
+
+struct EpiPostFirst {  // a9: r = b − K x;  d0 = c0·(r·invd)  (x += d0 is folded into the next step)
+    static constexpr bool kDot = false;
+    const double *b;
+    double *r;
+    const double *invd;
+    double *d0;
+    double c0;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        const double rr = b[i] - s;
+        r[i] = rr;
+        d0[i] = c0 * (rr * invd[i]);
+        return 0.0;
+    }
+};
+
+struct EpiRestrict {  // a6 (+a3 of the coarse level): b_c = R r;  d0_c = c0·(b_c·invd_c)
+    static constexpr bool kDot = false;
+    double *bc;
+    const double *invd;  // nullable (coarsest level: no smoother)
+    double *d0;
+    double c0;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        bc[i] = s;
+        if (invd) d0[i] = c0 * (s * invd[i]);
+        return 0.0;
+    }
+};
+
+struct EpiProlong {  // a8: x += P̄ e
+    static constexpr bool kDot = false;
+    double *x;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        x[i] = x[i] + s;
+        return 0.0;
+    }
+};
+
+// ------------------------------------------------------------------------------------------------
+// The streaming CSR2 core: warp per group of G rows, 128-bit loads, 2 row chunks in flight per lane.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int2 ld_stream(const int2 *p) {
+    int2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
+template <int G, class Epi>
+__global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp, const int2 *__restrict__ ci2,
+                                                 const double2 *__restrict__ v2, const double *__restrict__ g,
+                                                 int64_t nrows, Epi epi, DotCtx dc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t ngroups = (nrows + G - 1) / G;
+    double dacc = 0.0;
+    for (int64_t grp = warp; grp < ngroups; grp += nwarps) {
+        const int64_t r0 = grp * G;
+        const int nr = (int)(nrows - r0 < (int64_t)G ? nrows - r0 : (int64_t)G);
+        double mine = 0.0;
+        for (int t = 0; t < nr; t++) {
+            const int64_t row = r0 + t;
+            const int64_t b = __ldg(rp + row) >> 1, e = __ldg(rp + row + 1) >> 1;
+            double s0 = 0.0, s1 = 0.0;
+            int64_t k = b + lane;
+            for (; k + 32 < e; k += 64) {
+                const double2 va = ld_stream(v2 + k);
+                const int2 ca = ld_stream(ci2 + k);
+                const double2 vb = ld_stream(v2 + k + 32);
+                const int2 cb = ld_stream(ci2 + k + 32);
+                s0 = fma(va.x, __ldg(g + ca.x), s0);
+                s1 = fma(va.y, __ldg(g + ca.y), s1);
+                s0 = fma(vb.x, __ldg(g + cb.x), s0);
+                s1 = fma(vb.y, __ldg(g + cb.y), s1);
+            }
+            if (k < e) {
+                const double2 va = ld_stream(v2 + k);
+                const int2 ca = ld_stream(ci2 + k);
+                s0 = fma(va.x, __ldg(g + ca.x), s0);
+                s1 = fma(va.y, __ldg(g + ca.y), s1);
+            }
+            const double s = warp_sum(s0 + s1);
+            if (lane == t) mine = s;
+        }
+        if (lane < nr) dacc += epi(r0 + lane, mine);
+    }
+    if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Elementwise / reduction kernels (grid-stride, fused)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_cheb_first(int64_t n, const double *__restrict__ b,
+                                                        const double *__restrict__ invd, double *__restrict__ d0,
+                                                        double c0) {
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        d0[i] = c0 * (b[i] * invd[i]);
+}
+
+__global__ void __launch_bounds__(kBlock) k_axpy1(int64_t n, const double *__restrict__ d, double *__restrict__ x) {
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        x[i] = x[i] + d[i];
+}
+
+// dot(a, b) -> scalar of kind dc.kind
+__global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+                                                 DotCtx dc) {
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        s += a[i] * b[i];
+    block_dot_finalize(s, dc);
+}
+
+// a2: u += α p; r −= α q; ‖r‖² (α from device scalars, computed by the spmv_dot last block)
+__global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *__restrict__ p,
+                                                        const double *__restrict__ q, double *__restrict__ u,
+                                                        double *__restrict__ r, DotCtx dc) {
+    const double alpha = dc.S->alpha;
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        u[i] = u[i] + alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        s += ri * ri;
+    }
+    block_dot_finalize(s, dc);
+}
+
+// a11: p = z + β p  (first: p = z)
+__global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__restrict__ z, double *__restrict__ p,
+                                                      const Scalars *__restrict__ S, int first) {
+    const double beta = first ? 0.0 : S->beta;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        p[i] = first ? z[i] : z[i] + beta * p[i];
+}
+
+// a7: coarsest level, `sweeps` ℓ1-Jacobi sweeps from x = 0, one CTA, x double-buffered in shared memory.
+__global__ void __launch_bounds__(1024) k_coarse_solve(int n, const int64_t *__restrict__ rp,
+                                                        const int *__restrict__ ci, const double *__restrict__ v,
+                                                        const double *__restrict__ invd, const double *__restrict__ b,
+                                                        double *__restrict__ x, int sweeps) {
+    extern __shared__ double sm[];
+    double *xa = sm, *xb = sm + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) xa[i] = 0.0;
+    __syncthreads();
+    for (int s = 0; s < sweeps; s++) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double t = 0.0;
+            for (int64_t k = rp[i]; k < rp[i + 1]; k++) t = fma(v[k], xa[ci[k]], t);
+            xb[i] = xa[i] + (b[i] - t) * invd[i];
+        }
+        __syncthreads();
+        double *tmp = xa; xa = xb; xb = tmp;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xa[i];
+}
+
+}  // namespace dev
+}  // namespace amgb

@@ -1,0 +1,170 @@
+"""GPU parity of the CUDA solve path against the oracle (element by element), through the C ABI.
+
+Tolerances: device sums run in a different order than the oracle's sequential ones and
+use FMA, so operator applications agree to a few ulps of Σ|a_ij x_j| (checked at 1e-13 relative to
+that bound), one V-cycle to 1e-12 relative (max-norm), the PCG solution after the same number of
+iterations to 1e-10 relative, and PCG iteration counts at rtol 1e-6 within ±1 (north star).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import bspline
+import amg_inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _amg():
+    import paper_2511_21268_b200 as amg
+    return amg
+
+
+CASES = {
+    "C1": (2, 2, 16),
+    "cube12p3": (3, 3, 12),
+    "C2": (3, 2, 32),
+    "cube10p4": (3, 4, 10),
+}
+
+_cache = {}
+
+
+def build(case, **kw):
+    key = (case, tuple(sorted(kw.items())))
+    if key not in _cache:
+        amg = _amg()
+        dim, p, n = CASES[case]
+        K, F = amg.iga_poisson(dim, p, n)
+        H = amg.Hierarchy(K, amg.params(p, **kw))
+        Ho = oracle.setup(K.to_scipy(), oracle.OParams.for_degree(p, **kw))
+        _cache[key] = (K.to_scipy(), F, H, Ho)
+    return _cache[key]
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_level_operators(case):
+    """K_l, P̄_l and R_l applied on the device vs the oracle's sequential SpMV, every level."""
+    K, F, H, Ho = build(case)
+    rng = np.random.default_rng(1)
+    for l, L in enumerate(Ho.levels):
+        ops = [(0, L.K)] + ([] if L.P is None else [(1, L.P), (2, L.R)])
+        for op, A in ops:
+            x = rng.uniform(-1, 1, A.shape[1])
+            y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+            H.apply(l, op, dev(x), y)
+            ref = oracle.spmv(A, x)
+            bound = abs(A) @ np.abs(x)
+            assert np.all(np.abs(y.cpu().numpy() - ref) <= 1e-13 * bound + 1e-300), (l, op)
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_vcycle(case):
+    """One V-cycle (c.18: Chebyshev pre/post smoothing, restriction, coarse solve, prolongation)."""
+    K, F, H, Ho = build(case)
+    for seed in (3, 4):
+        r = amg_inputs.uniform_pm1(K.shape[0], seed=seed)
+        z = H.vcycle(dev(r)).cpu().numpy()
+        zo = oracle.vcycle(Ho, r)
+        assert np.abs(z - zo).max() <= 1e-12 * np.abs(zo).max()
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_pcg_fixed_iterations_and_counts(case):
+    """c.19: same iterate after the same number of iterations (1e-10), and iteration counts at
+    rtol 1e-6 equal within ±1, for the manufactured RHS and a seeded random RHS."""
+    K, F, H, Ho = build(case)
+    for rhs in (F, amg_inputs.uniform_pm1(K.shape[0])):
+        uo, ito, rro, histo, rco = oracle.pcg(Ho, rhs, rtol=1e-6, maxit=200)
+        assert rco == 0
+        u, it, rr, hist, st = H.solve(dev(rhs), rtol=1e-6, maxit=200)
+        assert st == 0 and abs(it - ito) <= 1
+        assert rr <= 1e-6
+        u2, it2, _, hist2, _ = H.solve(dev(rhs), rtol=0.0, maxit=ito)
+        assert it2 == ito
+        uo_n = np.linalg.norm(uo)
+        assert np.linalg.norm(u2.cpu().numpy() - uo) <= 1e-10 * uo_n
+        assert np.allclose(hist2, histo, rtol=1e-8, atol=0)
+        # true residual of the converged device solution
+        ud = u.cpu().numpy()
+        assert np.linalg.norm(rhs - oracle.spmv(K, ud)) <= 1.05e-6 * np.linalg.norm(rhs)
+
+
+def test_host_pointer_entry_matches_device_entry():
+    K, F, H, Ho = build("C2")
+    u_dev, it, rr, _, _ = H.solve(dev(F))
+    u_host, it2, rr2, _ = H.solve_host(F)
+    assert it == it2 and np.array_equal(u_dev.cpu().numpy(), u_host)
+
+
+def test_deterministic_runs():
+    K, F, H, Ho = build("cube12p3")
+    a = H.solve(dev(F))[0].cpu().numpy()
+    b = H.solve(dev(F))[0].cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_edge_cases():
+    amg = _amg()
+    K, F, H, Ho = build("C1")
+    # F = 0 -> u = 0, 0 iterations
+    u, it, rr, hist, st = H.solve(torch.zeros(K.shape[0], dtype=torch.float64, device="cuda"))
+    assert it == 0 and st == 0 and not u.any()
+    # maxit = 0 -> not converged, u unchanged (0)
+    u, it, rr, hist, st = H.solve(dev(F), maxit=0)
+    assert it == 0 and st == 1 and not u.any()
+    # nonzero initial guess: start from the exact-ish solution -> converges immediately
+    uo = oracle.pcg(Ho, F, rtol=1e-12)[0]
+    u, it, rr, hist, st = H.solve(dev(F), u=dev(uo), rtol=1e-6)
+    assert it == 0 and st == 0
+    # single-level hierarchy (N <= coarse_size): V = 30 ℓ1-Jacobi sweeps
+    Ks, Fs = amg.iga_poisson(2, 2, 4)
+    Hs = amg.Hierarchy(Ks, amg.params(2, coarse_size=1000))
+    Hso = oracle.setup(Ks.to_scipy(), oracle.OParams.for_degree(2, coarse_size=1000))
+    assert Hs.info()["levels"] == 1
+    r = amg_inputs.uniform_pm1(Ks.shape[0], seed=7)
+    assert np.abs(Hs.vcycle(dev(r)).cpu().numpy() - oracle.vcycle(Hso, r)).max() <= 1e-12 * np.abs(r).max()
+    # degree-1 smoother and odd degree paths
+    for m in (1, 3):
+        Km, Fm = amg.iga_poisson(3, 2, 8)
+        Hm = amg.Hierarchy(Km, amg.params(2, cheb_degree=m))
+        Hmo = oracle.setup(Km.to_scipy(), oracle.OParams(cheb_degree=m))
+        r = amg_inputs.uniform_pm1(Km.shape[0], seed=8)
+        zo = oracle.vcycle(Hmo, r)
+        assert np.abs(Hm.vcycle(dev(r)).cpu().numpy() - zo).max() <= 1e-12 * np.abs(zo).max()
+
+
+def test_c3_full_size_properties():
+    """C3 (k=96, p=3; 941,094 DOFs) in the bench's configuration: hierarchy identical to the host
+    export, level-0 SpMV vs the oracle on all rows, V-cycle symmetry, converged true residual."""
+    amg = _amg()
+    K, F = amg.iga_poisson(3, 3, 96)
+    Ks = K.to_scipy()
+    H = amg.Hierarchy(K, amg.params(3))
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, Ks.shape[0])
+    y = torch.empty(Ks.shape[0], dtype=torch.float64, device="cuda")
+    H.apply(0, 0, dev(x), y)
+    ref = oracle.spmv(Ks, x)
+    assert np.all(np.abs(y.cpu().numpy() - ref) <= 1e-13 * (abs(Ks) @ np.abs(x)))
+    r1 = dev(amg_inputs.uniform_pm1(Ks.shape[0], seed=1))
+    r2 = dev(amg_inputs.uniform_pm1(Ks.shape[0], seed=2))
+    a = torch.dot(H.vcycle(r1), r2).item()
+    b = torch.dot(r1, H.vcycle(r2)).item()
+    assert abs(a - b) <= 1e-11 * abs(a)
+    u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6)
+    assert st == 0 and 5 <= it <= 40
+    ud = u.cpu().numpy()
+    assert np.linalg.norm(F - oracle.spmv(Ks, ud)) <= 1.05e-6 * np.linalg.norm(F)

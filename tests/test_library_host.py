@@ -1,0 +1,126 @@
+"""CPU tests of the product library's host side: C-ABI symbols, error behaviour, and BITWISE parity of
+the generator and the hierarchy setup with the oracle (DESIGN.md §3 canonical arithmetic contract).
+
+The library and the oracle share no code; both follow the readings c.1-c.15.  The oracle is pinned
+separately (tests/test_oracle_*.py)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import tables
+import paper_2511_21268_b200 as amg
+from paper_2511_21268_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "amg_b200.h")).read()
+    declared = set(re.findall(r"\b(amg_[a-z_]+)\s*\(", hdr)) - {"amg_alloc_fn", "amg_free_fn"}
+    declared = {d for d in declared if not d.endswith("_fn")}
+    L = _lib.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert declared == set(_lib.EXPORTED)
+
+
+def test_errors_are_reported_not_raised_through_abi():
+    d = _lib.amg_iga_desc(4, 2, 8, 7, 0)
+    Kp = C.POINTER(_lib.amg_csr)()
+    Fp = C.POINTER(C.c_double)()
+    st = _lib.lib().amg_iga_poisson(C.byref(d), C.byref(Kp), C.byref(Fp))
+    assert st == -1 and b"dim" in _lib.lib().amg_last_error()
+    with pytest.raises(amg.AmgError):
+        amg.params(0)
+    # non-symmetric K is rejected
+    import scipy.sparse as sp
+    A = sp.csr_matrix(np.array([[2.0, -1.0], [-0.5, 2.0]]))
+    with pytest.raises(amg.AmgError, match="symmetric"):
+        amg.Hierarchy(A, amg.params(2, host_only=1))
+    # non-positive diagonal
+    A = sp.csr_matrix(np.array([[0.0, -1.0], [-1.0, 2.0]]))
+    with pytest.raises(amg.AmgError, match="ENOTSPD"):
+        amg.Hierarchy(A, amg.params(2, host_only=1))
+
+
+def test_solve_without_device_part_fails_loudly():
+    K, F = amg.iga_poisson(2, 2, 4)
+    H = amg.Hierarchy(K.to_scipy(), amg.params(2, host_only=1))
+    with pytest.raises(amg.AmgError, match="ENODEV"):
+        H.solve_host(F)
+
+
+@pytest.mark.parametrize("p,n", [(1, 7), (2, 16), (3, 12), (4, 9), (5, 11), (6, 20)])
+def test_tables_bitwise_equal_exact_rationals(p, n):
+    """c.3: binary128 Gauss + one rounding == correctly rounded exact rationals, every entry."""
+    M, K = amg.iga_tables(p, n)
+    Mo, Ko = tables.hat_tables(p, n)
+    assert np.array_equal(M, Mo) and np.array_equal(K, Ko)
+
+
+def _bitwise(a, b):
+    return (a.shape == b.shape and np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+            and np.array_equal(a.data.view(np.uint64), b.data.view(np.uint64)))
+
+
+@pytest.mark.parametrize("dim,p,n,sides", [(2, 2, 16, 7), (3, 2, 8, 7), (3, 3, 12, 7), (3, 4, 6, 7),
+                                           (3, 2, 5, 0), (3, 3, 4, 0b111111), (2, 1, 9, 0b1010)])
+def test_generator_bitwise(dim, p, n, sides):
+    """c.4: the library's K is bitwise the oracle's; the load vectors agree to 1e-14 (c.5)."""
+    K, F = amg.iga_poisson(dim, p, n, sides)
+    Ko = oracle.assemble(dim, p, n, sides)
+    assert _bitwise(K.to_scipy(), Ko)
+    if sides == 7:
+        from oracle import bspline
+        Fo = bspline.load_vector(dim, p, n, sides)
+        assert np.abs(F - Fo).max() <= 1e-14 * np.abs(Fo).max()
+
+
+def _compare_hierarchies(H, Ho):
+    info = H.info()
+    assert info["N"] == [L.N for L in Ho.levels]
+    for l, Lo in enumerate(Ho.levels):
+        e = H.export(l)
+        assert _bitwise(e["K"].to_scipy(), Lo.K), f"K_{l}"
+        assert np.array_equal(e["dhat"], Lo.dhat), f"dhat_{l}"
+        if Lo.P is None:
+            assert e["P"] is None and e["agg"] is None
+        else:
+            assert np.array_equal(e["agg"], Lo.agg), f"aggregates_{l}"
+            assert _bitwise(e["P"].to_scipy(), Lo.P), f"P_{l}"
+            assert e["omega"] == Lo.omega
+    assert info["opc"] == pytest.approx(Ho.opc(), rel=1e-15)
+
+
+@pytest.mark.parametrize("dim,p,n,kw", [
+    (2, 2, 16, {}),                                  # C1
+    (3, 3, 12, {}),
+    (3, 2, 32, {}),                                  # C2
+    (3, 4, 10, {}),
+    (3, 3, 12, dict(filter_theta=0.0)),              # literal (I − ωD⁻¹K)P
+    (3, 2, 10, dict(smooth_prolong=0)),              # unsmoothed
+    (3, 2, 10, dict(agg_steps=1, coarse_size=20)),   # pairwise aggregation, deeper hierarchy
+    (3, 3, 8, dict(match_threshold=0.0)),            # maximal matching eligibility
+])
+def test_setup_bitwise_vs_oracle(dim, p, n, kw):
+    """c.6-c.15: aggregate maps, patterns AND values of every level bitwise equal to the oracle."""
+    K, _ = amg.iga_poisson(dim, p, n)
+    prm = amg.params(p, host_only=1, **kw)
+    H = amg.Hierarchy(K, prm)
+    okw = {k: v for k, v in kw.items()}
+    Ho = oracle.setup(oracle.assemble(dim, p, n), oracle.OParams.for_degree(p, **okw))
+    _compare_hierarchies(H, Ho)
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+def test_setup_independent_of_thread_count(threads):
+    K, _ = amg.iga_poisson(3, 2, 12)
+    ref = amg.Hierarchy(K, amg.params(2, host_only=1))
+    H = amg.Hierarchy(K, amg.params(2, host_only=1, num_threads=threads))
+    for l in range(ref.info()["levels"]):
+        a, b = ref.export(l), H.export(l)
+        assert _bitwise(a["K"].to_scipy(), b["K"].to_scipy())
