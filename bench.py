@@ -148,7 +148,7 @@ def run_gpu(args) -> None:
     K, F = amg.iga_poisson(dim, p, n)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    H = amg.Hierarchy(K, amg.params(p))
+    H = amg.Hierarchy(K, amg.params(p, format=args.format))
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     info = H.info()
@@ -241,7 +241,7 @@ def run_gpu(args) -> None:
                 "workload": f"{args.config}: {dim}-D Poisson, B-spline p={p}, n={n} elements/dir, "
                             f"{N} free DOFs, AMG-PCG rtol {args.rtol}",
                 "dofs": N, "nnz_K0": info["nnz"][0], "levels": info["levels"], "level_N": info["N"],
-                "opc": round(info["opc"], 4), "cheb_degree": m, "coarse_sweeps": 30,
+                "opc": round(info["opc"], 4), "cheb_degree": m, "coarse_sweeps": 30, "format": args.format,
                 "parallelism": "replicas" if world > 1 else "single",
                 "l2": "inputs exceed L2 (K0 = %.2f GB >> 126 MB); no flush needed" % (12e-9 * info["nnz"][0]),
             },
@@ -356,6 +356,7 @@ def main():
     ap.add_argument("--maxit", type=int, default=200)
     ap.add_argument("--ref-iters", type=int, default=15, help="iteration count the reference arm scales to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--format", type=int, default=0, help="0 auto, 1 CSR2, 2 SELL2")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -39,9 +39,14 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// A device operator in one of two streaming formats (kernels.cuh):
+//   CSR2 (fmt 0): rows padded to even length; warp per group of G rows.
+//   SELL2 (fmt 1): 32-row slices, one row per lane, pair-interleaved columns; soff = slice offsets.
 struct DCsr {
-    int64_t nrows = 0, ncols = 0, nnz2 = 0;  // nnz2: padded entries (even per row)
-    int64_t *rp = nullptr;
+    int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
+    int fmt = 0;
+    int64_t *rp = nullptr;    // CSR2 row pointers (entries)
+    int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
     int32_t *ci = nullptr;
     double *v = nullptr;
     int G = 32;
@@ -114,9 +119,14 @@ int choose_G(int64_t nrows) {
     return G;
 }
 
-// Upload a host CSR as CSR2 (rows padded to even length; pad = (first column of the row or the
-// diagonal for square matrices, 0.0)).
-void upload_csr(DevState &D, const HCsr &A, DCsr &out, bool square) {
+// Pad column of row i: the diagonal for square operators, else the row's first column.
+inline int32_t pad_col(const HCsr &A, int64_t i, bool square) {
+    if (square) return (int32_t)i;
+    return A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i]] : 0;
+}
+
+// Upload a host CSR as CSR2 (rows padded to even length with (pad column, 0.0)).
+void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square) {
     const int64_t n = A.nrows;
     Buf<int64_t> rp(n + 1);
     rp[0] = 0;
@@ -135,13 +145,12 @@ void upload_csr(DevState &D, const HCsr &A, DCsr &out, bool square) {
             v[o] = A.v[k];
         }
         if (o < rp[i + 1]) {
-            ci[o] = square ? (int32_t)i : (A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i]] : 0);
+            ci[o] = pad_col(A, i, square);
             v[o] = 0.0;
         }
     }
-    out.nrows = n;
-    out.ncols = A.ncols;
-    out.nnz2 = nnz2;
+    out.fmt = 0;
+    out.stored = nnz2;
     out.rp = D.alloc_n<int64_t>(n + 1);
     out.ci = D.alloc_n<int32_t>(nnz2);
     out.v = D.alloc_n<double>(nnz2);
@@ -149,6 +158,72 @@ void upload_csr(DevState &D, const HCsr &A, DCsr &out, bool square) {
     CUDA_OK(cudaMemcpy(out.rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.ci, ci.data(), sizeof(int32_t) * nnz2, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * nnz2, cudaMemcpyHostToDevice));
+}
+
+// Slice offsets (in pairs) of the SELL2 layout; returns the stored entry count.
+int64_t sell2_offsets(const HCsr &A, Buf<int64_t> &soff) {
+    const int64_t n = A.nrows, nsl = (n + 31) / 32;
+    soff.alloc(nsl + 1);
+    soff[0] = 0;
+    for (int64_t s = 0; s < nsl; s++) {
+        int64_t W = 0;
+        for (int64_t i = s * 32; i < std::min(n, s * 32 + 32); i++) W = std::max(W, (A.rp[i + 1] - A.rp[i] + 1) / 2);
+        soff[s + 1] = soff[s] + 32 * W;
+    }
+    return 2 * soff[nsl];
+}
+
+void upload_sell2(DevState &D, const HCsr &A, DCsr &out, bool square) {
+    const int64_t n = A.nrows, nsl = (n + 31) / 32;
+    Buf<int64_t> soff;
+    const int64_t stored = sell2_offsets(A, soff);
+    Buf<int32_t> ci(stored);
+    Buf<double> v(stored);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t s = 0; s < nsl; s++) {
+        const int64_t W = (soff[s + 1] - soff[s]) / 32;
+        for (int l = 0; l < 32; l++) {
+            const int64_t i = s * 32 + l;
+            const int64_t b = i < n ? A.rp[i] : 0, len = i < n ? A.rp[i + 1] - A.rp[i] : 0;
+            const int32_t pc = i < n ? pad_col(A, i, square) : 0;
+            for (int64_t k = 0; k < W; k++)
+                for (int h = 0; h < 2; h++) {
+                    const int64_t e = 2 * k + h;
+                    const int64_t dst = 2 * (soff[s] + 32 * k + l) + h;
+                    ci[dst] = e < len ? A.ci[b + e] : pc;
+                    v[dst] = e < len ? A.v[b + e] : 0.0;
+                }
+        }
+    }
+    out.fmt = 1;
+    out.stored = stored;
+    out.soff = D.alloc_n<int64_t>(nsl + 1);
+    out.ci = D.alloc_n<int32_t>(stored);
+    out.v = D.alloc_n<double>(stored);
+    CUDA_OK(cudaMemcpy(out.soff, soff.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.ci, ci.data(), sizeof(int32_t) * stored, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * stored, cudaMemcpyHostToDevice));
+}
+
+// Format choice (amg_params.format): 1 = CSR2 everywhere; 2 = SELL2 wherever allowed; 0 = auto:
+// SELL2 when there are enough 32-row slices to fill the GPU (>= 4 per SM) and padding <= 10 %.
+void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, bool force_csr) {
+    out.nrows = A.nrows;
+    out.ncols = A.ncols;
+    out.nnz = A.nnz();
+    bool sell = false;
+    if (!force_csr && format != 1) {
+        if (format == 2) {
+            sell = true;
+        } else {
+            Buf<int64_t> soff;
+            const int64_t stored = sell2_offsets(A, soff);
+            const int64_t nsl = (A.nrows + 31) / 32;
+            sell = nsl >= 4 * D.nsm && (double)stored <= 1.10 * (double)std::max<int64_t>(out.nnz, 1);
+        }
+    }
+    if (sell) upload_sell2(D, A, out, square);
+    else upload_csr2(D, A, out, square);
 }
 
 int grid_for(const DevState &D, int64_t n) {
@@ -160,12 +235,21 @@ dev::DotCtx dotctx(DevState &D, int kind) { return dev::DotCtx{D.partials, D.cou
 
 template <class Epi>
 void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind = dev::DOT_NONE) {
+    const int2 *ci2 = reinterpret_cast<const int2 *>(A.ci);
+    const double2 *v2 = reinterpret_cast<const double2 *>(A.v);
+    if (A.fmt == 1) {
+        const int64_t nsl = (A.nrows + 31) / 32;
+        const int64_t wpb = dev::kBlock / 32;
+        int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, D.max_grid));
+        dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind));
+        D.launches_total++;
+        CUDA_OK(cudaGetLastError());
+        return;
+    }
     const int64_t ngroups = (A.nrows + A.G - 1) / A.G;
     const int64_t warps_per_block = dev::kBlock / 32;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, D.max_grid));
     dev::DotCtx dc = dotctx(D, dotkind);
-    const int2 *ci2 = reinterpret_cast<const int2 *>(A.ci);
-    const double2 *v2 = reinterpret_cast<const double2 *>(A.v);
     switch (A.G) {
 #define CASE(GG) \
     case GG: dev::k_csr2<GG, Epi><<<grid, dev::kBlock, 0, st>>>(A.rp, ci2, v2, g, A.nrows, epi, dc); break;
@@ -348,10 +432,11 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist) {
             DLevel &L = D->lev[l];
             L.N = h.N;
             L.nnz = h.K.nnz();
-            upload_csr(*D, h.K, L.K, true);
-            if (l + 1 < H.nlevels) {
-                upload_csr(*D, h.P, L.P, false);
-                upload_csr(*D, h.R, L.R, false);
+            const bool coarsest = (l + 1 == H.nlevels);
+            upload_op(*D, h.K, L.K, true, H.prm.format, coarsest);
+            if (!coarsest) {
+                upload_op(*D, h.P, L.P, false, H.prm.format, false);
+                upload_op(*D, h.R, L.R, false, H.prm.format, false);
             }
             Buf<double> invd(h.N);
             for (int64_t i = 0; i < h.N; i++) invd[i] = 1.0 / h.dhat[i];

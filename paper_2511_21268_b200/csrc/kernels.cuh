@@ -257,6 +257,57 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
 }
 
 // ------------------------------------------------------------------------------------------------
+// The streaming SELL-32 core ("SELL2"): slices of 32 consecutive rows, one row per lane.  Within a
+// slice, pair-column k of lane l lives at pair index soff[s] + 32·k + l, so each warp-wide load is a
+// contiguous 512-byte value segment + 256-byte column segment.  No shuffles; the epilogue is one
+// row per lane (coalesced).  U independent pair loads per lane are in flight per iteration.
+// ------------------------------------------------------------------------------------------------
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ soff, const int2 *__restrict__ ci2,
+                                                  const double2 *__restrict__ v2, const double *__restrict__ g,
+                                                  int64_t nrows, Epi epi, DotCtx dc) {
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t nslices = (nrows + 31) >> 5;
+    double dacc = 0.0;
+    for (int64_t sl = warp; sl < nslices; sl += nwarps) {
+        const int64_t off = __ldg(soff + sl);
+        const int W = (int)((__ldg(soff + sl + 1) - off) >> 5);
+        const double2 *vp = v2 + off + lane;
+        const int2 *cp = ci2 + off + lane;
+        double acc[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) acc[u] = 0.0;
+        int k = 0;
+        for (; k + U <= W; k += U) {
+            double2 va[U];
+            int2 ca[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                va[u] = ld_stream(vp + (int64_t)(k + u) * 32);
+                ca[u] = ld_stream(cp + (int64_t)(k + u) * 32);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                acc[u] = fma(va[u].x, __ldg(g + ca[u].x), acc[u]);
+                acc[u] = fma(va[u].y, __ldg(g + ca[u].y), acc[u]);
+            }
+        }
+        for (; k < W; k++) {
+            const double2 va = ld_stream(vp + (int64_t)k * 32);
+            const int2 ca = ld_stream(cp + (int64_t)k * 32);
+            acc[0] = fma(va.x, __ldg(g + ca.x), acc[0]);
+            acc[0] = fma(va.y, __ldg(g + ca.y), acc[0]);
+        }
+        const int64_t row = (sl << 5) + lane;
+        if (row < nrows) dacc += epi(row, (acc[0] + acc[1]) + (acc[2] + acc[3]));
+    }
+    if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+}
+
+// ------------------------------------------------------------------------------------------------
 // Elementwise / reduction kernels (grid-stride, fused)
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock) k_cheb_first(int64_t n, const double *__restrict__ b,

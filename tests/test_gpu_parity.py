@@ -38,13 +38,16 @@ CASES = {
 _cache = {}
 
 
-def build(case, **kw):
-    key = (case, tuple(sorted(kw.items())))
+FORMATS = [1, 2]  # 1 = CSR2 (warp per row group), 2 = SELL2 (row per lane) on every non-coarsest operator
+
+
+def build(case, fmt=0, **kw):
+    key = (case, fmt, tuple(sorted(kw.items())))
     if key not in _cache:
         amg = _amg()
         dim, p, n = CASES[case]
         K, F = amg.iga_poisson(dim, p, n)
-        H = amg.Hierarchy(K, amg.params(p, **kw))
+        H = amg.Hierarchy(K, amg.params(p, format=fmt, **kw))
         Ho = oracle.setup(K.to_scipy(), oracle.OParams.for_degree(p, **kw))
         _cache[key] = (K.to_scipy(), F, H, Ho)
     return _cache[key]
@@ -54,10 +57,11 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("case", list(CASES))
-def test_level_operators(case):
+def test_level_operators(case, fmt):
     """K_l, P̄_l and R_l applied on the device vs the oracle's sequential SpMV, every level."""
-    K, F, H, Ho = build(case)
+    K, F, H, Ho = build(case, fmt)
     rng = np.random.default_rng(1)
     for l, L in enumerate(Ho.levels):
         ops = [(0, L.K)] + ([] if L.P is None else [(1, L.P), (2, L.R)])
@@ -70,10 +74,11 @@ def test_level_operators(case):
             assert np.all(np.abs(y.cpu().numpy() - ref) <= 1e-13 * bound + 1e-300), (l, op)
 
 
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("case", list(CASES))
-def test_vcycle(case):
+def test_vcycle(case, fmt):
     """One V-cycle (c.18: Chebyshev pre/post smoothing, restriction, coarse solve, prolongation)."""
-    K, F, H, Ho = build(case)
+    K, F, H, Ho = build(case, fmt)
     for seed in (3, 4):
         r = amg_inputs.uniform_pm1(K.shape[0], seed=seed)
         z = H.vcycle(dev(r)).cpu().numpy()
@@ -81,11 +86,12 @@ def test_vcycle(case):
         assert np.abs(z - zo).max() <= 1e-12 * np.abs(zo).max()
 
 
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("case", list(CASES))
-def test_pcg_fixed_iterations_and_counts(case):
+def test_pcg_fixed_iterations_and_counts(case, fmt):
     """c.19: same iterate after the same number of iterations (1e-10), and iteration counts at
     rtol 1e-6 equal within ±1, for the manufactured RHS and a seeded random RHS."""
-    K, F, H, Ho = build(case)
+    K, F, H, Ho = build(case, fmt)
     for rhs in (F, amg_inputs.uniform_pm1(K.shape[0])):
         uo, ito, rro, histo, rco = oracle.pcg(Ho, rhs, rtol=1e-6, maxit=200)
         assert rco == 0
@@ -137,22 +143,23 @@ def test_edge_cases():
     r = amg_inputs.uniform_pm1(Ks.shape[0], seed=7)
     assert np.abs(Hs.vcycle(dev(r)).cpu().numpy() - oracle.vcycle(Hso, r)).max() <= 1e-12 * np.abs(r).max()
     # degree-1 smoother and odd degree paths
-    for m in (1, 3):
+    for m, fmt in ((1, 1), (3, 2), (2, 2)):
         Km, Fm = amg.iga_poisson(3, 2, 8)
-        Hm = amg.Hierarchy(Km, amg.params(2, cheb_degree=m))
+        Hm = amg.Hierarchy(Km, amg.params(2, cheb_degree=m, format=fmt))
         Hmo = oracle.setup(Km.to_scipy(), oracle.OParams(cheb_degree=m))
         r = amg_inputs.uniform_pm1(Km.shape[0], seed=8)
         zo = oracle.vcycle(Hmo, r)
         assert np.abs(Hm.vcycle(dev(r)).cpu().numpy() - zo).max() <= 1e-12 * np.abs(zo).max()
 
 
-def test_c3_full_size_properties():
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_c3_full_size_properties(fmt):
     """C3 (k=96, p=3; 941,094 DOFs) in the bench's configuration: hierarchy identical to the host
     export, level-0 SpMV vs the oracle on all rows, V-cycle symmetry, converged true residual."""
     amg = _amg()
     K, F = amg.iga_poisson(3, 3, 96)
     Ks = K.to_scipy()
-    H = amg.Hierarchy(K, amg.params(3))
+    H = amg.Hierarchy(K, amg.params(3, format=fmt))
     rng = np.random.default_rng(11)
     x = rng.uniform(-1, 1, Ks.shape[0])
     y = torch.empty(Ks.shape[0], dtype=torch.float64, device="cuda")
