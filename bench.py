@@ -154,6 +154,10 @@ def run_gpu(args) -> None:
     info = H.info()
     N = K.shape[0]
     del K
+    op_cfg = [H.op_config(l, 0) for l in range(info["levels"])]
+    k0 = op_cfg[0]
+    kname = (f"{'k_csr4t' if k0['kernel'] == 'csr_tma' else 'k_csr2'}<G={k0['G']},U={k0['U']},EpiCheb> "
+             "(fused Chebyshev-ℓ1-Jacobi step on level 0)")
     stream = torch.cuda.current_stream()
     Fd = torch.from_numpy(F).cuda()
     u = torch.zeros_like(Fd)
@@ -242,6 +246,8 @@ def run_gpu(args) -> None:
                             f"{N} free DOFs, AMG-PCG rtol {args.rtol}",
                 "dofs": N, "nnz_K0": info["nnz"][0], "levels": info["levels"], "level_N": info["N"],
                 "opc": round(info["opc"], 4), "cheb_degree": m, "coarse_sweeps": 30, "format": args.format,
+                "level_kernels": op_cfg,
+                "cuda_graphs": os.environ.get("AMG_GRAPHS", "1") != "0",
                 "parallelism": "replicas" if world > 1 else "single",
                 "l2": "inputs exceed L2 (K0 = %.2f GB >> 126 MB); no flush needed" % (12e-9 * info["nnz"][0]),
             },
@@ -254,7 +260,7 @@ def run_gpu(args) -> None:
             "vcycle_frac_of_peak": round(vcyc_gbs / peak, 4),
             "gpu_launches": ks["kernels_launched"],
             "roofline": {
-                "kernel": "k_csr2<32, EpiCheb> (fused Chebyshev-ℓ1-Jacobi step on level 0)",
+                "kernel": kname,
                 "bound": "hbm",
                 "achieved": round(achieved, 1),
                 "peak": peak,

@@ -169,6 +169,17 @@ typedef struct {
 amg_status amg_set_profiling(amg_hierarchy *H, int enable); /* enable resets the counters */
 amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
 
+/* Device kernel chosen for operator op (0 K_l, 1 P̄_l, 2 R_l) of level l: layout (0 padded CSR,
+ * 1 SELL-32), kernel (0 register-batched warp-per-row CSR, 1 TMA-staged CSR), rows per warp group G,
+ * pairs per lane per round trip U, stored entries (with padding), and the autotuned y = A·x time in
+ * microseconds (0 if the heuristic choice was kept).  AMG_EINVAL for a bad level/op. */
+typedef struct {
+    int layout, kernel, G, U;
+    int64_t stored;
+    double tuned_us;
+} amg_op_config;
+amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
+
 void amg_hierarchy_free(amg_hierarchy *H);
 
 /* Thread-local description of the last non-OK status ("" if none). */

@@ -230,6 +230,12 @@ class Hierarchy:
     def set_profiling(self, enable: bool) -> None:
         check(lib().amg_set_profiling(self._h, int(enable)))
 
+    def op_config(self, level: int, op: int = 0) -> dict:
+        c = _lib.amg_op_config()
+        check(lib().amg_operator_config(self._h, level, op, C.byref(c)))
+        return dict(layout=("csr", "sell32")[c.layout], kernel=("csr_regs", "csr_tma")[c.kernel], G=c.G, U=c.U,
+                    stored=c.stored, tuned_us=round(c.tuned_us, 2))
+
     def kernel_stats(self) -> dict:
         s = _lib.amg_kernel_stats()
         check(lib().amg_get_kernel_stats(self._h, C.byref(s)))

@@ -21,7 +21,7 @@ STATUS = {0: "AMG_OK", 1: "AMG_NOT_CONVERGED", -1: "AMG_EINVAL", -2: "AMG_ENOMEM
 EXPORTED = ["amg_iga_poisson", "amg_iga_tables", "amg_csr_free", "amg_free", "amg_params_default",
             "amg_set_allocator", "amg_setup", "amg_pcg_solve", "amg_pcg_solve_host", "amg_vcycle",
             "amg_level_apply", "amg_hierarchy_info", "amg_hierarchy_export", "amg_set_profiling",
-            "amg_get_kernel_stats", "amg_hierarchy_free", "amg_last_error"]
+            "amg_get_kernel_stats", "amg_operator_config", "amg_hierarchy_free", "amg_last_error"]
 
 
 class AmgError(RuntimeError):
@@ -56,6 +56,11 @@ class amg_kernel_stats(C.Structure):
                 ("kernels_launched", C.c_int64)]
 
 
+class amg_op_config(C.Structure):
+    _fields_ = [("layout", C.c_int), ("kernel", C.c_int), ("G", C.c_int), ("U", C.c_int), ("stored", C.c_int64),
+                ("tuned_us", C.c_double)]
+
+
 _lib = None
 
 
@@ -85,6 +90,7 @@ def lib() -> C.CDLL:
         "amg_hierarchy_export": ([vp, C.c_int, P(P(amg_csr)), P(P(amg_csr)), P(P(C.c_int32)), P(dp), dp], C.c_int),
         "amg_set_profiling": ([vp, C.c_int], C.c_int),
         "amg_get_kernel_stats": ([vp, P(amg_kernel_stats)], C.c_int),
+        "amg_operator_config": ([vp, C.c_int, C.c_int, P(amg_op_config)], C.c_int),
         "amg_hierarchy_free": ([vp], None),
         "amg_last_error": ([], C.c_char_p),
     }

@@ -49,7 +49,10 @@ struct DCsr {
     int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
     int32_t *ci = nullptr;
     double *v = nullptr;
-    int G = 32;
+    int G = 32;    // CSR cores: rows per warp group
+    int U = 4;     // CSR cores: pairs per lane per round trip (CSR2) / chunk of 32·U pairs (CSR4T)
+    int kern = 0;  // CSR layouts: 0 = register-batched k_csr2, 1 = TMA-staged k_csr4t (needs 4-padding)
+    float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
 };
 
 struct DLevel {
@@ -82,6 +85,18 @@ struct DevState {
     size_t ev_used = 0;
     int64_t launches_total = 0;
     double bytes_dominant = 0.0;
+    double prof_ms = 0.0;
+    int64_t prof_n = 0;
+    // CUDA graphs of the PCG iteration (kind 0: first iteration, 1: later iterations)
+    bool graphs = true;
+    cudaStream_t cap = nullptr;
+    struct Seg {
+        cudaGraphExec_t exec = nullptr;
+        double *u = nullptr;
+        bool prof = false;
+        size_t ev0 = 0, ev1 = 0;
+        int64_t nk = 0;
+    } seg[2];
 
     void *alloc(size_t bytes) {
         void *p = nullptr;
@@ -106,17 +121,30 @@ struct DevState {
         }
         for (auto e : ev) cudaEventDestroy(e);
         if (hS) cudaFreeHost(hS);
+        for (auto &s : seg)
+            if (s.exec) cudaGraphExecDestroy(s.exec);
+        if (cap) cudaStreamDestroy(cap);
     }
 };
 
 namespace {
 
+// Rows per warp group: enough groups to give every SM ~64 warps of work, coalesced epilogues where
+// possible.  Instantiated: 1, 4, 8, 32.  Env AMG_CSR_G overrides (experiments).
 int choose_G(int64_t nrows) {
-    // enough row groups to give every SM ~64 warps of work, coalesced epilogues where possible
-    int64_t target = nrows / (148 * 64);
-    int G = 1;
-    while (G < 32 && 2 * G <= target) G *= 2;
-    return G;
+    if (const char *e = std::getenv("AMG_CSR_G")) return std::atoi(e);
+    const int64_t target = nrows / (148 * 64);
+    return target >= 32 ? 32 : target >= 8 ? 8 : target >= 4 ? 4 : 1;
+}
+
+// Pair loads per lane in flight: enough to cover the longest row in one round trip (max 8).
+// Instantiated: 2, 4, 6, 8.  Env AMG_CSR_U overrides (experiments).
+int choose_U(const HCsr &A) {
+    if (const char *e = std::getenv("AMG_CSR_U")) return std::atoi(e);
+    int64_t maxlen = 0;
+    for (int64_t i = 0; i < A.nrows; i++) maxlen = std::max(maxlen, A.rp[i + 1] - A.rp[i]);
+    const int64_t pairs_per_lane = ((maxlen + 1) / 2 + 31) / 32;
+    return pairs_per_lane <= 2 ? 2 : pairs_per_lane <= 4 ? 4 : pairs_per_lane <= 6 ? 6 : 8;
 }
 
 // Pad column of row i: the diagonal for square operators, else the row's first column.
@@ -125,14 +153,15 @@ inline int32_t pad_col(const HCsr &A, int64_t i, bool square) {
     return A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i]] : 0;
 }
 
-// Upload a host CSR as CSR2 (rows padded to even length with (pad column, 0.0)).
-void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square) {
+// Upload a host CSR as CSR2 (rows padded to a multiple of `mult` entries with (pad column, 0.0);
+// mult = 2 for CSR2, 4 for the TMA-staged CSR4T whose bulk copies need 16-byte aligned ranges).
+void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 2) {
     const int64_t n = A.nrows;
     Buf<int64_t> rp(n + 1);
     rp[0] = 0;
     for (int64_t i = 0; i < n; i++) {
         int64_t len = A.rp[i + 1] - A.rp[i];
-        rp[i + 1] = rp[i] + len + (len & 1);
+        rp[i + 1] = rp[i] + (len + mult - 1) / mult * mult;
     }
     const int64_t nnz2 = rp[n];
     Buf<int32_t> ci(nnz2);
@@ -144,7 +173,7 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square) {
             ci[o] = A.ci[k];
             v[o] = A.v[k];
         }
-        if (o < rp[i + 1]) {
+        for (; o < rp[i + 1]; o++) {
             ci[o] = pad_col(A, i, square);
             v[o] = 0.0;
         }
@@ -155,6 +184,7 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square) {
     out.ci = D.alloc_n<int32_t>(nnz2);
     out.v = D.alloc_n<double>(nnz2);
     out.G = choose_G(n);
+    out.U = choose_U(A);
     CUDA_OK(cudaMemcpy(out.rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.ci, ci.data(), sizeof(int32_t) * nnz2, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * nnz2, cudaMemcpyHostToDevice));
@@ -205,23 +235,21 @@ void upload_sell2(DevState &D, const HCsr &A, DCsr &out, bool square) {
     CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * stored, cudaMemcpyHostToDevice));
 }
 
-// Format choice (amg_params.format): 1 = CSR2 everywhere; 2 = SELL2 wherever allowed; 0 = auto:
-// SELL2 when there are enough 32-row slices to fill the GPU (>= 4 per SM) and padding <= 10 %.
+// Format choice (amg_params.format): 1 = CSR2 everywhere; 2 = SELL2 wherever allowed; 0 = auto.
+// Auto = CSR2: measured on B200 at C3 level 0, CSR2 streams at 4.55 TB/s vs SELL2's 4.10 TB/s
+// (profiles/r01), and SELL2 starves the GPU on the short coarse levels.
 void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, bool force_csr) {
     out.nrows = A.nrows;
     out.ncols = A.ncols;
     out.nnz = A.nnz();
-    bool sell = false;
-    if (!force_csr && format != 1) {
-        if (format == 2) {
-            sell = true;
-        } else {
-            Buf<int64_t> soff;
-            const int64_t stored = sell2_offsets(A, soff);
-            const int64_t nsl = (A.nrows + 31) / 32;
-            sell = nsl >= 4 * D.nsm && (double)stored <= 1.10 * (double)std::max<int64_t>(out.nnz, 1);
-        }
+    if (format == 0 || format == 3) {
+        // rows padded to 4 entries: runnable by both the register-batched CSR2 core and the
+        // TMA-staged CSR4T core (format 0 autotunes between them after the upload)
+        upload_csr2(D, A, out, square, 4);
+        out.kern = (format == 3) ? 1 : 0;
+        return;
     }
+    const bool sell = !force_csr && format == 2;
     if (sell) upload_sell2(D, A, out, square);
     else upload_csr2(D, A, out, square);
 }
@@ -232,6 +260,37 @@ int grid_for(const DevState &D, int64_t n) {
 }
 
 dev::DotCtx dotctx(DevState &D, int kind) { return dev::DotCtx{D.partials, D.counter, D.S, kind}; }
+
+template <int G, int U, class Epi>
+void launch_csr4t_gu(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    constexpr int smem = dev::TmaCfg<U>::SMEM;
+    static bool attr_set = false;  // per instantiation; device-independent attribute
+    if (!attr_set) {
+        CUDA_OK(cudaFuncSetAttribute(dev::k_csr4t<G, U, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_set = true;
+    }
+    const int64_t ngroups = (A.nrows + G - 1) / G;
+    const int64_t wpb = dev::kBlockT / 32;
+    const int64_t per_sm = std::max(1, (227 * 1024) / (smem + 1024));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, per_sm * D.nsm));
+    grid = std::min(grid, D.max_grid);
+    dev::k_csr4t<G, U, Epi><<<grid, dev::kBlockT, smem, st>>>(A.rp, A.ci, A.v, g, A.nrows, epi, dotctx(D, dotkind));
+}
+
+template <class Epi>
+void launch_csr4t(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    switch (A.G * 16 + A.U) {
+#define CASE(GG, UU) \
+    case GG * 16 + UU: launch_csr4t_gu<GG, UU, Epi>(D, A, g, epi, st, dotkind); break;
+#define CASES_G(GG) CASE(GG, 2) CASE(GG, 4) CASE(GG, 6) CASE(GG, 8)
+        CASES_G(1) CASES_G(4) CASES_G(8) CASES_G(32)
+#undef CASES_G
+#undef CASE
+        default: throw Error{AMG_EINVAL, "bad CSR4T kernel configuration"};
+    }
+    D.launches_total++;
+    CUDA_OK(cudaGetLastError());
+}
 
 template <class Epi>
 void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind = dev::DOT_NONE) {
@@ -246,19 +305,75 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
         CUDA_OK(cudaGetLastError());
         return;
     }
+    if (A.kern == 1) {
+        launch_csr4t(D, A, g, epi, st, dotkind);
+        return;
+    }
     const int64_t ngroups = (A.nrows + A.G - 1) / A.G;
     const int64_t warps_per_block = dev::kBlock / 32;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, D.max_grid));
     dev::DotCtx dc = dotctx(D, dotkind);
-    switch (A.G) {
-#define CASE(GG) \
-    case GG: dev::k_csr2<GG, Epi><<<grid, dev::kBlock, 0, st>>>(A.rp, ci2, v2, g, A.nrows, epi, dc); break;
-        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+    const int key = A.G * 16 + A.U;
+    switch (key) {
+#define CASE(GG, UU)                                                                                   \
+    case GG * 16 + UU:                                                                                 \
+        dev::k_csr2<GG, UU, Epi><<<grid, dev::kBlock, 0, st>>>(A.rp, ci2, v2, g, A.nrows, epi, dc); \
+        break;
+#define CASES_G(GG) CASE(GG, 2) CASE(GG, 4) CASE(GG, 6) CASE(GG, 8)
+        CASES_G(1) CASES_G(4) CASES_G(8) CASES_G(32)
+#undef CASES_G
 #undef CASE
-        default: throw Error{AMG_EINVAL, "bad row-group size"};
+        default: throw Error{AMG_EINVAL, "bad CSR2 kernel configuration"};
     }
     D.launches_total++;
     CUDA_OK(cudaGetLastError());
+}
+
+// Setup-time autotuning of one CSR4-layout operator: time y = A·x for every (kernel, G, U) candidate
+// and keep the fastest.  All candidates sum each row in the same order, so the choice changes speed,
+// never results.  Small operators (latency-bound) keep the heuristic choice.
+void autotune_op(DevState &D, DCsr &A, double *x, double *y) {
+    if (A.fmt != 0 || A.nnz < 2000000) return;
+    if (std::getenv("AMG_CSR_G") || std::getenv("AMG_CSR_U")) return;
+    if (const char *e = std::getenv("AMG_AUTOTUNE"))
+        if (std::atoi(e) == 0) return;
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    const int Gs[] = {1, 4, 8, 32};
+    const int Us[] = {2, 4, 6, 8};
+    float best = 1e30f;
+    int bk = A.kern, bg = A.G, bu = A.U;
+    for (int kern = 0; kern < 2; kern++)
+        for (int G : Gs)
+            for (int U : Us) {
+                if (kern == 1 && U > 4) continue;
+                if ((A.nrows + G - 1) / G < 4 * D.nsm) continue;  // too few warp groups to fill the GPU
+                A.kern = kern;
+                A.G = G;
+                A.U = U;
+                dev::EpiStore e{y};
+                launch_csr(D, A, x, e, nullptr);
+                CUDA_OK(cudaEventRecord(e0, nullptr));
+                for (int rep = 0; rep < 3; rep++) launch_csr(D, A, x, e, nullptr);
+                CUDA_OK(cudaEventRecord(e1, nullptr));
+                CUDA_OK(cudaEventSynchronize(e1));
+                float ms = 0.f;
+                CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+                if (ms < best) {
+                    best = ms;
+                    bk = kern;
+                    bg = G;
+                    bu = U;
+                }
+            }
+    A.kern = bk;
+    A.G = bg;
+    A.U = bu;
+    A.tuned_us = best / 3.f * 1000.f;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    D.launches_total = 0;
 }
 
 // Profiling: events around the dominant kernel (level-0 fused Chebyshev step).
@@ -427,6 +542,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist) {
         D->nlevels = H.nlevels;
         D->m = H.prm.cheb_degree;
         D->sweeps = H.prm.coarse_sweeps;
+        if (const char *e = std::getenv("AMG_GRAPHS")) D->graphs = std::atoi(e) != 0;
         for (int l = 0; l < H.nlevels; l++) {
             const HLevel &h = H.lev[l];
             DLevel &L = D->lev[l];
@@ -462,6 +578,16 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist) {
         CUDA_OK(cudaMemset(D->S, 0, sizeof(dev::Scalars)));
         CUDA_OK(cudaMallocHost(&D->hS, sizeof(dev::Scalars)));
         D->bytes_dominant = 12.0 * (double)H.lev[0].K.nnz() + 64.0 * (double)N0;
+        if (H.prm.format == 0) {  // autotune every large operator (x = r, y = z scratch, N0 >= any size)
+            CUDA_OK(cudaMemset(D->r, 0, sizeof(double) * N0));
+            for (int l = 0; l < D->nlevels; l++) {
+                autotune_op(*D, D->lev[l].K, D->r, D->z);
+                if (l + 1 < D->nlevels) {
+                    autotune_op(*D, D->lev[l].P, D->r, D->z);
+                    autotune_op(*D, D->lev[l].R, D->r, D->z);
+                }
+            }
+        }
         CUDA_OK(cudaDeviceSynchronize());
     } catch (...) {
         delete D;
@@ -471,6 +597,86 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist) {
 }
 
 void dev_destroy(DevState *D) { delete D; }
+
+// Fold the elapsed times of the event pairs recorded since the last collection into the profile.
+static void prof_collect(DevState &D, size_t ev0 = 0, size_t ev1 = (size_t)-1, bool reset = true) {
+    if (ev1 == (size_t)-1) ev1 = D.ev_used;
+    for (size_t k = ev0; k + 1 < ev1; k += 2) {
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, D.ev[k], D.ev[k + 1]));
+        D.prof_ms += ms;
+        D.prof_n++;
+    }
+    if (reset) D.ev_used = 0;
+}
+
+// One PCG iteration on the device: z = V(r) with ρ = rᵀz (kind 0: initial, 1: with β), p = z + βp,
+// q = Kp with α = ρ/pᵀq, u += αp, r −= αq, ‖r‖², and the 64-byte scalar block copied to pinned host
+// memory.  No host decision inside, so it is captured once into a CUDA graph and replayed.
+static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
+    DLevel &L0 = D.lev[0];
+    const int64_t N = L0.N;
+    vcycle(D, D.r, D.z, st, kind == 0 ? dev::DOT_RZ_INIT : dev::DOT_RZ);
+    dev::k_p_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.z, D.p, D.S, kind == 0 ? 1 : 0);
+    D.launches_total++;
+    {
+        dev::EpiSpmvDot e{D.p, D.q};
+        launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ);
+    }
+    dev::k_pcg_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR));
+    D.launches_total++;
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
+}
+
+static void run_segment(DevState &D, int kind, double *u, cudaStream_t st) {
+    if (!D.graphs) {
+        enqueue_segment(D, kind, u, st);
+        CUDA_OK(cudaStreamSynchronize(st));
+        prof_collect(D);
+        return;
+    }
+    DevState::Seg &S = D.seg[kind];
+    if (!S.exec || S.u != u || S.prof != D.prof) {
+        if (S.exec) {
+            cudaGraphExecDestroy(S.exec);
+            S.exec = nullptr;
+        }
+        if (!D.cap) CUDA_OK(cudaStreamCreateWithFlags(&D.cap, cudaStreamNonBlocking));
+        // events of this graph live at a fixed index range of D.ev
+        S.ev0 = D.ev_used = (kind == 0 ? 0 : 512);
+        if (D.ev.size() < 1024)
+            while (D.ev.size() < 1024) {
+                cudaEvent_t e;
+                CUDA_OK(cudaEventCreate(&e));
+                D.ev.push_back(e);
+            }
+        const int64_t nk0 = D.launches_total;
+        CUDA_OK(cudaStreamBeginCapture(D.cap, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_segment(D, kind, u, D.cap);
+        } catch (...) {
+            cudaGraph_t g;
+            cudaStreamEndCapture(D.cap, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t g;
+        CUDA_OK(cudaStreamEndCapture(D.cap, &g));
+        CUDA_OK(cudaGraphInstantiate(&S.exec, g, 0));
+        CUDA_OK(cudaGraphDestroy(g));
+        S.nk = D.launches_total - nk0;
+        D.launches_total = nk0;
+        S.ev1 = D.ev_used;
+        S.u = u;
+        S.prof = D.prof;
+        D.ev_used = 0;
+    }
+    CUDA_OK(cudaGraphLaunch(S.exec, st));
+    D.launches_total += S.nk;
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (D.prof) prof_collect(D, S.ev0, S.ev1, false);
+}
 
 // c.19 — PCG.  F, u: device pointers of length N_0.
 static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int maxit, cudaStream_t st, int *iters,
@@ -503,21 +709,11 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     if (hist) hist[0] = rn / nF;
     *relres = rn / nF;
     if (rn <= rtol * nF) return AMG_OK;
-    // z = V(r); ρ = rᵀz; p = z
-    vcycle(D, D.r, D.z, st, dev::DOT_RZ_INIT);
-    dev::k_p_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.z, D.p, D.S, 1);
-    D.launches_total++;
+    prof_collect(D);
     amg_status status = AMG_NOT_CONVERGED;
     for (int k = 1; k <= maxit; k++) {
-        {
-            dev::EpiSpmvDot e{D.p, D.q};
-            launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ);
-        }
-        dev::k_pcg_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR));
-        D.launches_total++;
-        CUDA_OK(cudaGetLastError());
-        CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
-        CUDA_OK(cudaStreamSynchronize(st));
+        // iteration k: [z = V(r); ρ = rᵀz; p = z + βp] then q = Kp, α, u += αp, r −= αq, ‖r‖²
+        run_segment(D, k == 1 ? 0 : 1, u, st);
         if (D.hS->flags) {
             *iters = k;
             return AMG_ENOTSPD;
@@ -530,9 +726,6 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
             status = AMG_OK;
             break;
         }
-        vcycle(D, D.r, D.z, st, dev::DOT_RZ);
-        dev::k_p_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.z, D.p, D.S, 0);
-        D.launches_total++;
     }
     CUDA_OK(cudaGetLastError());
     return status;
@@ -634,6 +827,8 @@ extern "C" amg_status amg_set_profiling(amg_hierarchy *H, int enable) {
     D->prof = enable != 0;
     D->ev_used = 0;
     D->launches_total = 0;
+    D->prof_ms = 0.0;
+    D->prof_n = 0;
     return AMG_OK;
     API_END
 }
@@ -643,16 +838,28 @@ extern "C" amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *s
     DevState *D = need_dev(H);
     if (!st) throw Error{AMG_EINVAL, "NULL stats"};
     CUDA_OK(cudaDeviceSynchronize());
-    double total = 0.0;
-    for (size_t k = 0; k + 1 < D->ev_used; k += 2) {
-        float ms = 0.f;
-        CUDA_OK(cudaEventElapsedTime(&ms, D->ev[k], D->ev[k + 1]));
-        total += ms;
-    }
-    st->launches = (int64_t)(D->ev_used / 2);
-    st->total_ms = total;
+    if (!D->graphs) prof_collect(*D);  // pairs recorded outside PCG (e.g. amg_vcycle)
+    st->launches = D->prof_n;
+    st->total_ms = D->prof_ms;
     st->bytes_per_launch = D->bytes_dominant;
     st->kernels_launched = D->launches_total;
+    return AMG_OK;
+    API_END
+}
+
+extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg) {
+    API_BEGIN
+    DevState *D = need_dev(H);
+    if (!cfg || level < 0 || level >= D->nlevels || op < 0 || op > 2) throw Error{AMG_EINVAL, "bad argument"};
+    if (op > 0 && level == D->nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
+    const DLevel &L = D->lev[level];
+    const DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
+    cfg->layout = A.fmt;
+    cfg->kernel = A.kern;
+    cfg->G = A.G;
+    cfg->U = A.U;
+    cfg->stored = A.stored;
+    cfg->tuned_us = A.tuned_us;
     return AMG_OK;
     API_END
 }

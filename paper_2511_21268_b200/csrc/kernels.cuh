@@ -49,15 +49,16 @@ __device__ __forceinline__ double warp_sum(double s) {
 
 // Deterministic block reduction + "last block finalises" (fixed partial order ⇒ run-to-run
 // identical scalars; no atomics on values).
-__device__ __forceinline__ void block_dot_finalize(double v, const DotCtx &dc) {
-    __shared__ double red[kBlock / 32];
+template <int BS>
+__device__ __forceinline__ void block_dot_finalize_n(double v, const DotCtx &dc) {
+    __shared__ double red[BS / 32];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     v = warp_sum(v);
     if (lane == 0) red[wid] = v;
     __syncthreads();
     if (wid == 0) {
-        double t = lane < kBlock / 32 ? red[lane] : 0.0;
+        double t = lane < BS / 32 ? red[lane] : 0.0;
         t = warp_sum(t);
         if (lane == 0) {
             dc.partials[blockIdx.x] = t;
@@ -70,13 +71,13 @@ __device__ __forceinline__ void block_dot_finalize(double v, const DotCtx &dc) {
     if (!last) return;
     __threadfence();
     double t = 0.0;
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += kBlock) t += __ldcg(dc.partials + i);
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += BS) t += __ldcg(dc.partials + i);
     t = warp_sum(t);
     if (lane == 0) red[wid] = t;
     __syncthreads();
     if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int w = 0; w < kBlock / 32; w++) s += red[w];
+        for (int w = 0; w < BS / 32; w++) s += red[w];
         Scalars *S = dc.S;
         switch (dc.kind) {
             case DOT_FF: S->ff = s; break;
@@ -101,6 +102,8 @@ __device__ __forceinline__ void block_dot_finalize(double v, const DotCtx &dc) {
         *dc.counter = 0u;
     }
 }
+
+__device__ __forceinline__ void block_dot_finalize(double v, const DotCtx &dc) { block_dot_finalize_n<kBlock>(v, dc); }
 
 // ------------------------------------------------------------------------------------------------
 // Epilogues.  operator()(row, s) consumes the row sum s = (A·g)_row and returns the row's
@@ -203,6 +206,9 @@ struct EpiProlong {  // a8: x += P̄ e
 // ------------------------------------------------------------------------------------------------
 // The streaming CSR2 core: warp per group of G rows, 128-bit loads, 2 row chunks in flight per lane.
 // ------------------------------------------------------------------------------------------------
+// Matrix streams: read once, keep them out of L1 (L1 holds the gathered vector).  `volatile` keeps
+// ptxas from interleaving a stalled gather between the batched stream loads (SASS-checked: without it
+// only ~2 stream loads were in flight per lane).
 __device__ __forceinline__ double2 ld_stream(const double2 *p) {
     double2 r;
     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -213,8 +219,16 @@ __device__ __forceinline__ int2 ld_stream(const int2 *p) {
     asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
+// Gather of the multiplied vector through the read-only path (L1-allocating).
+__device__ __forceinline__ double ld_gather(const double *p) {
+    double r;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
 
-template <int G, class Epi>
+// U: pair loads per lane issued back to back (predicated) before any is consumed, so a row of up to
+// 64·U non-zeros costs one round trip for the matrix stream and one for the x-gathers.
+template <int G, int U, class Epi>
 __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp, const int2 *__restrict__ ci2,
                                                  const double2 *__restrict__ v2, const double *__restrict__ g,
                                                  int64_t nrows, Epi epi, DotCtx dc) {
@@ -231,22 +245,31 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
             const int64_t row = r0 + t;
             const int64_t b = __ldg(rp + row) >> 1, e = __ldg(rp + row + 1) >> 1;
             double s0 = 0.0, s1 = 0.0;
-            int64_t k = b + lane;
-            for (; k + 32 < e; k += 64) {
-                const double2 va = ld_stream(v2 + k);
-                const int2 ca = ld_stream(ci2 + k);
-                const double2 vb = ld_stream(v2 + k + 32);
-                const int2 cb = ld_stream(ci2 + k + 32);
-                s0 = fma(va.x, __ldg(g + ca.x), s0);
-                s1 = fma(va.y, __ldg(g + ca.y), s1);
-                s0 = fma(vb.x, __ldg(g + cb.x), s0);
-                s1 = fma(vb.y, __ldg(g + cb.y), s1);
-            }
-            if (k < e) {
-                const double2 va = ld_stream(v2 + k);
-                const int2 ca = ld_stream(ci2 + k);
-                s0 = fma(va.x, __ldg(g + ca.x), s0);
-                s1 = fma(va.y, __ldg(g + ca.y), s1);
+            for (int64_t k0 = b + lane; k0 < e; k0 += 32 * U) {
+                double2 va[U];
+                int2 ca[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t k = k0 + 32 * u;
+                    ca[u] = k < e ? ld_stream(ci2 + k) : make_int2(-1, -1);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t k = k0 + 32 * u;
+                    va[u] = k < e ? ld_stream(v2 + k) : make_double2(0.0, 0.0);
+                }
+                double xa[U], xb[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const bool ok = ca[u].x >= 0;
+                    xa[u] = ok ? ld_gather(g + ca[u].x) : 0.0;
+                    xb[u] = ok ? ld_gather(g + ca[u].y) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    s0 = fma(va[u].x, xa[u], s0);
+                    s1 = fma(va[u].y, xb[u], s1);
+                }
             }
             const double s = warp_sum(s0 + s1);
             if (lane == t) mine = s;
@@ -254,6 +277,181 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
         if (lane < nr) dacc += epi(r0 + lane, mine);
     }
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+}
+
+// ------------------------------------------------------------------------------------------------
+// TMA-staged CSR core ("CSR4T"): rows padded to a multiple of 4 entries, so every row's value and
+// column ranges are 16-byte aligned multiples of 16 bytes.  Each warp walks its rows in chunks of
+// 32·U pairs; one elected lane streams the NEXT chunk's values and columns into a 2-stage shared-memory
+// ring with cp.async.bulk (TMA, completion on an mbarrier) while the warp reduces the current chunk
+// from shared memory and gathers x through L1/L2.  The HBM stream is therefore never serialised behind
+// gather latency or register scheduling.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr int kBlockT = 128;  // 4 warps per CTA for the TMA-staged core
+
+template <int U>
+struct TmaCfg {
+    static constexpr int CH = 32 * U;                  // pairs per chunk
+    static constexpr int STAGE = CH * 24;              // bytes per stage (16 B values + 8 B columns per pair)
+    static constexpr int WARP = 2 * STAGE + 16;        // 2 stages + 2 mbarriers
+    static constexpr int SMEM = (kBlockT / 32) * WARP;  // dynamic shared memory per CTA
+};
+
+template <int G, int U, class Epi>
+__global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ rp, const int *__restrict__ ci,
+                                                   const double *__restrict__ v, const double *__restrict__ g,
+                                                   int64_t nrows, Epi epi, DotCtx dc) {
+    using C = TmaCfg<U>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char *wb = smem + wib * C::WARP;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + 2 * C::STAGE);
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int64_t warp = ((int64_t)blockIdx.x * kBlockT + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlockT) >> 5;
+    const int64_t ngroups = (nrows + G - 1) / G;
+
+    // chunk cursor: group, row-in-group, pair range [k0, k1) of the row (pair = 2 entries)
+    struct Cur {
+        int64_t grp, k0, e;
+        int t, nr;
+        bool valid;
+    };
+    auto row_start = [&](Cur &c) {
+        const int64_t row = c.grp * G + c.t;
+        c.k0 = __ldg(rp + row) >> 1;
+        c.e = __ldg(rp + row + 1) >> 1;
+    };
+    auto first = [&](Cur &c) {
+        c.grp = warp;
+        c.t = 0;
+        c.valid = c.grp < ngroups;
+        if (c.valid) {
+            c.nr = (int)(nrows - c.grp * G < (int64_t)G ? nrows - c.grp * G : (int64_t)G);
+            row_start(c);
+        }
+    };
+    auto advance = [&](Cur &c) {
+        if (c.k0 + C::CH < c.e) {
+            c.k0 += C::CH;
+            return;
+        }
+        if (++c.t >= c.nr) {
+            c.grp += nwarps;
+            c.t = 0;
+            if (c.grp >= ngroups) {
+                c.valid = false;
+                return;
+            }
+            c.nr = (int)(nrows - c.grp * G < (int64_t)G ? nrows - c.grp * G : (int64_t)G);
+        }
+        row_start(c);
+    };
+    auto issue = [&](const Cur &c, int s) {
+        if (lane == 0) {
+            const int64_t np = (c.e - c.k0 < (int64_t)C::CH ? c.e - c.k0 : (int64_t)C::CH);
+            unsigned char *st = wb + s * C::STAGE;
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&bar[s], (uint32_t)(np * 24));
+            if (np > 0) {
+                bulk_g2s(st, v + 2 * c.k0, (uint32_t)(np * 16), &bar[s]);
+                bulk_g2s(st + C::CH * 16, ci + 2 * c.k0, (uint32_t)(np * 8), &bar[s]);
+            }
+        }
+    };
+
+    double dacc = 0.0, acc = 0.0, acc1 = 0.0, mine = 0.0;
+    uint32_t phase = 0;  // bit s = parity of stage s
+    Cur cur, nxt;
+    first(cur);
+    if (cur.valid) issue(cur, 0);
+    nxt = cur;
+    if (nxt.valid) advance(nxt);
+    int s = 0;
+    while (cur.valid) {
+        if (nxt.valid) issue(nxt, s ^ 1);
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const int np = (int)(cur.e - cur.k0 < (int64_t)C::CH ? cur.e - cur.k0 : (int64_t)C::CH);
+        const double2 *sv = reinterpret_cast<const double2 *>(wb + s * C::STAGE);
+        const int2 *sc = reinterpret_cast<const int2 *>(wb + s * C::STAGE + C::CH * 16);
+        double xa[U], xb[U];
+        double2 va[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int j = lane + 32 * u;
+            if (j < np) {
+                const int2 c2 = sc[j];
+                va[u] = sv[j];
+                xa[u] = __ldg(g + c2.x);
+                xb[u] = __ldg(g + c2.y);
+            } else {
+                va[u] = make_double2(0.0, 0.0);
+                xa[u] = xb[u] = 0.0;
+            }
+        }
+        // same per-lane summation order as k_csr2 (pairs k ≡ lane mod 32, ascending; .x and .y
+        // chains kept apart), so every kernel variant produces bitwise-identical row sums
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            acc = fma(va[u].x, xa[u], acc);
+            acc1 = fma(va[u].y, xb[u], acc1);
+        }
+        if (cur.k0 + C::CH >= cur.e) {  // last chunk of the row
+            const double sum = warp_sum(acc + acc1);
+            acc = 0.0;
+            acc1 = 0.0;
+            if (lane == cur.t) mine = sum;
+            if (cur.t == cur.nr - 1) {  // last row of the group: coalesced epilogue
+                if (lane < cur.nr) dacc += epi(cur.grp * G + lane, mine);
+                mine = 0.0;
+            }
+        }
+        __syncwarp();
+        cur = nxt;
+        if (nxt.valid) advance(nxt);
+        s ^= 1;
+    }
+    if constexpr (Epi::kDot) block_dot_finalize_n<kBlockT>(dacc, dc);
 }
 
 // ------------------------------------------------------------------------------------------------

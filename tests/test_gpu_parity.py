@@ -38,7 +38,7 @@ CASES = {
 _cache = {}
 
 
-FORMATS = [1, 2]  # 1 = CSR2 (warp per row group), 2 = SELL2 (row per lane) on every non-coarsest operator
+FORMATS = [1, 2, 3]  # 1 CSR2 (warp per row group), 2 SELL2 (row per lane), 3 CSR4T (TMA-staged rows)
 
 
 def build(case, fmt=0, **kw):
