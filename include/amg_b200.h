@@ -120,6 +120,17 @@ typedef struct {
 
 typedef struct amg_hierarchy amg_hierarchy; /* opaque, library-owned */
 
+/* Rank 0 creates the NCCL unique id (128 bytes) and broadcasts it to the other ranks (e.g. with
+ * torch.distributed) before they call amg_setup with amg_dist.  AMG_ENCCL on failure. */
+amg_status amg_nccl_unique_id(unsigned char id[128]);
+
+/* Multi-GPU row ownership: every level is split into contiguous row blocks balanced by
+ * nnz; levels with nnz <= 7e6 (env AMG_REPLICATE_NNZ) and the coarsest are replicated on all ranks.
+ * With nranks > 1, the F and u passed to amg_pcg_solve are this rank's rows [row_begin, row_end) of
+ * level 0 (global numbering); every rank builds the same global hierarchy on the host from the same
+ * full K.  Returns [0, N_0) on one GPU. */
+amg_status amg_local_rows(amg_hierarchy *H, int64_t *row_begin, int64_t *row_end);
+
 /* Builds the hierarchy of K on the host (deterministic; bitwise reproducible; c.6-c.15) and, unless
  * prm->host_only, uploads it to the device.  K is borrowed (copied).  K must be square, symmetric
  * and have a positive diagonal (else AMG_ENOTSPD).  prm NULL -> amg_params_default(·, 2).
@@ -179,6 +190,22 @@ typedef struct {
     double tuned_us;
 } amg_op_config;
 amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
+
+/* Host view of this rank's share of operator op (0 K_l, 1 P̄_l, 2 R_l) on level l, for hierarchies
+ * set up with an amg_dist of nranks > 1 (host_only or not).  Local columns are
+ * [owned: global col_begin..col_end-1 | ghosts: ghost[0..n_ghost-1]]; ghost values are received from
+ * rank q at offsets recv_off[q] .. recv_off[q]+recv_count[q]; this rank sends the owned entries
+ * send_idx[send_off[q] .. send_off[q]+send_count[q]) (local indices) to rank q.  All arrays are
+ * library-owned and valid until amg_hierarchy_free.  replicated = 1: the level is held whole by every
+ * rank (no view).  AMG_EINVAL if the hierarchy is not distributed or level/op is bad. */
+typedef struct {
+    int nranks, replicated, full_cols;
+    int64_t row_begin, row_end, col_begin, col_end, n_ghost;
+    const int64_t *ghost;
+    const int32_t *send_count, *send_off, *send_idx, *recv_count, *recv_off;
+    amg_csr local;
+} amg_dist_view;
+amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist_view *view);
 
 void amg_hierarchy_free(amg_hierarchy *H);
 

@@ -105,6 +105,32 @@ def use_torch_allocator() -> None:
     _ALLOC_REFS = refs
 
 
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    check(lib().amg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def make_dist(rank: int, nranks: int, device: int = 0, nccl_id: bytes | None = None) -> _lib.amg_dist:
+    """amg_dist for one process per GPU.  Without nccl_id, rank 0 creates the NCCL unique id and it is
+    broadcast with torch.distributed (the default process group must be initialised)."""
+    if nccl_id is None and nranks > 1:
+        import torch
+        import torch.distributed as dist
+        be = dist.get_backend()
+        dev = torch.device("cuda", torch.cuda.current_device()) if be == "nccl" else torch.device("cpu")
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nccl_id = bytes(t.cpu().numpy().tobytes())
+    d = _lib.amg_dist()
+    d.rank, d.nranks, d.device = rank, nranks, device
+    if nccl_id is not None:
+        C.memmove(d.nccl_id, nccl_id, 128)
+    return d
+
+
 def _borrow(K) -> tuple:
     """View a HostCsr / scipy CSR as an amg_csr (arrays kept alive by the returned tuple)."""
     indptr = np.ascontiguousarray(K.indptr, dtype=np.int64)
@@ -229,6 +255,33 @@ class Hierarchy:
 
     def set_profiling(self, enable: bool) -> None:
         check(lib().amg_set_profiling(self._h, int(enable)))
+
+    def local_rows(self) -> tuple[int, int]:
+        """This rank's rows [begin, end) of level 0 (global numbering); F and u are these rows."""
+        b, e = C.c_int64(), C.c_int64()
+        check(lib().amg_local_rows(self._h, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def dist_view(self, level: int, op: int = 0) -> dict:
+        """Host view (numpy copies) of this rank's share of an operator and its halo plan."""
+        v = _lib.amg_dist_view()
+        check(lib().amg_dist_view_get(self._h, level, op, C.byref(v)))
+        out = dict(nranks=v.nranks, replicated=bool(v.replicated))
+        if v.replicated:
+            return out
+        nr = v.nranks
+        def arr(ptr, n):
+            if n <= 0 or not ptr:  # empty std::vector -> NULL data pointer
+                return np.zeros(0, dtype={C.c_int64: np.int64, C.c_int32: np.int32}[ptr._type_])
+            return np.ctypeslib.as_array(ptr, shape=(n,)).copy()
+        rp, ci, val, shape = _lib.csr_to_numpy(v.local)
+        out.update(full_cols=bool(v.full_cols), row_begin=v.row_begin, row_end=v.row_end,
+                   col_begin=v.col_begin, col_end=v.col_end, ghost=arr(v.ghost, v.n_ghost),
+                   send_count=arr(v.send_count, nr), send_off=arr(v.send_off, nr + 1),
+                   recv_count=arr(v.recv_count, nr), recv_off=arr(v.recv_off, nr + 1),
+                   local=HostCsr(rp, ci, val, shape))
+        out["send_idx"] = arr(v.send_idx, int(out["send_off"][-1]))
+        return out
 
     def op_config(self, level: int, op: int = 0) -> dict:
         c = _lib.amg_op_config()

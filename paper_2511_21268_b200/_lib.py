@@ -21,7 +21,8 @@ STATUS = {0: "AMG_OK", 1: "AMG_NOT_CONVERGED", -1: "AMG_EINVAL", -2: "AMG_ENOMEM
 EXPORTED = ["amg_iga_poisson", "amg_iga_tables", "amg_csr_free", "amg_free", "amg_params_default",
             "amg_set_allocator", "amg_setup", "amg_pcg_solve", "amg_pcg_solve_host", "amg_vcycle",
             "amg_level_apply", "amg_hierarchy_info", "amg_hierarchy_export", "amg_set_profiling",
-            "amg_get_kernel_stats", "amg_operator_config", "amg_hierarchy_free", "amg_last_error"]
+            "amg_get_kernel_stats", "amg_operator_config", "amg_nccl_unique_id", "amg_local_rows",
+            "amg_dist_view_get", "amg_hierarchy_free", "amg_last_error"]
 
 
 class AmgError(RuntimeError):
@@ -61,6 +62,15 @@ class amg_op_config(C.Structure):
                 ("tuned_us", C.c_double)]
 
 
+class amg_dist_view(C.Structure):
+    _fields_ = [("nranks", C.c_int), ("replicated", C.c_int), ("full_cols", C.c_int),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("col_begin", C.c_int64), ("col_end", C.c_int64),
+                ("n_ghost", C.c_int64), ("ghost", C.POINTER(C.c_int64)),
+                ("send_count", C.POINTER(C.c_int32)), ("send_off", C.POINTER(C.c_int32)),
+                ("send_idx", C.POINTER(C.c_int32)), ("recv_count", C.POINTER(C.c_int32)),
+                ("recv_off", C.POINTER(C.c_int32)), ("local", amg_csr)]
+
+
 _lib = None
 
 
@@ -71,6 +81,10 @@ def lib() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2511_21268_b200.build` "
                           "(there is no CPU fallback)")
+    try:  # load torch first so the library binds to the process's single libnccl.so.2 (torch's)
+        import torch  # noqa: F401
+    except Exception:  # noqa: BLE001
+        pass
     L = C.CDLL(LIB_PATH)
     vp, dp, ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)
     P = C.POINTER
@@ -91,6 +105,9 @@ def lib() -> C.CDLL:
         "amg_set_profiling": ([vp, C.c_int], C.c_int),
         "amg_get_kernel_stats": ([vp, P(amg_kernel_stats)], C.c_int),
         "amg_operator_config": ([vp, C.c_int, C.c_int, P(amg_op_config)], C.c_int),
+        "amg_nccl_unique_id": ([P(C.c_ubyte)], C.c_int),
+        "amg_local_rows": ([vp, P(C.c_int64), P(C.c_int64)], C.c_int),
+        "amg_dist_view_get": ([vp, C.c_int, C.c_int, P(amg_dist_view)], C.c_int),
         "amg_hierarchy_free": ([vp], None),
         "amg_last_error": ([], C.c_char_p),
     }

@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "libamg_b200.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
-HOST_SRCS = ["api.cpp", "iga_gen.cpp", "setup.cpp"]
+HOST_SRCS = ["api.cpp", "iga_gen.cpp", "setup.cpp", "dist.cpp"]
 CUDA_SRCS = ["device.cu"]
 HEADERS = ["common.hpp", "kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                   "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off", "-I", INCLUDE, "-c", s, "-o", o], verbose)
     if force or _newer(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-lquadmath",
+        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-lquadmath", "-lnccl",
               "-lcudart"], verbose)
         os.replace(tmp, LIB)
     return LIB

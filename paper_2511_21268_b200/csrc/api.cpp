@@ -129,10 +129,18 @@ amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist 
     if (prm.agg_steps < 1 || prm.cheb_degree < 1 || prm.coarse_sweeps < 0 || prm.max_levels < 1 ||
         prm.coarse_size < 1 || !(prm.filter_theta >= 0.0))
         throw Error{AMG_EINVAL, "bad parameter"};
+    if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+        throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
     amg_hierarchy *H = new amg_hierarchy();
     try {
         build_hierarchy(*K, prm, H->host);
-        if (!prm.host_only) H->dev = dev_create(H->host, dist);
+        if (dist && dist->nranks > 1) {
+            int64_t rep = 7000000;  // replicate levels below ~7e6 non-zeros
+            if (const char *e = std::getenv("AMG_REPLICATE_NNZ")) rep = std::atoll(e);
+            build_dist_plan(H->host, dist->rank, dist->nranks, rep, H->plan);
+            H->distributed = true;
+        }
+        if (!prm.host_only) H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
     } catch (...) {
         delete H;
         throw;
@@ -189,6 +197,39 @@ amg_status amg_hierarchy_export(const amg_hierarchy *H, int level, amg_csr **K_l
         std::memcpy(*dhat, L.dhat.data(), sizeof(double) * L.N);
     }
     if (omega) *omega = L.omega;
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist_view *v) {
+    API_BEGIN
+    if (!H || !v || !H->distributed) throw Error{AMG_EINVAL, "hierarchy is not distributed"};
+    if (level < 0 || level >= H->host.nlevels || op < 0 || op > 2) throw Error{AMG_EINVAL, "bad level/op"};
+    if (op > 0 && level == H->host.nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
+    const DistLevel &D = H->plan.lev[level];
+    std::memset(v, 0, sizeof(*v));
+    v->nranks = H->plan.nranks;
+    v->replicated = D.replicated ? 1 : 0;
+    if (D.replicated) return AMG_OK;
+    const LocalOp &L = op == 0 ? D.K : op == 1 ? D.P : D.R;
+    v->full_cols = L.full_cols ? 1 : 0;
+    v->row_begin = L.row_begin;
+    v->row_end = L.row_end;
+    v->col_begin = L.col_begin;
+    v->col_end = L.col_end;
+    v->n_ghost = (int64_t)L.ghost.size();
+    v->ghost = L.ghost.data();
+    v->send_count = L.send_count.data();
+    v->send_off = L.send_off.data();
+    v->send_idx = L.send_idx.data();
+    v->recv_count = L.recv_count.data();
+    v->recv_off = L.recv_off.data();
+    v->local.n_rows = L.A.nrows;
+    v->local.n_cols = L.A.ncols;
+    v->local.nnz = L.A.nnz();
+    v->local.row_ptr = const_cast<int64_t *>(L.A.rp.data());
+    v->local.col = const_cast<int32_t *>(L.A.ci.data());
+    v->local.val = const_cast<double *>(L.A.v.data());
     return AMG_OK;
     API_END
 }

@@ -7,6 +7,7 @@
 #include <new>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "amg_b200.h"
 
@@ -80,6 +81,36 @@ struct HHierarchy {
     HLevel lev[32];
 };
 
+// ---- multi-GPU plumbing (dist.cpp) ------------------------------------------------------------
+// One rank's share of a distributed operator: its rows [row_begin, row_end), columns renumbered as
+// [owned columns (global col_begin..col_end-1) | ghost columns (ascending global ids)], and the halo
+// plan that fills the ghost slots.  Ghosts owned by rank q are contiguous (global order = rank order).
+struct LocalOp {
+    int64_t row_begin = 0, row_end = 0;
+    int64_t col_begin = 0, col_end = 0;  // owned column range; full_cols: [0, ncols)
+    bool full_cols = false;              // columns index a replicated (whole) vector: no ghosts
+    HCsr A;                              // local rows x (owned + ghost) columns
+    std::vector<int64_t> ghost;          // global ids of the ghost columns
+    std::vector<int32_t> send_count, send_off, send_idx;  // per destination rank; local owned indices
+    std::vector<int32_t> recv_count, recv_off;            // per source rank; offsets into the ghost area
+};
+
+struct DistLevel {
+    bool replicated = false;       // whole level on every rank (coarse levels)
+    std::vector<int64_t> bounds;   // row partition (nranks+1) of the level (also for replicated levels)
+    LocalOp K, P, R;               // R: rows = this level's coarse rows partition of level l+1
+};
+
+struct DistPlan {
+    int rank = 0, nranks = 1;
+    int last_dist = 0;             // last distributed level (levels > last_dist are replicated)
+    DistLevel lev[32];
+};
+
+// Row partition of every level balanced by nnz, the replication cut, and this rank's local
+// operators + halo plans.  Deterministic; identical on every rank given the same hierarchy.
+void build_dist_plan(const HHierarchy &H, int rank, int nranks, int64_t replicate_nnz, DistPlan &P);
+
 // iga_gen.cpp
 void iga_tables_hat(int p, int n, double *mhat, double *khat);
 void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F);
@@ -89,7 +120,7 @@ void build_hierarchy(const amg_csr &K, const amg_params &prm, HHierarchy &H);
 
 // device.cu
 struct DevState;
-DevState *dev_create(const HHierarchy &H, const amg_dist *dist);
+DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *plan);
 void dev_destroy(DevState *D);
 
 }  // namespace amgb
@@ -97,4 +128,6 @@ void dev_destroy(DevState *D);
 struct amg_hierarchy {
     amgb::HHierarchy host;
     amgb::DevState *dev = nullptr;
+    amgb::DistPlan plan;  // host view of this rank's share (multi-GPU setups)
+    bool distributed = false;
 };

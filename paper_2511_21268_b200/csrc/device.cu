@@ -5,6 +5,7 @@
 // Everything is device-resident after amg_setup: per iteration the host only enqueues kernels and
 // reads back one 64-byte scalar block (‖r‖² and breakdown flags) for the convergence test.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -53,11 +54,19 @@ struct DCsr {
     int U = 4;     // CSR cores: pairs per lane per round trip (CSR2) / chunk of 32·U pairs (CSR4T)
     int kern = 0;  // CSR layouts: 0 = register-batched k_csr2, 1 = TMA-staged k_csr4t (needs 4-padding)
     float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
+    // halo plan (multi-GPU): ghost slots [nown, nown + nghost) of the gathered vector
+    bool halo = false;
+    int64_t nown = 0, nghost = 0, nsend = 0;
+    int *sidx = nullptr;     // device: local owned indices to send, by destination rank
+    double *sbuf = nullptr;  // device: packed send buffer
+    std::vector<int> hs_count, hs_off, hr_count, hr_off;  // halo send/recv counts and offsets per rank
 };
 
 struct DLevel {
-    int64_t N = 0;
+    int64_t N = 0;    // global rows
+    int64_t n = 0;    // rows held by this rank (N when replicated or on one GPU)
     int64_t nnz = 0;  // unpadded nnz(K_l)
+    bool replicated = false;
     DCsr K, P, R;
     double *invd = nullptr;
     double *b = nullptr, *x = nullptr, *r = nullptr, *d[2] = {nullptr, nullptr};
@@ -70,6 +79,13 @@ struct DevState {
     int m = 4;
     int sweeps = 30;
     DLevel lev[32];
+    // multi-GPU (one process per GPU; NCCL over NVLink/NVSwitch)
+    int rank = 0, nranks = 1, last_dist = 0;
+    ncclComm_t comm = nullptr;
+    int64_t row_begin0 = 0, row_end0 = 0;  // this rank's rows of level 0 (global ids)
+    double *ag_send = nullptr, *ag_recv = nullptr;  // all-gather into the first replicated level
+    int64_t ag_stride = 0;
+    int64_t *ag_bounds = nullptr;                   // device copy of that level's row partition
     std::vector<DevBuf> bufs;
     // PCG vectors and scalars
     double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
@@ -124,6 +140,7 @@ struct DevState {
         for (auto &s : seg)
             if (s.exec) cudaGraphExecDestroy(s.exec);
         if (cap) cudaStreamDestroy(cap);
+        if (comm) ncclCommDestroy(comm);
     }
 };
 
@@ -329,10 +346,23 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
     CUDA_OK(cudaGetLastError());
 }
 
-// Setup-time autotuning of one CSR4-layout operator: time y = A·x for every (kernel, G, U) candidate
-// and keep the fastest.  All candidates sum each row in the same order, so the choice changes speed,
-// never results.  Small operators (latency-bound) keep the heuristic choice.
-void autotune_op(DevState &D, DCsr &A, double *x, double *y) {
+// Setup-time autotuning of one CSR4-layout operator: time it with the epilogue it runs in the V-cycle
+// (role 0: K_l with the fused Chebyshev step, 1: P̄_l with prolongation, 2: R_l with restriction) for
+// every (kernel, G, U) candidate and keep the fastest.  All candidates sum each row in the same order,
+// so the choice changes speed, never results.  Small operators (latency-bound) keep the heuristic.
+template <class Epi>
+float time_op(DevState &D, DCsr &A, const double *x, const Epi &e, cudaEvent_t e0, cudaEvent_t e1) {
+    launch_csr(D, A, x, e, nullptr);
+    CUDA_OK(cudaEventRecord(e0, nullptr));
+    for (int rep = 0; rep < 3; rep++) launch_csr(D, A, x, e, nullptr);
+    CUDA_OK(cudaEventRecord(e1, nullptr));
+    CUDA_OK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+    return ms;
+}
+
+void autotune_op(DevState &D, DCsr &A, int role, double *x, double *y1, double *y2, double *y3) {
     if (A.fmt != 0 || A.nnz < 2000000) return;
     if (std::getenv("AMG_CSR_G") || std::getenv("AMG_CSR_U")) return;
     if (const char *e = std::getenv("AMG_AUTOTUNE"))
@@ -352,14 +382,19 @@ void autotune_op(DevState &D, DCsr &A, double *x, double *y) {
                 A.kern = kern;
                 A.G = G;
                 A.U = U;
-                dev::EpiStore e{y};
-                launch_csr(D, A, x, e, nullptr);
-                CUDA_OK(cudaEventRecord(e0, nullptr));
-                for (int rep = 0; rep < 3; rep++) launch_csr(D, A, x, e, nullptr);
-                CUDA_OK(cudaEventRecord(e1, nullptr));
-                CUDA_OK(cudaEventSynchronize(e1));
-                float ms = 0.f;
-                CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+                float ms;
+                if (role == 0) {
+                    dev::EpiCheb<false> e{};
+                    e.rin = y1; e.rout = y1; e.dold = x; e.dnew = y2; e.invd = y3;
+                    e.xin = y3; e.dpend = nullptr; e.xout = y3; e.bdot = nullptr; e.a = 0.5; e.bc = 0.5;
+                    ms = time_op(D, A, x, e, e0, e1);
+                } else if (role == 1) {
+                    dev::EpiProlong e{y1};
+                    ms = time_op(D, A, x, e, e0, e1);
+                } else {
+                    dev::EpiRestrict e{y1, y3, y2, 1.0};
+                    ms = time_op(D, A, x, e, e0, e1);
+                }
                 if (ms < best) {
                     best = ms;
                     bk = kern;
@@ -390,19 +425,50 @@ struct ProfScope {
                 D.ev.push_back(e);
             }
         }
-        CUDA_OK(cudaEventRecord(D.ev[D.ev_used], st));
+        // External: inside stream capture this becomes a real event-record node of the graph, so
+        // the pair can be timed after every graph launch
+        CUDA_OK(cudaEventRecordWithFlags(D.ev[D.ev_used], st, cudaEventRecordExternal));
     }
     ~ProfScope() {
         if (!on) return;
-        cudaEventRecord(D.ev[D.ev_used + 1], st);
+        cudaEventRecordWithFlags(D.ev[D.ev_used + 1], st, cudaEventRecordExternal);
         D.ev_used += 2;
     }
 };
 
+#define NCCL_OK(call)                                                                              \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            throw Error{AMG_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)};            \
+    } while (0)
+
+// a12: fill the ghost slots of x (the vector A gathers) from their owning ranks — pack the owned
+// entries others need, then one grouped NCCL send/recv per neighbour straight into the ghost area.
+void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
+    if (!A.halo) return;
+    if (A.nsend > 0) {
+        dev::k_pack<<<grid_for(D, A.nsend), dev::kBlock, 0, st>>>(A.nsend, A.sidx, x, A.sbuf);
+        D.launches_total++;
+    }
+    NCCL_OK(ncclGroupStart());
+    for (int q = 0; q < D.nranks; q++) {
+        if (A.hs_count[q]) NCCL_OK(ncclSend(A.sbuf + A.hs_off[q], (size_t)A.hs_count[q], ncclFloat64, q, D.comm, st));
+        if (A.hr_count[q]) NCCL_OK(ncclRecv(x + A.nown + A.hr_off[q], (size_t)A.hr_count[q], ncclFloat64, q, D.comm, st));
+    }
+    NCCL_OK(ncclGroupEnd());
+}
+
+// a12: sum a per-rank dot-product partial across ranks, in place in the device scalar block.
+void allreduce_slot(DevState &D, double *slot, cudaStream_t st) {
+    if (D.nranks > 1) NCCL_OK(ncclAllReduce(slot, slot, 1, ncclFloat64, ncclSum, D.comm, st));
+}
+
 const double kC0 = 4.0 / 3.0;
 
 // c.16 pre-smoothing steps i = 1..m-1 and the residual (a4, a5), restriction (a6), recursion,
-// prolongation (a8), post-smoothing (a9, a10).  b, x: this level's right-hand side and output.
+// prolongation (a8), post-smoothing (a9, a10).  b, x: this level's right-hand side and output
+// (this rank's rows; ghost slots are filled by halo() before every gathering kernel).
 void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot) {
     DLevel &L = D.lev[l];
     const int m = D.m;
@@ -418,12 +484,13 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
     const bool coarse_is_last = (l + 1 == D.nlevels - 1);
     // --- pre-smoothing from x = 0: d0 = c0·b·invd (level 0 here; coarse levels: restrict epilogue)
     if (l == 0) {
-        dev::k_cheb_first<<<grid_for(D, L.N), dev::kBlock, 0, st>>>(L.N, b, L.invd, L.d[0], kC0);
+        dev::k_cheb_first<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, b, L.invd, L.d[0], kC0);
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
     }
     int cur = 0;
     for (int i = 1; i < m; i++) {
+        halo(D, L.K, L.d[cur], st);
         dev::EpiCheb<false> e{};
         e.rin = (i == 1) ? b : L.r;
         e.rout = L.r;
@@ -441,6 +508,7 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
     }
     // residual r = r − K d_{m−1}   (m == 1: r = b − K d0, x = d0)
     {
+        halo(D, L.K, L.d[cur], st);
         dev::EpiResidualFrom e{};
         e.b = (m == 1) ? b : L.r;
         e.r = L.r;
@@ -449,7 +517,26 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         launch_csr(D, L.K, L.d[cur], e, st);
     }
     // restriction b_c = R r, fused with the coarse level's first smoothing step d0_c = c0·b_c·invd_c
-    {
+    halo(D, L.R, L.r, st);
+    if (C.replicated && !L.replicated) {
+        // last distributed level: each rank restricts its share of the coarse rows, then an
+        // all-gather assembles the whole coarse right-hand side on every rank
+        dev::EpiRestrict e{};
+        e.bc = D.ag_send;
+        e.invd = nullptr;
+        e.d0 = nullptr;
+        e.c0 = kC0;
+        launch_csr(D, L.R, L.r, e, st);
+        NCCL_OK(ncclAllGather(D.ag_send, D.ag_recv, (size_t)D.ag_stride, ncclFloat64, D.comm, st));
+        dev::k_unpack_allgather<<<grid_for(D, D.ag_stride), dev::kBlock, 0, st>>>(D.nranks, D.ag_stride,
+                                                                                D.ag_bounds, D.ag_recv, C.b);
+        D.launches_total++;
+        if (!coarse_is_last) {
+            dev::k_cheb_first<<<grid_for(D, C.n), dev::kBlock, 0, st>>>(C.n, C.b, C.invd, C.d[0], kC0);
+            D.launches_total++;
+        }
+        CUDA_OK(cudaGetLastError());
+    } else {
         dev::EpiRestrict e{};
         e.bc = C.b;
         e.invd = coarse_is_last ? nullptr : C.invd;
@@ -460,12 +547,14 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
     vcycle_level(D, l + 1, C.b, C.x, st, dev::DOT_NONE);
     // prolongation x += P̄ x_c
     {
+        halo(D, L.P, C.x, st);
         dev::EpiProlong e{};
         e.x = x;
         launch_csr(D, L.P, C.x, e, st);
     }
     // post-smoothing: r = b − K x; d0 = c0·r·invd
     {
+        halo(D, L.K, x, st);
         dev::EpiPostFirst e{};
         e.b = b;
         e.r = L.r;
@@ -479,6 +568,7 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         const bool last = (i == m - 1) && final_dot != dev::DOT_NONE;
         const double a = (double)(2 * i - 1) / (double)(2 * i + 3);
         const double bcf = (double)(8 * i + 4) / (double)(2 * i + 3);
+        halo(D, L.K, L.d[cur], st);
         ProfScope ps(D, st, l == 0);
         if (last) {
             dev::EpiCheb<true> e{};
@@ -494,7 +584,7 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         cur ^= 1;
     }
     if (m == 1) {
-        dev::k_axpy1<<<grid_for(D, L.N), dev::kBlock, 0, st>>>(L.N, L.d[0], x);
+        dev::k_axpy1<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, L.d[0], x);
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
     }
@@ -502,28 +592,45 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
 
 }  // namespace
 
-// V-cycle with the rᵀz dot (kind) fused into the last level-0 post-smoothing step.
+// V-cycle with the rᵀz dot (kind) fused into the last level-0 post-smoothing step (then summed
+// across ranks).
 static void vcycle(DevState &D, const double *b, double *x, cudaStream_t st, int dotkind) {
-    if (D.nlevels == 1) {
-        vcycle_level(D, 0, b, x, st, dev::DOT_NONE);
-        if (dotkind != dev::DOT_NONE) {
-            dev::k_dot<<<grid_for(D, D.lev[0].N), dev::kBlock, 0, st>>>(D.lev[0].N, b, x, dotctx(D, dotkind));
-            D.launches_total++;
-        }
-        return;
-    }
-    const bool fused = dotkind != dev::DOT_NONE && D.m > 1;
+    const int64_t n0 = D.lev[0].n;
+    const bool fused = dotkind != dev::DOT_NONE && D.m > 1 && D.nlevels > 1;
     vcycle_level(D, 0, b, x, st, fused ? dotkind : dev::DOT_NONE);
     if (dotkind != dev::DOT_NONE && !fused) {
-        dev::k_dot<<<grid_for(D, D.lev[0].N), dev::kBlock, 0, st>>>(D.lev[0].N, b, x, dotctx(D, dotkind));
+        dev::k_dot<<<grid_for(D, n0), dev::kBlock, 0, st>>>(n0, b, x, dotctx(D, dotkind));
         D.launches_total++;
     }
+    if (dotkind == dev::DOT_RZ) allreduce_slot(D, &D.S->rz, st);
 }
 
-DevState *dev_create(const HHierarchy &H, const amg_dist *dist) {
+namespace {
+// Upload one rank's share of a distributed operator (local columns + halo plan).
+void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format) {
+    upload_op(D, op.A, out, false, format, false);
+    if (op.full_cols || D.nranks == 1) return;
+    out.halo = true;
+    out.nown = op.col_end - op.col_begin;
+    out.nghost = (int64_t)op.ghost.size();
+    out.hs_count.assign(op.send_count.begin(), op.send_count.end());
+    out.hs_off.assign(op.send_off.begin(), op.send_off.end());
+    out.hr_count.assign(op.recv_count.begin(), op.recv_count.end());
+    out.hr_off.assign(op.recv_off.begin(), op.recv_off.end());
+    out.nsend = (int64_t)op.send_idx.size();
+    if (out.nsend > 0) {
+        out.sidx = D.alloc_n<int>(out.nsend);
+        out.sbuf = D.alloc_n<double>(out.nsend);
+        CUDA_OK(cudaMemcpy(out.sidx, op.send_idx.data(), sizeof(int) * out.nsend, cudaMemcpyHostToDevice));
+    }
+}
+}  // namespace
+
+DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *planp) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw Error{AMG_ENODEV, "no CUDA device"};
-    if (dist && dist->nranks > 1) throw Error{AMG_EINVAL, "multi-GPU hierarchies are not built by this version"};
+    if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+        throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
     auto D = new DevState();
     try {
         int dev_id = 0;
@@ -543,50 +650,109 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist) {
         D->m = H.prm.cheb_degree;
         D->sweeps = H.prm.coarse_sweeps;
         if (const char *e = std::getenv("AMG_GRAPHS")) D->graphs = std::atoi(e) != 0;
+        const int nr = dist ? dist->nranks : 1;
+        D->rank = dist ? dist->rank : 0;
+        D->nranks = nr;
+        if (nr > 1 && (!planp || planp->nranks != nr)) throw Error{AMG_EINVAL, "missing distribution plan"};
+        const DistPlan &plan = *planp;
+        if (nr > 1) {
+            D->last_dist = plan.last_dist;
+            ncclUniqueId id;
+            static_assert(sizeof(id) == sizeof(dist->nccl_id), "ncclUniqueId size");
+            std::memcpy(&id, dist->nccl_id, sizeof(id));
+            NCCL_OK(ncclCommInitRank(&D->comm, nr, id, D->rank));
+        } else {
+            D->last_dist = H.nlevels - 1;
+        }
+        const int fmt = H.prm.format;
         for (int l = 0; l < H.nlevels; l++) {
             const HLevel &h = H.lev[l];
             DLevel &L = D->lev[l];
             L.N = h.N;
             L.nnz = h.K.nnz();
             const bool coarsest = (l + 1 == H.nlevels);
-            upload_op(*D, h.K, L.K, true, H.prm.format, coarsest);
-            if (!coarsest) {
-                upload_op(*D, h.P, L.P, false, H.prm.format, false);
-                upload_op(*D, h.R, L.R, false, H.prm.format, false);
+            L.replicated = nr > 1 && l > D->last_dist;
+            int64_t r0 = 0;
+            if (nr > 1 && !L.replicated) {
+                const DistLevel &P = plan.lev[l];
+                r0 = P.K.row_begin;
+                L.n = P.K.row_end - P.K.row_begin;
+                upload_local(*D, P.K, L.K, fmt);
+                if (!coarsest) {
+                    upload_local(*D, P.P, L.P, fmt);
+                    upload_local(*D, P.R, L.R, fmt);
+                }
+            } else {
+                L.n = h.N;
+                upload_op(*D, h.K, L.K, true, fmt, coarsest);
+                if (!coarsest) {
+                    upload_op(*D, h.P, L.P, false, fmt, false);
+                    upload_op(*D, h.R, L.R, false, fmt, false);
+                }
             }
-            Buf<double> invd(h.N);
-            for (int64_t i = 0; i < h.N; i++) invd[i] = 1.0 / h.dhat[i];
-            L.invd = D->alloc_n<double>(h.N);
-            CUDA_OK(cudaMemcpy(L.invd, invd.data(), sizeof(double) * h.N, cudaMemcpyHostToDevice));
-            L.b = D->alloc_n<double>(h.N);
-            L.x = D->alloc_n<double>(h.N);
-            L.r = D->alloc_n<double>(h.N);
-            L.d[0] = D->alloc_n<double>(h.N);
-            L.d[1] = D->alloc_n<double>(h.N);
+            Buf<double> invd(L.n);
+            for (int64_t i = 0; i < L.n; i++) invd[i] = 1.0 / h.dhat[r0 + i];
+            L.invd = D->alloc_n<double>(L.n);
+            CUDA_OK(cudaMemcpy(L.invd, invd.data(), sizeof(double) * L.n, cudaMemcpyHostToDevice));
+            // vectors gathered by K_l, R_l (fine side) or P̄_{l-1} (coarse side) need ghost capacity
+            int64_t cap = L.n + std::max(L.K.nghost, L.R.nghost);
+            if (l > 0) cap = std::max(cap, L.n + D->lev[l - 1].P.nghost);
+            L.b = D->alloc_n<double>(cap);
+            L.x = D->alloc_n<double>(cap);
+            L.r = D->alloc_n<double>(cap);
+            L.d[0] = D->alloc_n<double>(cap);
+            L.d[1] = D->alloc_n<double>(cap);
         }
         const HLevel &hl = H.lev[H.nlevels - 1];
         if (hl.N > 3072) throw Error{AMG_EINVAL, "coarsest level larger than 3072 rows (raise max_levels)"};
-        const int64_t N0 = H.lev[0].N;
-        D->r = D->alloc_n<double>(N0);
-        D->z = D->alloc_n<double>(N0);
-        D->p = D->alloc_n<double>(N0);
-        D->q = D->alloc_n<double>(N0);
+        if (nr > 1) {
+            const int lr = D->last_dist + 1;  // first replicated level
+            const std::vector<int64_t> &bd = plan.lev[lr].bounds;
+            for (int q = 0; q < nr; q++) D->ag_stride = std::max(D->ag_stride, bd[q + 1] - bd[q]);
+            D->ag_send = D->alloc_n<double>(D->ag_stride);
+            D->ag_recv = D->alloc_n<double>(D->ag_stride * nr);
+            D->ag_bounds = D->alloc_n<int64_t>(nr + 1);
+            CUDA_OK(cudaMemcpy(D->ag_bounds, bd.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice));
+            D->row_begin0 = plan.lev[0].K.row_begin;
+            D->row_end0 = plan.lev[0].K.row_end;
+        } else {
+            D->row_begin0 = 0;
+            D->row_end0 = H.lev[0].N;
+        }
+        const int64_t n0 = D->lev[0].n, cap0 = n0 + D->lev[0].K.nghost;
+        D->r = D->alloc_n<double>(n0);
+        D->z = D->alloc_n<double>(cap0);
+        D->p = D->alloc_n<double>(cap0);
+        D->q = D->alloc_n<double>(n0);
         D->partials = D->alloc_n<double>(D->max_grid + 32);
         D->counter = D->alloc_n<unsigned>(4);
         D->S = D->alloc_n<dev::Scalars>(1);
         CUDA_OK(cudaMemset(D->counter, 0, 4 * sizeof(unsigned)));
         CUDA_OK(cudaMemset(D->S, 0, sizeof(dev::Scalars)));
         CUDA_OK(cudaMallocHost(&D->hS, sizeof(dev::Scalars)));
-        D->bytes_dominant = 12.0 * (double)H.lev[0].K.nnz() + 64.0 * (double)N0;
-        if (H.prm.format == 0) {  // autotune every large operator (x = r, y = z scratch, N0 >= any size)
-            CUDA_OK(cudaMemset(D->r, 0, sizeof(double) * N0));
-            for (int l = 0; l < D->nlevels; l++) {
-                autotune_op(*D, D->lev[l].K, D->r, D->z);
-                if (l + 1 < D->nlevels) {
-                    autotune_op(*D, D->lev[l].P, D->r, D->z);
-                    autotune_op(*D, D->lev[l].R, D->r, D->z);
+        D->bytes_dominant = 12.0 * (double)D->lev[0].K.nnz + 64.0 * (double)n0;
+        if (fmt == 0) {  // autotune every large operator on scratch vectors
+            int64_t big = 1;
+            for (int l = 0; l < D->nlevels; l++)
+                for (const DCsr *A : {&D->lev[l].K, &D->lev[l].P, &D->lev[l].R})
+                    big = std::max(big, std::max(A->nrows, A->ncols));
+            double *scr = nullptr;  // x, y1, y2, y3 scratch vectors
+            CUDA_OK(cudaMalloc(&scr, sizeof(double) * big * 4));
+            CUDA_OK(cudaMemset(scr, 0, sizeof(double) * big * 4));
+            double *sx = scr, *y1 = scr + big, *y2 = scr + 2 * big, *y3 = scr + 3 * big;
+            try {
+                for (int l = 0; l < D->nlevels; l++) {
+                    autotune_op(*D, D->lev[l].K, 0, sx, y1, y2, y3);
+                    if (l + 1 < D->nlevels) {
+                        autotune_op(*D, D->lev[l].P, 1, sx, y1, y2, y3);
+                        autotune_op(*D, D->lev[l].R, 2, sx, y1, y2, y3);
+                    }
                 }
+            } catch (...) {
+                cudaFree(scr);
+                throw;
             }
+            cudaFree(scr);
         }
         CUDA_OK(cudaDeviceSynchronize());
     } catch (...) {
@@ -615,16 +781,20 @@ static void prof_collect(DevState &D, size_t ev0 = 0, size_t ev1 = (size_t)-1, b
 // memory.  No host decision inside, so it is captured once into a CUDA graph and replayed.
 static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
     DLevel &L0 = D.lev[0];
-    const int64_t N = L0.N;
-    vcycle(D, D.r, D.z, st, kind == 0 ? dev::DOT_RZ_INIT : dev::DOT_RZ);
-    dev::k_p_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.z, D.p, D.S, kind == 0 ? 1 : 0);
-    D.launches_total++;
+    const int64_t n = L0.n;
+    vcycle(D, D.r, D.z, st, dev::DOT_RZ);  // ρ = rᵀz (all-reduced)
+    dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0);
+    dev::k_roll_rho<<<1, 1, 0, st>>>(D.S);
+    D.launches_total += 2;
     {
+        halo(D, L0.K, D.p, st);
         dev::EpiSpmvDot e{D.p, D.q};
         launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ);
+        allreduce_slot(D, &D.S->pq, st);
     }
-    dev::k_pcg_update<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR));
+    dev::k_pcg_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR));
     D.launches_total++;
+    allreduce_slot(D, &D.S->rr, st);
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
 }
@@ -682,20 +852,24 @@ static void run_segment(DevState &D, int kind, double *u, cudaStream_t st) {
 static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int maxit, cudaStream_t st, int *iters,
                       double *relres, double *hist) {
     DLevel &L0 = D.lev[0];
-    const int64_t N = L0.N;
+    const int64_t N = L0.n;  // this rank's rows
     *iters = 0;
     *relres = 0.0;
     CUDA_OK(cudaMemsetAsync(D.S, 0, sizeof(dev::Scalars), st));
     // ‖F‖²
     dev::k_dot<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, F, F, dotctx(D, dev::DOT_FF));
     D.launches_total++;
-    // r = F − K u ; ‖r‖²
+    allreduce_slot(D, &D.S->ff, st);
+    // r = F − K u ; ‖r‖²   (u is copied into z, which has the ghost slots K_0 gathers)
     {
+        CUDA_OK(cudaMemcpyAsync(D.z, u, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+        halo(D, L0.K, D.z, st);
         dev::EpiResidualFrom e{F, D.r, nullptr, nullptr};
-        launch_csr(D, L0.K, u, e, st);
+        launch_csr(D, L0.K, D.z, e, st);
     }
     dev::k_dot<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.r, D.r, dotctx(D, dev::DOT_RR));
     D.launches_total++;
+    allreduce_slot(D, &D.S->rr, st);
     CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
     const double nF = std::sqrt(D.hS->ff);
@@ -714,7 +888,7 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     for (int k = 1; k <= maxit; k++) {
         // iteration k: [z = V(r); ρ = rᵀz; p = z + βp] then q = Kp, α, u += αp, r −= αq, ‖r‖²
         run_segment(D, k == 1 ? 0 : 1, u, st);
-        if (D.hS->flags) {
+        if (!(D.hS->rz > 0.0) || !(D.hS->pq > 0.0)) {  // CG breakdown: rᵀz <= 0 or pᵀKp <= 0
             *iters = k;
             return AMG_ENOTSPD;
         }
@@ -785,7 +959,7 @@ extern "C" amg_status amg_pcg_solve_host(amg_hierarchy *H, const double *F, doub
     DevState *D = need_dev(H);
     if (!F || !u || !iters || !relres || maxit < 0 || !(rtol >= 0.0)) throw Error{AMG_EINVAL, "bad argument"};
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t N = D->lev[0].N;
+    const int64_t N = D->lev[0].n;  // this rank's rows
     if (!D->stage) D->stage = D->alloc_n<double>(2 * N);
     double *dF = D->stage, *dU = D->stage + N;
     CUDA_OK(cudaMemcpyAsync(dF, F, sizeof(double) * N, cudaMemcpyHostToDevice, st));
@@ -814,8 +988,29 @@ extern "C" amg_status amg_level_apply(amg_hierarchy *H, int level, int op, const
     if (op > 0 && level == D->nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
     DLevel &L = D->lev[level];
     const DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
+    if (A.halo) throw Error{AMG_EINVAL, "amg_level_apply: operator is distributed (use a single-GPU hierarchy)"};
     dev::EpiStore e{y};
     launch_csr(*D, A, x, e, (cudaStream_t)stream);
+    return AMG_OK;
+    API_END
+}
+
+extern "C" amg_status amg_nccl_unique_id(unsigned char id[128]) {
+    API_BEGIN
+    if (!id) throw Error{AMG_EINVAL, "NULL id"};
+    ncclUniqueId u;
+    NCCL_OK(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+    return AMG_OK;
+    API_END
+}
+
+extern "C" amg_status amg_local_rows(amg_hierarchy *H, int64_t *row_begin, int64_t *row_end) {
+    API_BEGIN
+    DevState *D = need_dev(H);
+    if (!row_begin || !row_end) throw Error{AMG_EINVAL, "NULL argument"};
+    *row_begin = D->row_begin0;
+    *row_end = D->row_end0;
     return AMG_OK;
     API_END
 }

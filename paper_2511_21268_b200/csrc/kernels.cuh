@@ -20,19 +20,19 @@ namespace dev {
 
 constexpr int kBlock = 256;
 
+// Device scalar block.  Reductions only deposit sums (per rank; the multi-GPU path all-reduces the
+// slot right after the kernel); consumers derive α = ρ/pᵀq and β = ρ/ρ_prev themselves, so the
+// same kernels serve 1 and N GPUs.  The host reads the whole block once per iteration.
 struct Scalars {
     double ff;       // F·F
     double rr;       // r·r (after the CG update)
     double pq;       // pᵀKp
-    double rho;      // rᵀz (current)
-    double rho_new;  // rᵀz (new)
-    double alpha;    // ρ/(pᵀq)
-    double beta;     // ρ_new/ρ
-    int flags;       // bit0: pᵀq <= 0, bit1: rᵀz <= 0
-    int pad;
+    double rz;       // ρ = rᵀz of the current iteration
+    double rz_prev;  // ρ of the previous iteration (set at the end of each iteration)
+    double pad[3];
 };
 
-enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ_INIT, DOT_RZ };
+enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ };
 
 struct DotCtx {
     double *partials;    // >= gridDim.x
@@ -82,21 +82,8 @@ __device__ __forceinline__ void block_dot_finalize_n(double v, const DotCtx &dc)
         switch (dc.kind) {
             case DOT_FF: S->ff = s; break;
             case DOT_RR: S->rr = s; break;
-            case DOT_PQ:
-                S->pq = s;
-                S->alpha = S->rho / s;
-                if (!(s > 0.0)) S->flags |= 1;
-                break;
-            case DOT_RZ_INIT:
-                S->rho = s;
-                if (!(s > 0.0)) S->flags |= 2;
-                break;
-            case DOT_RZ:
-                S->rho_new = s;
-                S->beta = s / S->rho;
-                S->rho = s;
-                if (!(s > 0.0)) S->flags |= 2;
-                break;
+            case DOT_PQ: S->pq = s; break;
+            case DOT_RZ: S->rz = s; break;
             default: break;
         }
         *dc.counter = 0u;
@@ -529,11 +516,11 @@ __global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const double *__restr
     block_dot_finalize(s, dc);
 }
 
-// a2: u += α p; r −= α q; ‖r‖² (α from device scalars, computed by the spmv_dot last block)
+// a2: u += α p; r −= α q; ‖r‖² with α = ρ/pᵀq from the (all-reduced) device scalars
 __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *__restrict__ p,
                                                         const double *__restrict__ q, double *__restrict__ u,
                                                         double *__restrict__ r, DotCtx dc) {
-    const double alpha = dc.S->alpha;
+    const double alpha = dc.S->rz / dc.S->pq;
     double s = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         u[i] = u[i] + alpha * p[i];
@@ -544,12 +531,33 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *
     block_dot_finalize(s, dc);
 }
 
-// a11: p = z + β p  (first: p = z)
+// a11: p = z + β p with β = ρ/ρ_prev  (first iteration: p = z)
 __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                                                       const Scalars *__restrict__ S, int first) {
-    const double beta = first ? 0.0 : S->beta;
+    const double beta = first ? 0.0 : S->rz / S->rz_prev;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
         p[i] = first ? z[i] : z[i] + beta * p[i];
+}
+
+// end of a PCG iteration: ρ_prev <- ρ (one thread; after every consumer of ρ in this iteration)
+__global__ void k_roll_rho(Scalars *S) { S->rz_prev = S->rz; }
+
+// gather/scatter helpers of the multi-GPU path
+__global__ void __launch_bounds__(kBlock) k_pack(int64_t n, const int *__restrict__ idx, const double *__restrict__ x,
+                                                  double *__restrict__ buf) {
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        buf[i] = x[idx[i]];
+}
+// recv (nranks x stride) -> full[bounds[q] + i] for i < bounds[q+1]-bounds[q]
+__global__ void __launch_bounds__(kBlock) k_unpack_allgather(int nranks, int64_t stride,
+                                                              const int64_t *__restrict__ bounds,
+                                                              const double *__restrict__ recv,
+                                                              double *__restrict__ full) {
+    for (int q = 0; q < nranks; q++) {
+        const int64_t b = bounds[q], c = bounds[q + 1] - b;
+        for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < c; i += (int64_t)gridDim.x * kBlock)
+            full[b + i] = recv[q * stride + i];
+    }
 }
 
 // a7: coarsest level, `sweeps` ℓ1-Jacobi sweeps from x = 0, one CTA, x double-buffered in shared memory.

@@ -1,0 +1,122 @@
+"""Multi-GPU host logic on the CPU: world_size-2 gloo processes build the same hierarchy, take their
+row blocks and halo plans from the library (amg_dist_view_get), exchange ghost values over gloo exactly
+as the device path does over NCCL, and check
+
+* the row blocks of every level tile [0, N_l) contiguously;
+* every local row maps back (owned / ghost column numbering) to the global row, bitwise;
+* the halo exchange delivers exactly x[ghost ids];
+* the distributed product equals the global product on every owned row.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, rep_nnz, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        os.environ["AMG_REPLICATE_NNZ"] = str(rep_nnz)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2511_21268_b200 as amg
+        import amg_inputs
+        dim, p, n = case
+        K, F = amg.iga_poisson(dim, p, n)
+        H = amg.Hierarchy(K, amg.params(p, host_only=1), dist=amg.make_dist(rank, world, nccl_id=bytes(128)))
+        info = H.info()
+        checked = 0
+        for l in range(info["levels"]):
+            e = H.export(l)
+            Kg = e["K"].to_scipy()
+            ops = [(0, Kg)]
+            if e["P"] is not None:
+                Pg = e["P"].to_scipy()
+                ops += [(1, Pg), (2, Pg.T.tocsr())]
+            for op, A in ops:
+                v = H.dist_view(l, op)
+                if v["replicated"]:
+                    continue
+                # row blocks tile the level
+                rb = torch.tensor([v["row_begin"], v["row_end"]], dtype=torch.int64)
+                allb = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+                dist.all_gather(allb, rb)
+                allb = [t.tolist() for t in allb]
+                assert allb[0][0] == 0 and allb[-1][1] == A.shape[0]
+                assert all(allb[k][1] == allb[k + 1][0] for k in range(world - 1))
+                loc = v["local"].to_scipy()
+                nown = v["col_end"] - v["col_begin"]
+                ghost = v["ghost"]
+                # local -> global column map reproduces the global rows bitwise
+                gmap = np.concatenate([np.arange(v["col_begin"], v["col_end"]), ghost]) if not v["full_cols"] \
+                    else np.arange(A.shape[1])
+                Ar = A[v["row_begin"]:v["row_end"]]
+                assert np.array_equal(gmap[loc.indices], Ar.indices) and np.array_equal(loc.indptr, Ar.indptr)
+                assert np.array_equal(loc.data.view(np.uint64), Ar.data.view(np.uint64))
+                # halo exchange over gloo
+                x = amg_inputs.uniform_pm1(A.shape[1], seed=100 + 10 * l + op)
+                if v["full_cols"]:
+                    xl = x
+                else:
+                    xown = x[v["col_begin"]:v["col_end"]]
+                    ghosts = np.full(len(ghost), np.nan)
+                    reqs, bufs = [], []
+                    for r in range(world):
+                        if r == rank:
+                            continue
+                        s0, sc = v["send_off"][r], v["send_count"][r]
+                        sb = torch.from_numpy(np.ascontiguousarray(xown[v["send_idx"][s0:s0 + sc]]))
+                        rbuf = torch.zeros(int(v["recv_count"][r]), dtype=torch.float64)
+                        if sc:
+                            reqs.append(dist.isend(sb, r))
+                        if len(rbuf):
+                            reqs.append(dist.irecv(rbuf, r))
+                        bufs.append((r, rbuf, sb))
+                    for rq in reqs:
+                        rq.wait()
+                    for r, rbuf, _ in bufs:
+                        o = v["recv_off"][r]
+                        ghosts[o:o + len(rbuf)] = rbuf.numpy()
+                    assert np.array_equal(ghosts, x[ghost])
+                    xl = np.concatenate([xown, ghosts])
+                y = loc @ xl
+                yref = Ar @ x
+                assert np.abs(y - yref).max() <= 1e-14 * (abs(Ar) @ np.abs(x)).max()
+                checked += 1
+        dist.barrier()
+        q.put((rank, "ok", checked))
+    except Exception as ex:  # noqa: BLE001
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,rep_nnz", [((3, 2, 12), 1000), ((3, 3, 10), 20000), ((2, 2, 16), 100)])
+def test_partition_and_halo_plans_world2(case, rep_nnz):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, rep_nnz, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, status, detail in res:
+        assert status == "ok", detail
+        assert detail >= 3  # at least K_0, P̄_0, R_0 were distributed and checked

@@ -1,0 +1,95 @@
+"""Multi-GPU solve (NCCL halos + all-reduced dots) vs the single-GPU solve and the oracle.
+
+Needs >= 2 GPUs (skipped otherwise; run with `gpurun --gpus 2`).  Each rank is a process on its own GPU.
+The distributed hierarchy is the global one (host setup is global), every row sum is bitwise the 1-GPU
+one, and only the dot-product reduction order differs, so the iteration count must match within ±1
+and the iterate after the same number of iterations within 1e-10 (SURVEY §4 multi-GPU strategy).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, rep_nnz, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        os.environ["AMG_REPLICATE_NNZ"] = str(rep_nnz)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+        import paper_2511_21268_b200 as amg
+        import amg_inputs
+        dim, p, n = case
+        K, F = amg.iga_poisson(dim, p, n)
+        H = amg.Hierarchy(K, amg.params(p), dist=amg.make_dist(rank, world, device=rank))
+        b, e = H.local_rows()
+        out = {}
+        for name, rhs in (("sine", F), ("random", amg_inputs.uniform_pm1(K.shape[0]))):
+            Fl = torch.from_numpy(np.ascontiguousarray(rhs[b:e])).cuda()
+            u, it, rr, hist, st = H.solve(Fl, rtol=1e-6)
+            u2, it2, _, hist2, _ = H.solve(Fl, rtol=0.0, maxit=8)
+            parts = [None] * world
+            dist.all_gather_object(parts, (b, e, u.cpu().numpy(), u2.cpu().numpy()))
+            out[name] = (it, st, hist, parts)
+        if rank == 0:
+            ref = {}
+            H1 = amg.Hierarchy(K, amg.params(p))
+            for name, rhs in (("sine", F), ("random", amg_inputs.uniform_pm1(K.shape[0]))):
+                Fd = torch.from_numpy(rhs).cuda()
+                u, it, rr, hist, st = H1.solve(Fd, rtol=1e-6)
+                u2 = H1.solve(Fd, rtol=0.0, maxit=8)[0]
+                ref[name] = (it, u.cpu().numpy(), u2.cpu().numpy(), hist)
+            q.put(("ok", out, ref, K.shape[0]))
+        dist.barrier()
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("fail", traceback.format_exc(), None, None))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case,rep_nnz", [((3, 3, 12), 100000), ((3, 2, 32), 200000), ((3, 2, 20), 10 ** 12)])
+def test_distributed_solve_matches_single_gpu(world, case, rep_nnz):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, rep_nnz, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, out, ref, N = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert status == "ok", out
+    for name in ("sine", "random"):
+        it, st, hist, parts = out[name]
+        it1, u1, u1_8, hist1 = ref[name]
+        assert st == 0 and abs(it - it1) <= 1
+        u = np.zeros(N)
+        u8 = np.zeros(N)
+        for b, e, ul, ul8 in parts:
+            u[b:e] = ul
+            u8[b:e] = ul8
+        assert np.linalg.norm(u8 - u1_8) <= 1e-10 * np.linalg.norm(u1_8)
+        if it == it1:
+            assert np.linalg.norm(u - u1) <= 1e-10 * np.linalg.norm(u1)
+        assert np.allclose(hist[: min(len(hist), len(hist1))], hist1[: min(len(hist), len(hist1))], rtol=1e-8)
