@@ -1,6 +1,6 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel.
 
-    python tools/summarize_launches.py gpurun_out/launches_c3.csv [--md]
+    python tools/summarize_launches.py gpurun_out/launches_c3.csv [--md] [--solve-only]
 Groups by the demangled kernel name (template arguments kept, namespaces stripped) and grid size,
 prints count, total and mean µs, and the share of the total device time.
 """
@@ -26,6 +26,10 @@ def short(name: str) -> str:
 def main():
     path = sys.argv[1]
     rows = [r for r in load(path) if r["Metric Name"] == "gpu__time_duration.sum"]
+    if "--solve-only" in sys.argv:
+        # drop the setup-time autotuning launches: a solve starts with the ‖F‖² k_dot
+        first = next(i for i, r in enumerate(rows) if "k_dot" in r["Kernel Name"])
+        rows = rows[first:]
     agg = defaultdict(lambda: [0, 0.0])
     total = 0.0
     for r in rows:
