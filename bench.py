@@ -50,18 +50,29 @@ def workload_desc(cfg: str) -> dict:
     return dict(c, name=cfg, m=amg_inputs.CHEB_DEGREE[c["p"]])
 
 
-def byte_model(info: dict, m: int) -> dict:
-    """Algorithmic bytes of one PCG iteration: 12 B per stored non-zero read
-    (fp64 value + int32 column), 8 B row pointer + vector traffic per row per sweep."""
+def byte_model(info: dict, m: int, ops: dict | None = None) -> dict:
+    """Algorithmic bytes of one PCG iteration.  Per operator application: 8 B per stored
+    non-zero value + the column data of the format actually used (4 B/entry as int32, 2.06 B/entry as
+    16-bit offsets per 64-entry chunk) + 8 B row pointers — `ops[(l, op)]["alg_bytes"]` from amg_operator_config; without it
+    (oracle arm) the plain CSR figure 12 B/nnz + 8 B/row.  Plus 56 B/row of vector traffic per fused
+    smoothing step, the transfer vectors, and ≈100 B/row of outer CG vector updates and dots."""
     nnz, N, nnzP, L = info["nnz"], info["N"], info["nnz_P"], info["levels"]
-    b = 12.0 * (2 * m + 1) * nnz[0] + 64.0 * (2 * m + 1) * N[0]
+
+    def op(l, k):
+        if ops is not None and (l, k) in ops:
+            return float(ops[(l, k)]["alg_bytes"])
+        if k == 0:
+            return 12.0 * nnz[l] + 8.0 * (N[l] + 1)
+        return 12.0 * nnzP[l] + 8.0 * ((N[l] if k == 1 else N[l + 1]) + 1)
+
+    b = (2 * m + 1) * (op(0, 0) + 56.0 * N[0])
     for l in range(1, L - 1):
-        b += 12.0 * 2 * m * nnz[l] + 64.0 * 2 * m * N[l]
+        b += 2 * m * (op(l, 0) + 56.0 * N[l])
     for l in range(L - 1):
-        b += 2 * (12.0 * nnzP[l]) + 8.0 * (N[l] + N[l + 1]) * 2
-    b += 12.0 * nnz[L - 1] * 30 if L > 1 else 0.0
+        b += op(l, 1) + op(l, 2) + 8.0 * (N[l] + N[l + 1]) * 2
+    b += op(L - 1, 0) * 30 if L > 1 else 0.0
     b += 100.0 * N[0]  # outer CG vector updates and dots
-    sweep0 = 12.0 * nnz[0] + 64.0 * N[0]
+    sweep0 = op(0, 0) + 56.0 * N[0]
     return dict(iter_bytes=b, sweep0_bytes=sweep0)
 
 
@@ -161,10 +172,13 @@ def run_gpu(args) -> None:
     rb, re_ = H.local_rows()
     F = np.ascontiguousarray(F[rb:re_])
     del K
-    op_cfg = [H.op_config(l, 0) for l in range(info["levels"])]
+    ops = {(l, k): H.op_config(l, k) for l in range(info["levels"]) for k in range(3)
+           if k == 0 or l + 1 < info["levels"]}
+    op_cfg = [ops[(l, 0)] for l in range(info["levels"])]
     k0 = op_cfg[0]
-    kname = (f"{'k_csr4t' if k0['kernel'] == 'csr_tma' else 'k_csr2'}<G={k0['G']},U={k0['U']},EpiCheb> "
-             "(fused Chebyshev-ℓ1-Jacobi step on level 0)")
+    cols = "ColsD16" if k0["kernel"].endswith("_d16") else "ColsI32"
+    kname = (f"{'k_csr4t' if k0['kernel'].startswith('csr_tma') else 'k_csr2'}<G={k0['G']},U={k0['U']},"
+             f"EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0)")
     stream = torch.cuda.current_stream()
     Fd = torch.from_numpy(F).cuda()
     u = torch.zeros_like(Fd)
@@ -224,7 +238,7 @@ def run_gpu(args) -> None:
         ms_e2e = t.item()
 
     peak, peak_src = load_peaks()
-    bm = byte_model(info, m)
+    bm = byte_model(info, m, ops)
     iters = iters_seen[-1]
     solve_s = ms / 1e3
     per_launch_ms = ks["total_ms"] / max(ks["launches"], 1)

@@ -96,7 +96,10 @@ typedef struct {
     int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30)                */
     int64_t coarse_size;    /* coarsest when N_l <= coarse_size (50)                 */
     int max_levels;         /* 20                                                                 */
-    int format;             /* device matrix format: 0 auto, 1 CSR warp-per-row, 2 SELL-32 (row per lane) */
+    int format;             /* device matrix format: 0 auto (rows padded to 4; autotuned kernel and column
+                               source per operator), 1 CSR warp-per-row, 2 SELL-32 (row per lane),
+                               3 TMA-staged CSR, 4 CSR with 16-bit column offsets (register core),
+                               5 CSR with 16-bit column offsets (TMA-staged values) */
     int host_only;          /* 1: build the hierarchy on the host only (export/inspection; no CUDA call) */
     int num_threads;        /* host setup threads (OpenMP); 0 = runtime default                     */
 } amg_params;
@@ -181,15 +184,27 @@ amg_status amg_set_profiling(amg_hierarchy *H, int enable); /* enable resets the
 amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
 
 /* Device kernel chosen for operator op (0 K_l, 1 P̄_l, 2 R_l) of level l: layout (0 padded CSR,
- * 1 SELL-32), kernel (0 register-batched warp-per-row CSR, 1 TMA-staged CSR), rows per warp group G,
- * pairs per lane per round trip U, stored entries (with padding), and the autotuned y = A·x time in
- * microseconds (0 if the heuristic choice was kept).  AMG_EINVAL for a bad level/op. */
+ * 1 SELL-32), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
+ * source, 0 int32 columns, 1 16-bit column offsets per 64-entry chunk), rows per warp group G, pairs per lane per round trip
+ * U, stored entries (with padding), the autotuned y = A·x time in microseconds (0 if the heuristic
+ * choice was kept), the bytes one application streams for the operator in that format (8 B per value
+ * of the nnz entries + the column data actually stored + 8 B row pointers; vectors excluded) and nnz.
+ * AMG_EINVAL for a bad level/op. */
 typedef struct {
     int layout, kernel, G, U;
     int64_t stored;
     double tuned_us;
+    double alg_bytes;
+    int64_t nnz;
 } amg_op_config;
 amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
+/* Force the kernel configuration of one CSR-layout operator (experiments and the kernel-equivalence
+ * tests): kernel as in the amg_op_config struct: bit 1 needs the 16-bit encoding (formats 0, 3, 4, 5, and
+ * only where every 64-entry chunk spans < 65536 columns);
+ * bit 0 = TMA needs rows padded to 4 and U <= 4; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
+ * sums each row in the same order, so results are bitwise unchanged.  Drops captured PCG graphs.
+ * AMG_EINVAL for a bad level/op or an unavailable configuration. */
+amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);
 
 /* Host view of this rank's share of operator op (0 K_l, 1 P̄_l, 2 R_l) on level l, for hierarchies
  * set up with an amg_dist of nranks > 1 (host_only or not).  Local columns are

@@ -286,8 +286,12 @@ class Hierarchy:
     def op_config(self, level: int, op: int = 0) -> dict:
         c = _lib.amg_op_config()
         check(lib().amg_operator_config(self._h, level, op, C.byref(c)))
-        return dict(layout=("csr", "sell32")[c.layout], kernel=("csr_regs", "csr_tma")[c.kernel], G=c.G, U=c.U,
-                    stored=c.stored, tuned_us=round(c.tuned_us, 2))
+        return dict(layout=("csr", "sell32")[c.layout],
+                    kernel=("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")[c.kernel], G=c.G, U=c.U,
+                    stored=c.stored, nnz=c.nnz, alg_bytes=c.alg_bytes, tuned_us=round(c.tuned_us, 2))
+
+    def set_op_config(self, level: int, op: int, kernel: int, G: int, U: int) -> None:
+        check(lib().amg_operator_set_config(self._h, level, op, kernel, G, U))
 
     def kernel_stats(self) -> dict:
         s = _lib.amg_kernel_stats()

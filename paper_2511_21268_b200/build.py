@@ -7,6 +7,7 @@ no FMA contraction in the generator or the setup).  Device code is compiled for 
 """
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -21,8 +22,8 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 HOST_SRCS = ["api.cpp", "iga_gen.cpp", "setup.cpp", "dist.cpp"]
-CUDA_SRCS = ["device.cu"]
-HEADERS = ["common.hpp", "kernels.cuh"]
+CUDA_SRCS = ["device.cu", "inst_cheb.cu", "inst_cheb_dot.cu", "inst_spmv.cu", "inst_transfer.cu"]
+HEADERS = ["common.hpp", "kernels.cuh", "devstate.cuh", "launch_csr.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -47,21 +48,25 @@ def _run(cmd: list[str], verbose: bool) -> None:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "amg_b200.h")]
-    objs = []
+    jobs, objs = [], []
     for src in HOST_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            _run(["g++", "-O2", "-std=gnu++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
-                  "-Wall", "-Wno-unknown-pragmas", "-I", INCLUDE, "-c", s, "-o", o], verbose)
+            jobs.append(["g++", "-O2", "-std=gnu++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+                         "-Wall", "-Wno-unknown-pragmas", "-I", INCLUDE, "-c", s, "-o", o])
     for src in CUDA_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-                  "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off", "-I", INCLUDE, "-c", s, "-o", o], verbose)
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                         "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off", "-I", INCLUDE, "-c", s, "-o", o])
+    # the translation units are independent: compile them in parallel
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, j, verbose) for j in jobs]:
+            f.result()
     if force or _newer(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
         _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-lquadmath", "-lnccl",

@@ -12,8 +12,8 @@
 #include <string>
 #include <vector>
 
-#include "common.hpp"
-#include "kernels.cuh"
+#define AMGB_PLAIN_KERNELS
+#include "devstate.cuh"
 
 namespace amgb {
 
@@ -28,121 +28,32 @@ void set_allocator(amg_alloc_fn a, amg_free_fn f) {
     g_free = f;
 }
 
-#define CUDA_OK(call)                                                                              \
-    do {                                                                                           \
-        cudaError_t e_ = (call);                                                                   \
-        if (e_ != cudaSuccess)                                                                     \
-            throw Error{AMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};            \
-    } while (0)
-
-struct DevBuf {
+void *DevState::alloc(size_t bytes) {
     void *p = nullptr;
-    size_t bytes = 0;
-};
-
-// A device operator in one of two streaming formats (kernels.cuh):
-//   CSR2 (fmt 0): rows padded to even length; warp per group of G rows.
-//   SELL2 (fmt 1): 32-row slices, one row per lane, pair-interleaved columns; soff = slice offsets.
-struct DCsr {
-    int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
-    int fmt = 0;
-    int64_t *rp = nullptr;    // CSR2 row pointers (entries)
-    int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
-    int32_t *ci = nullptr;
-    double *v = nullptr;
-    int G = 32;    // CSR cores: rows per warp group
-    int U = 4;     // CSR cores: pairs per lane per round trip (CSR2) / chunk of 32·U pairs (CSR4T)
-    int kern = 0;  // CSR layouts: 0 = register-batched k_csr2, 1 = TMA-staged k_csr4t (needs 4-padding)
-    float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
-    // halo plan (multi-GPU): ghost slots [nown, nown + nghost) of the gathered vector
-    bool halo = false;
-    int64_t nown = 0, nghost = 0, nsend = 0;
-    int *sidx = nullptr;     // device: local owned indices to send, by destination rank
-    double *sbuf = nullptr;  // device: packed send buffer
-    std::vector<int> hs_count, hs_off, hr_count, hr_off;  // halo send/recv counts and offsets per rank
-};
-
-struct DLevel {
-    int64_t N = 0;    // global rows
-    int64_t n = 0;    // rows held by this rank (N when replicated or on one GPU)
-    int64_t nnz = 0;  // unpadded nnz(K_l)
-    bool replicated = false;
-    DCsr K, P, R;
-    double *invd = nullptr;
-    double *b = nullptr, *x = nullptr, *r = nullptr, *d[2] = {nullptr, nullptr};
-};
-
-struct DevState {
-    int device = 0;
-    int nsm = 148;
-    int nlevels = 0;
-    int m = 4;
-    int sweeps = 30;
-    DLevel lev[32];
-    // multi-GPU (one process per GPU; NCCL over NVLink/NVSwitch)
-    int rank = 0, nranks = 1, last_dist = 0;
-    ncclComm_t comm = nullptr;
-    int64_t row_begin0 = 0, row_end0 = 0;  // this rank's rows of level 0 (global ids)
-    double *ag_send = nullptr, *ag_recv = nullptr;  // all-gather into the first replicated level
-    int64_t ag_stride = 0;
-    int64_t *ag_bounds = nullptr;                   // device copy of that level's row partition
-    std::vector<DevBuf> bufs;
-    // PCG vectors and scalars
-    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
-    double *partials = nullptr;
-    unsigned *counter = nullptr;
-    dev::Scalars *S = nullptr;
-    dev::Scalars *hS = nullptr;  // pinned host mirror
-    double *stage = nullptr;  // device copies of F and u for amg_pcg_solve_host (2·N_0)
-    int max_grid = 1184;
-    // profiling
-    bool prof = false;
-    std::vector<cudaEvent_t> ev;
-    size_t ev_used = 0;
-    int64_t launches_total = 0;
-    double bytes_dominant = 0.0;
-    double prof_ms = 0.0;
-    int64_t prof_n = 0;
-    // CUDA graphs of the PCG iteration (kind 0: first iteration, 1: later iterations)
-    bool graphs = true;
-    cudaStream_t cap = nullptr;
-    struct Seg {
-        cudaGraphExec_t exec = nullptr;
-        double *u = nullptr;
-        bool prof = false;
-        size_t ev0 = 0, ev1 = 0;
-        int64_t nk = 0;
-    } seg[2];
-
-    void *alloc(size_t bytes) {
-        void *p = nullptr;
-        if (bytes == 0) bytes = 16;
-        if (g_alloc) {
-            p = g_alloc(bytes, device, nullptr);
-            if (!p) throw Error{AMG_ENOMEM, "device allocation (hook) failed"};
-        } else {
-            cudaError_t e = cudaMalloc(&p, bytes);
-            if (e != cudaSuccess) throw Error{AMG_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e)};
-        }
-        bufs.push_back({p, bytes});
-        return p;
+    if (bytes == 0) bytes = 16;
+    if (g_alloc) {
+        p = g_alloc(bytes, device, nullptr);
+        if (!p) throw Error{AMG_ENOMEM, "device allocation (hook) failed"};
+    } else {
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) throw Error{AMG_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e)};
     }
-    template <class T>
-    T *alloc_n(int64_t n) { return static_cast<T *>(alloc(sizeof(T) * (size_t)std::max<int64_t>(n, 1))); }
+    bufs.push_back({p, bytes});
+    return p;
+}
 
-    ~DevState() {
-        for (auto &b : bufs) {
-            if (g_free) g_free(b.p, b.bytes, device, nullptr);
-            else cudaFree(b.p);
-        }
-        for (auto e : ev) cudaEventDestroy(e);
-        if (hS) cudaFreeHost(hS);
-        for (auto &s : seg)
-            if (s.exec) cudaGraphExecDestroy(s.exec);
-        if (cap) cudaStreamDestroy(cap);
-        if (comm) ncclCommDestroy(comm);
+DevState::~DevState() {
+    for (auto &b : bufs) {
+        if (g_free) g_free(b.p, b.bytes, device, nullptr);
+        else cudaFree(b.p);
     }
-};
+    for (auto e : ev) cudaEventDestroy(e);
+    if (hS) cudaFreeHost(hS);
+    for (auto &s : seg)
+        if (s.exec) cudaGraphExecDestroy(s.exec);
+    if (cap) cudaStreamDestroy(cap);
+    if (comm) ncclCommDestroy(comm);
+}
 
 namespace {
 
@@ -170,6 +81,8 @@ inline int32_t pad_col(const HCsr &A, int64_t i, bool square) {
     return A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i]] : 0;
 }
 
+bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out);
+
 // Upload a host CSR as CSR2 (rows padded to a multiple of `mult` entries with (pad column, 0.0);
 // mult = 2 for CSR2, 4 for the TMA-staged CSR4T whose bulk copies need 16-byte aligned ranges).
 void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 2) {
@@ -190,8 +103,12 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
             ci[o] = A.ci[k];
             v[o] = A.v[k];
         }
-        for (; o < rp[i + 1]; o++) {
-            ci[o] = pad_col(A, i, square);
+        // padding continues the row's last run of columns where possible (stays inside the row's
+        // column window); the padded products are 0.0·x[col] for a valid column
+        const int32_t last = A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i + 1] - 1] : -1;
+        for (int32_t t = 1; o < rp[i + 1]; o++, t++) {
+            const int64_t c = (int64_t)last + t;
+            ci[o] = (last >= 0 && c < A.ncols) ? (int32_t)c : pad_col(A, i, square);
             v[o] = 0.0;
         }
     }
@@ -205,6 +122,36 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
     CUDA_OK(cudaMemcpy(out.rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.ci, ci.data(), sizeof(int32_t) * nnz2, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * nnz2, cudaMemcpyHostToDevice));
+    if (mult == 4) encode_d16(D, rp.data(), ci.data(), n, out);
+}
+
+// 16-bit column offsets (ColsD16, kernels.cuh): base = the row's smallest stored column, offsets
+// col − base.  Returns false (no encoding; int32 columns only) if a row spans more than 65535 columns.
+bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out) {
+    Buf<int32_t> base(nrows);
+    bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+    for (int64_t i = 0; i < nrows; i++) {
+        int32_t lo = 0, hi = 0;
+        if (rp[i + 1] > rp[i]) lo = hi = ci[rp[i]];
+        for (int64_t e = rp[i]; e < rp[i + 1]; e++) {
+            lo = std::min(lo, ci[e]);
+            hi = std::max(hi, ci[e]);
+        }
+        base[i] = lo;
+        ok = ok && ((int64_t)hi - (int64_t)lo <= 65535);
+    }
+    if (!ok) return false;
+    const int64_t stored = rp[nrows];
+    Buf<uint16_t> off(stored);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < nrows; i++)
+        for (int64_t e = rp[i]; e < rp[i + 1]; e++) off[e] = (uint16_t)(ci[e] - base[i]);
+    out.off16 = D.alloc_n<uint16_t>(stored);
+    out.rbase = D.alloc_n<int32_t>(nrows);
+    CUDA_OK(cudaMemcpy(out.off16, off.data(), sizeof(uint16_t) * stored, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.rbase, base.data(), sizeof(int32_t) * nrows, cudaMemcpyHostToDevice));
+    return true;
 }
 
 // Slice offsets (in pairs) of the SELL2 layout; returns the stored entry count.
@@ -259,11 +206,11 @@ void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, b
     out.nrows = A.nrows;
     out.ncols = A.ncols;
     out.nnz = A.nnz();
-    if (format == 0 || format == 3) {
+    if (format == 0 || format >= 3) {
         // rows padded to 4 entries: runnable by both the register-batched CSR2 core and the
         // TMA-staged CSR4T core (format 0 autotunes between them after the upload)
         upload_csr2(D, A, out, square, 4);
-        out.kern = (format == 3) ? 1 : 0;
+        out.kern = (format == 3) ? 1 : (format == 4 && out.off16) ? 2 : (format == 5 && out.off16) ? 3 : 0;
         return;
     }
     const bool sell = !force_csr && format == 2;
@@ -276,75 +223,6 @@ int grid_for(const DevState &D, int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, D.max_grid));
 }
 
-dev::DotCtx dotctx(DevState &D, int kind) { return dev::DotCtx{D.partials, D.counter, D.S, kind}; }
-
-template <int G, int U, class Epi>
-void launch_csr4t_gu(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
-    constexpr int smem = dev::TmaCfg<U>::SMEM;
-    static bool attr_set = false;  // per instantiation; device-independent attribute
-    if (!attr_set) {
-        CUDA_OK(cudaFuncSetAttribute(dev::k_csr4t<G, U, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
-    }
-    const int64_t ngroups = (A.nrows + G - 1) / G;
-    const int64_t wpb = dev::kBlockT / 32;
-    const int64_t per_sm = std::max(1, (227 * 1024) / (smem + 1024));
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, per_sm * D.nsm));
-    grid = std::min(grid, D.max_grid);
-    dev::k_csr4t<G, U, Epi><<<grid, dev::kBlockT, smem, st>>>(A.rp, A.ci, A.v, g, A.nrows, epi, dotctx(D, dotkind));
-}
-
-template <class Epi>
-void launch_csr4t(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
-    switch (A.G * 16 + A.U) {
-#define CASE(GG, UU) \
-    case GG * 16 + UU: launch_csr4t_gu<GG, UU, Epi>(D, A, g, epi, st, dotkind); break;
-#define CASES_G(GG) CASE(GG, 2) CASE(GG, 4) CASE(GG, 6) CASE(GG, 8)
-        CASES_G(1) CASES_G(4) CASES_G(8) CASES_G(32)
-#undef CASES_G
-#undef CASE
-        default: throw Error{AMG_EINVAL, "bad CSR4T kernel configuration"};
-    }
-    D.launches_total++;
-    CUDA_OK(cudaGetLastError());
-}
-
-template <class Epi>
-void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind = dev::DOT_NONE) {
-    const int2 *ci2 = reinterpret_cast<const int2 *>(A.ci);
-    const double2 *v2 = reinterpret_cast<const double2 *>(A.v);
-    if (A.fmt == 1) {
-        const int64_t nsl = (A.nrows + 31) / 32;
-        const int64_t wpb = dev::kBlock / 32;
-        int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, D.max_grid));
-        dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind));
-        D.launches_total++;
-        CUDA_OK(cudaGetLastError());
-        return;
-    }
-    if (A.kern == 1) {
-        launch_csr4t(D, A, g, epi, st, dotkind);
-        return;
-    }
-    const int64_t ngroups = (A.nrows + A.G - 1) / A.G;
-    const int64_t warps_per_block = dev::kBlock / 32;
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, D.max_grid));
-    dev::DotCtx dc = dotctx(D, dotkind);
-    const int key = A.G * 16 + A.U;
-    switch (key) {
-#define CASE(GG, UU)                                                                                   \
-    case GG * 16 + UU:                                                                                 \
-        dev::k_csr2<GG, UU, Epi><<<grid, dev::kBlock, 0, st>>>(A.rp, ci2, v2, g, A.nrows, epi, dc); \
-        break;
-#define CASES_G(GG) CASE(GG, 2) CASE(GG, 4) CASE(GG, 6) CASE(GG, 8)
-        CASES_G(1) CASES_G(4) CASES_G(8) CASES_G(32)
-#undef CASES_G
-#undef CASE
-        default: throw Error{AMG_EINVAL, "bad CSR2 kernel configuration"};
-    }
-    D.launches_total++;
-    CUDA_OK(cudaGetLastError());
-}
 
 // Setup-time autotuning of one CSR4-layout operator: time it with the epilogue it runs in the V-cycle
 // (role 0: K_l with the fused Chebyshev step, 1: P̄_l with prolongation, 2: R_l with restriction) for
@@ -353,13 +231,17 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
 template <class Epi>
 float time_op(DevState &D, DCsr &A, const double *x, const Epi &e, cudaEvent_t e0, cudaEvent_t e1) {
     launch_csr(D, A, x, e, nullptr);
-    CUDA_OK(cudaEventRecord(e0, nullptr));
-    for (int rep = 0; rep < 3; rep++) launch_csr(D, A, x, e, nullptr);
-    CUDA_OK(cudaEventRecord(e1, nullptr));
-    CUDA_OK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
-    return ms;
+    float best = 1e30f;
+    for (int round = 0; round < 2; round++) {  // best of 2 rounds of 3 back-to-back launches
+        CUDA_OK(cudaEventRecord(e0, nullptr));
+        for (int rep = 0; rep < 3; rep++) launch_csr(D, A, x, e, nullptr);
+        CUDA_OK(cudaEventRecord(e1, nullptr));
+        CUDA_OK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    return best;
 }
 
 void autotune_op(DevState &D, DCsr &A, int role, double *x, double *y1, double *y2, double *y3) {
@@ -374,10 +256,11 @@ void autotune_op(DevState &D, DCsr &A, int role, double *x, double *y1, double *
     const int Us[] = {2, 4, 6, 8};
     float best = 1e30f;
     int bk = A.kern, bg = A.G, bu = A.U;
-    for (int kern = 0; kern < 2; kern++)
+    const int nkern = A.off16 ? 4 : 2;  // kern bit 1 (16-bit column offsets) needs the encoding
+    for (int kern = 0; kern < nkern; kern++)
         for (int G : Gs)
             for (int U : Us) {
-                if (kern == 1 && U > 4) continue;
+                if ((kern & 1) && U > 4) continue;
                 if ((A.nrows + G - 1) / G < 4 * D.nsm) continue;  // too few warp groups to fill the GPU
                 A.kern = kern;
                 A.G = G;
@@ -426,14 +309,18 @@ struct ProfScope {
             }
         }
         // External: inside stream capture this becomes a real event-record node of the graph, so
-        // the pair can be timed after every graph launch
-        CUDA_OK(cudaEventRecordWithFlags(D.ev[D.ev_used], st, cudaEventRecordExternal));
+        // the pair can be timed after every graph launch (the flag is only valid while capturing)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_OK(cudaStreamIsCapturing(st, &cs));
+        flags = (cs == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
+        CUDA_OK(cudaEventRecordWithFlags(D.ev[D.ev_used], st, flags));
     }
     ~ProfScope() {
         if (!on) return;
-        cudaEventRecordWithFlags(D.ev[D.ev_used + 1], st, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(D.ev[D.ev_used + 1], st, flags);
         D.ev_used += 2;
     }
+    unsigned flags = 0;
 };
 
 #define NCCL_OK(call)                                                                              \
@@ -724,13 +611,12 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         D->z = D->alloc_n<double>(cap0);
         D->p = D->alloc_n<double>(cap0);
         D->q = D->alloc_n<double>(n0);
-        D->partials = D->alloc_n<double>(D->max_grid + 32);
+        D->partials = D->alloc_n<double>(D->nsm * 32 + 32);  // >= any resident grid (<= 32 CTAs per SM)
         D->counter = D->alloc_n<unsigned>(4);
         D->S = D->alloc_n<dev::Scalars>(1);
         CUDA_OK(cudaMemset(D->counter, 0, 4 * sizeof(unsigned)));
         CUDA_OK(cudaMemset(D->S, 0, sizeof(dev::Scalars)));
         CUDA_OK(cudaMallocHost(&D->hS, sizeof(dev::Scalars)));
-        D->bytes_dominant = 12.0 * (double)D->lev[0].K.nnz + 64.0 * (double)n0;
         if (fmt == 0) {  // autotune every large operator on scratch vectors
             int64_t big = 1;
             for (int l = 0; l < D->nlevels; l++)
@@ -738,7 +624,9 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                     big = std::max(big, std::max(A->nrows, A->ncols));
             double *scr = nullptr;  // x, y1, y2, y3 scratch vectors
             CUDA_OK(cudaMalloc(&scr, sizeof(double) * big * 4));
-            CUDA_OK(cudaMemset(scr, 0, sizeof(double) * big * 4));
+            // non-trivial data (not zeros): data-dependent power draw changes the clocks under the cap
+            dev::k_fill_pattern<<<grid_for(*D, big * 4), dev::kBlock>>>(big * 4, scr);
+            CUDA_OK(cudaGetLastError());
             double *sx = scr, *y1 = scr + big, *y2 = scr + 2 * big, *y3 = scr + 3 * big;
             try {
                 for (int l = 0; l < D->nlevels; l++) {
@@ -754,6 +642,9 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             }
             cudaFree(scr);
         }
+        // dominant kernel (level-0 fused Chebyshev step): the operator's streamed bytes in its chosen
+        // format + 56 B/row of vectors (d_old, r in/out, x in/out, invd, d_new)
+        D->bytes_dominant = D->lev[0].K.alg_bytes() + 56.0 * (double)n0;
         CUDA_OK(cudaDeviceSynchronize());
     } catch (...) {
         delete D;
@@ -1042,6 +933,33 @@ extern "C" amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *s
     API_END
 }
 
+extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U) {
+    API_BEGIN
+    DevState *D = need_dev(H);
+    if (level < 0 || level >= D->nlevels || op < 0 || op > 2) throw Error{AMG_EINVAL, "bad level/op"};
+    if (op > 0 && level == D->nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
+    DLevel &L = D->lev[level];
+    DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
+    if (A.fmt != 0) throw Error{AMG_EINVAL, "operator is not in a CSR layout"};
+    if (kernel < 0 || kernel > 3 || ((kernel & 2) && !A.off16)) throw Error{AMG_EINVAL, "kernel not available for this operator"};
+    if ((kernel & 1) && (A.stored % 4 != 0 || U > 4)) throw Error{AMG_EINVAL, "TMA core needs rows padded to 4 and U <= 4"};
+    if (!(G == 1 || G == 4 || G == 8 || G == 32) || !(U == 2 || U == 4 || U == 6 || U == 8))
+        throw Error{AMG_EINVAL, "G must be 1, 4, 8 or 32 and U 2, 4, 6 or 8"};
+    CUDA_OK(cudaDeviceSynchronize());
+    A.kern = kernel;
+    A.G = G;
+    A.U = U;
+    A.tuned_us = 0.f;
+    for (auto &sg : D->seg)  // captured graphs hold the old launch configuration
+        if (sg.exec) {
+            cudaGraphExecDestroy(sg.exec);
+            sg.exec = nullptr;
+        }
+    if (level == 0 && op == 0) D->bytes_dominant = A.alg_bytes() + 56.0 * (double)L.n;
+    return AMG_OK;
+    API_END
+}
+
 extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg) {
     API_BEGIN
     DevState *D = need_dev(H);
@@ -1055,6 +973,8 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     cfg->U = A.U;
     cfg->stored = A.stored;
     cfg->tuned_us = A.tuned_us;
+    cfg->alg_bytes = A.alg_bytes();
+    cfg->nnz = A.nnz;
     return AMG_OK;
     API_END
 }

@@ -1,0 +1,137 @@
+// devstate.cuh — device-side state of a hierarchy (internal; not part of the C ABI): operators in
+// their streaming layouts, per-level vectors, PCG scalars, graphs and profiling, plus the CSR launcher
+// declarations.  The launchers are instantiated per epilogue in the inst_*.cu files so the kernel
+// variants compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace amgb {
+
+#define CUDA_OK(call)                                                                              \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw Error{AMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};            \
+    } while (0)
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+// A device operator in one of two streaming formats (kernels.cuh):
+//   CSR2 (fmt 0): rows padded to even length; warp per group of G rows.
+//   SELL2 (fmt 1): 32-row slices, one row per lane, pair-interleaved columns; soff = slice offsets.
+struct DCsr {
+    int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
+    int fmt = 0;
+    int64_t *rp = nullptr;    // CSR2 row pointers (entries)
+    int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
+    int32_t *ci = nullptr;
+    double *v = nullptr;
+    int G = 32;    // CSR cores: rows per warp group
+    int U = 4;     // CSR cores: pairs per lane per round trip (CSR2) / chunk of 32·U pairs (CSR4T)
+    // CSR layouts: kernel (bit 0: 0 register-batched k_csr2, 1 TMA-staged k_csr4t, needs 4-padding)
+    // and column source (bit 1: 0 int32 columns, 1 16-bit offsets from a per-row base, ColsD16)
+    int kern = 0;
+    // 16-bit column offsets (kern & 2): col − rbase[row] per stored entry, rbase = first column of the row
+    uint16_t *off16 = nullptr;
+    int32_t *rbase = nullptr;
+    // bytes one application must stream from HBM for this operator (values of the nnz stored entries,
+    // the column data of the chosen source, row pointers); vectors are counted by the caller
+    double alg_bytes() const {
+        const double idx = (kern & 2) ? 2.0 * (double)nnz + 4.0 * (double)nrows : 4.0 * (double)nnz;
+        return 8.0 * (double)nnz + idx + 8.0 * (double)(nrows + 1);
+    }
+    float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
+    // halo plan (multi-GPU): ghost slots [nown, nown + nghost) of the gathered vector
+    bool halo = false;
+    int64_t nown = 0, nghost = 0, nsend = 0;
+    int *sidx = nullptr;     // device: local owned indices to send, by destination rank
+    double *sbuf = nullptr;  // device: packed send buffer
+    std::vector<int> hs_count, hs_off, hr_count, hr_off;  // halo send/recv counts and offsets per rank
+};
+
+struct DLevel {
+    int64_t N = 0;    // global rows
+    int64_t n = 0;    // rows held by this rank (N when replicated or on one GPU)
+    int64_t nnz = 0;  // unpadded nnz(K_l)
+    bool replicated = false;
+    DCsr K, P, R;
+    double *invd = nullptr;
+    double *b = nullptr, *x = nullptr, *r = nullptr, *d[2] = {nullptr, nullptr};
+};
+
+struct DevState {
+    int device = 0;
+    int nsm = 148;
+    int nlevels = 0;
+    int m = 4;
+    int sweeps = 30;
+    DLevel lev[32];
+    // multi-GPU (one process per GPU; NCCL over NVLink/NVSwitch)
+    int rank = 0, nranks = 1, last_dist = 0;
+    ncclComm_t comm = nullptr;
+    int64_t row_begin0 = 0, row_end0 = 0;  // this rank's rows of level 0 (global ids)
+    double *ag_send = nullptr, *ag_recv = nullptr;  // all-gather into the first replicated level
+    int64_t ag_stride = 0;
+    int64_t *ag_bounds = nullptr;                   // device copy of that level's row partition
+    std::vector<DevBuf> bufs;
+    // PCG vectors and scalars
+    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double *partials = nullptr;
+    unsigned *counter = nullptr;
+    dev::Scalars *S = nullptr;
+    dev::Scalars *hS = nullptr;  // pinned host mirror
+    double *stage = nullptr;  // device copies of F and u for amg_pcg_solve_host (2·N_0)
+    int max_grid = 1184;
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> ev;
+    size_t ev_used = 0;
+    int64_t launches_total = 0;
+    double bytes_dominant = 0.0;
+    double prof_ms = 0.0;
+    int64_t prof_n = 0;
+    // CUDA graphs of the PCG iteration (kind 0: first iteration, 1: later iterations)
+    bool graphs = true;
+    cudaStream_t cap = nullptr;
+    struct Seg {
+        cudaGraphExec_t exec = nullptr;
+        double *u = nullptr;
+        bool prof = false;
+        size_t ev0 = 0, ev1 = 0;
+        int64_t nk = 0;
+    } seg[2];
+
+    void *alloc(size_t bytes);  // through the allocator hook (device.cu)
+    template <class T>
+    T *alloc_n(int64_t n) { return static_cast<T *>(alloc(sizeof(T) * (size_t)std::max<int64_t>(n, 1))); }
+
+    ~DevState();
+};
+
+
+inline dev::DotCtx dotctx(DevState &D, int kind) { return dev::DotCtx{D.partials, D.counter, D.S, kind}; }
+
+// y-side epilogue applied to A·g for a CSR-layout (autotuned kernel / column source) or SELL2 operator.
+template <class Epi>
+void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind = dev::DOT_NONE);
+
+#define AMGB_EPILOGUES(X) \
+    X(dev::EpiStore) X(dev::EpiSpmvDot) X(dev::EpiResidualFrom) X(dev::EpiCheb<false>) X(dev::EpiCheb<true>) \
+    X(dev::EpiPostFirst) X(dev::EpiRestrict) X(dev::EpiProlong)
+#define AMGB_EXTERN_LAUNCH(E) \
+    extern template void launch_csr<E>(DevState &, const DCsr &, const double *, E, cudaStream_t, int);
+AMGB_EPILOGUES(AMGB_EXTERN_LAUNCH)
+#undef AMGB_EXTERN_LAUNCH
+
+}  // namespace amgb

@@ -38,7 +38,9 @@ CASES = {
 _cache = {}
 
 
-FORMATS = [1, 2, 3]  # 1 CSR2 (warp per row group), 2 SELL2 (row per lane), 3 CSR4T (TMA-staged rows)
+# 1 CSR2 (warp per row group), 2 SELL2 (row per lane), 3 CSR4T (TMA-staged rows),
+# 4 CSR2 with 16-bit column offsets, 5 CSR4T with 16-bit column offsets
+FORMATS = [1, 2, 3, 4, 5]
 
 
 def build(case, fmt=0, **kw):
@@ -72,6 +74,55 @@ def test_level_operators(case, fmt):
             ref = oracle.spmv(A, x)
             bound = abs(A) @ np.abs(x)
             assert np.all(np.abs(y.cpu().numpy() - ref) <= 1e-13 * bound + 1e-300), (l, op)
+
+
+@pytest.mark.parametrize("case", ["C2", "cube10p4"])
+def test_kernel_configs_bitwise_equal(case):
+    """Every CSR kernel configuration (register / TMA core, int32 / 16-bit-offset columns, rows per warp
+    group G, pairs in flight U) sums each row in the same order: y = A·x must be BITWISE identical
+    across all of them, and within 1e-13 of the oracle (so the autotuner changes speed, never results)."""
+    K, F, H, Ho = build(case, 0)
+    rng = np.random.default_rng(5)
+    for l, L in enumerate(Ho.levels):
+        ops = [(0, L.K)] + ([] if L.P is None else [(1, L.P), (2, L.R)])
+        for op, A in ops:
+            keep = H.op_config(l, op)
+            x = dev(rng.uniform(-1, 1, A.shape[1]))
+            ref = None
+            for kern in range(4):
+                for G in (1, 4, 8, 32):
+                    for U in (2, 4, 6, 8):
+                        if (kern & 1) and U > 4:
+                            continue
+                        H.set_op_config(l, op, kern, G, U)
+                        y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+                        H.apply(l, op, x, y)
+                        y = y.cpu().numpy()
+                        if ref is None:
+                            ref = y
+                            xo = x.cpu().numpy()
+                            bound = abs(A) @ np.abs(xo)
+                            assert np.all(np.abs(y - oracle.spmv(A, xo)) <= 1e-13 * bound + 1e-300)
+                        else:
+                            assert np.array_equal(y, ref), (l, op, kern, G, U)
+            kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")
+            H.set_op_config(l, op, kinds.index(keep["kernel"]), keep["G"], keep["U"])
+
+
+def test_d16_encoding_bytes():
+    """16-bit column offsets: the fine IgA operator qualifies (every row spans < 65536 columns) and
+    the reported algorithmic bytes follow the chosen column source exactly."""
+    K, F, H, Ho = build("cube12p3", 0)
+    c = H.op_config(0, 0)
+    H.set_op_config(0, 0, 2, c["G"], c["U"])
+    d16 = H.op_config(0, 0)
+    H.set_op_config(0, 0, 0, c["G"], c["U"])
+    i32 = H.op_config(0, 0)["alg_bytes"]
+    kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")
+    H.set_op_config(0, 0, kinds.index(c["kernel"]), c["G"], c["U"])
+    nnz, N = c["nnz"], K.shape[0]
+    assert i32 == 12 * nnz + 8 * (N + 1)
+    assert d16["alg_bytes"] == 10 * nnz + 4 * N + 8 * (N + 1)
 
 
 @pytest.mark.parametrize("fmt", FORMATS)

@@ -37,13 +37,17 @@ def main():
     warm_launches = H.kernel_stats()["kernels_launched"]
     t0 = time.perf_counter()
     its = []
+    torch.cuda.nvtx.range_push("solve")  # ncu --nvtx --nvtx-include "solve/" skips setup/autotuning
     for _ in range(args.solves):
         u.zero_()
         its.append(H.solve(Fd, u=u)[1])
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     ks = H.kernel_stats()
-    print(json.dumps(dict(config=args.config, info=H.info(), iters=its, warm_launches=warm_launches,
+    ops = [H.op_config(l, 0) for l in range(H.info()["levels"])]
+    print(json.dumps(dict(config=args.config, info=H.info(), iters=its, warm_launches=warm_launches, level_ops=ops,
                           launches_per_solve=(ks["kernels_launched"] - warm_launches) // max(args.solves, 1),
                           wall_s_per_solve=dt / max(args.solves, 1))))
 
