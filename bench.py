@@ -276,7 +276,11 @@ def run_gpu(args) -> None:
                 "opc": round(info["opc"], 4), "cheb_degree": m, "coarse_sweeps": 30, "format": args.format,
                 "level_kernels": op_cfg,
                 "cuda_graphs": os.environ.get("AMG_GRAPHS", "1") != "0",
-                "parallelism": f"row-block x{world} (NCCL halos, replicated coarse levels)" if world > 1 else "single",
+                "parallelism": (f"row-block x{world}, replicated coarse levels, "
+                                + ("NCCL halos + all-reduces" if os.environ.get("AMG_TRANSPORT") == "nccl"
+                                   else "P2P: ghost pushes from the producing kernels into peer memory over "
+                                        "NVLink + cross-GPU kernel lock-step, no NCCL in the solve"))
+                               if world > 1 else "single",
                 "l2": "inputs exceed L2 (K0 = %.2f GB >> 126 MB); no flush needed" % (12e-9 * info["nnz"][0]),
             },
             "iters": iters,

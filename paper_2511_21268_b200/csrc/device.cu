@@ -52,6 +52,19 @@ DevState::~DevState() {
     for (auto &s : seg)
         if (s.exec) cudaGraphExecDestroy(s.exec);
     if (cap) cudaStreamDestroy(cap);
+    for (char *p : peer_slabs) cudaIpcCloseMemHandle(p);
+    if (slab) {
+        // no rank may still store into this slab: barrier over the communicator before freeing it
+        if (comm) {
+            int64_t *one = nullptr;
+            if (cudaMalloc(&one, sizeof(int64_t)) == cudaSuccess) {
+                if (ncclAllReduce(one, one, 1, ncclInt64, ncclSum, comm, nullptr) == ncclSuccess)
+                    cudaStreamSynchronize(nullptr);
+                cudaFree(one);
+            }
+        }
+        cudaFree(slab);
+    }
     if (comm) ncclCommDestroy(comm);
 }
 
@@ -330,10 +343,11 @@ struct ProfScope {
             throw Error{AMG_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)};            \
     } while (0)
 
-// a12: fill the ghost slots of x (the vector A gathers) from their owning ranks — pack the owned
-// entries others need, then one grouped NCCL send/recv per neighbour straight into the ghost area.
+// a12 (NCCL transport): fill the ghost slots of x (the vector A gathers) from their owning ranks —
+// pack the owned entries others need, then one grouped NCCL send/recv per neighbour straight into the
+// ghost area.  With the P2P transport the producers already pushed the ghosts: nothing to do.
 void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
-    if (!A.halo) return;
+    if (!A.halo || D.p2p) return;
     if (A.nsend > 0) {
         dev::k_pack<<<grid_for(D, A.nsend), dev::kBlock, 0, st>>>(A.nsend, A.sidx, x, A.sbuf);
         D.launches_total++;
@@ -341,37 +355,55 @@ void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
     NCCL_OK(ncclGroupStart());
     for (int q = 0; q < D.nranks; q++) {
         if (A.hs_count[q]) NCCL_OK(ncclSend(A.sbuf + A.hs_off[q], (size_t)A.hs_count[q], ncclFloat64, q, D.comm, st));
-        if (A.hr_count[q]) NCCL_OK(ncclRecv(x + A.nown + A.hr_off[q], (size_t)A.hr_count[q], ncclFloat64, q, D.comm, st));
+        if (A.hr_count[q]) NCCL_OK(ncclRecv(x + A.gbase + A.hr_off[q], (size_t)A.hr_count[q], ncclFloat64, q, D.comm, st));
     }
     NCCL_OK(ncclGroupEnd());
 }
 
-// a12: sum a per-rank dot-product partial across ranks, in place in the device scalar block.
-void allreduce_slot(DevState &D, double *slot, cudaStream_t st) {
-    if (D.nranks > 1) NCCL_OK(ncclAllReduce(slot, slot, 1, ncclFloat64, ncclSum, D.comm, st));
+// a12: sum a per-rank dot product across ranks into the device scalar block: NCCL all-reduce, or (P2P)
+// a one-thread kernel adding the ranks' deposited sums in rank order.
+void allreduce_dot(DevState &D, int kind, cudaStream_t st) {
+    if (D.nranks == 1) return;
+    if (D.p2p) {
+        dev::k_dot_collect<<<1, 32, 0, st>>>(kind, D.S, D.pp);
+        D.launches_total++;
+        CUDA_OK(cudaGetLastError());
+        return;
+    }
+    double *slot = kind == dev::DOT_FF ? &D.S->ff : kind == dev::DOT_RR ? &D.S->rr : kind == dev::DOT_PQ ? &D.S->pq : &D.S->rz;
+    NCCL_OK(ncclAllReduce(slot, slot, 1, ncclFloat64, ncclSum, D.comm, st));
 }
 
 const double kC0 = 4.0 / 3.0;
 
 // c.16 pre-smoothing steps i = 1..m-1 and the residual (a4, a5), restriction (a6), recursion,
 // prolongation (a8), post-smoothing (a9, a10).  b, x: this level's right-hand side and output
-// (this rank's rows; ghost slots are filled by halo() before every gathering kernel).
+// (this rank's rows).  Ghost values reach the gathering kernels either by halo() (NCCL) right before
+// them, or (P2P) by the producing epilogues' pushes (push_of: d_new/d0 along K_l's plan, r along R_l's,
+// x after prolongation along K_l's, the final x of a coarse level along P̄_{l-1}'s).
 void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot) {
     DLevel &L = D.lev[l];
     const int m = D.m;
+    // the first replicated level waits (P2P) for every rank's share of its right-hand side
+    const bool first_rep = D.nranks > 1 && L.replicated && !D.lev[l - 1].replicated;
     if (l == D.nlevels - 1) {
         const int n = (int)L.N;
         const size_t smem = sizeof(double) * 2 * (size_t)n;
-        dev::k_coarse_solve<<<1, 1024, smem, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps);
+        dev::k_coarse_solve<<<1, 1024, smem, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps,
+                                                  p2p_of(D, first_rep));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
         return;
     }
     DLevel &C = D.lev[l + 1];
     const bool coarse_is_last = (l + 1 == D.nlevels - 1);
-    // --- pre-smoothing from x = 0: d0 = c0·b·invd (level 0 here; coarse levels: restrict epilogue)
-    if (l == 0) {
-        dev::k_cheb_first<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, b, L.invd, L.d[0], kC0);
+    const DCsr *Pabove = l > 0 ? &D.lev[l - 1].P : nullptr;  // gathers this level's final x
+    // --- pre-smoothing from x = 0: d0 = c0·b·invd (level 0 and the first replicated level; other
+    //     coarse levels: restriction epilogue)
+    if (l == 0 || first_rep) {
+        dev::k_cheb_first<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, b, L.invd, L.d[0], kC0,
+                                                                   push_of(D, L.K, L.d[0]),
+                                                                   p2p_of(D, l == 0 || first_rep));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
     }
@@ -389,6 +421,7 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         e.xout = x;
         e.a = (double)(2 * i - 1) / (double)(2 * i + 3);
         e.bc = (double)(8 * i + 4) / (double)(2 * i + 3);
+        e.pushD = push_of(D, L.K, L.d[cur ^ 1]);
         ProfScope ps(D, st, l == 0);
         launch_csr(D, L.K, L.d[cur], e, st);
         cur ^= 1;
@@ -401,12 +434,23 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         e.r = L.r;
         e.dpend = (m == 1) ? L.d[cur] : nullptr;
         e.x = x;
+        e.pushR = push_of(D, L.R, L.r);
         launch_csr(D, L.K, L.d[cur], e, st);
     }
     // restriction b_c = R r, fused with the coarse level's first smoothing step d0_c = c0·b_c·invd_c
     halo(D, L.R, L.r, st);
-    if (C.replicated && !L.replicated) {
-        // last distributed level: each rank restricts its share of the coarse rows, then an
+    if (C.replicated && !L.replicated && D.p2p) {
+        // last distributed level (P2P): each rank restricts its share of the coarse rows straight into
+        // every rank's whole coarse right-hand side (an all-gather by pushes)
+        dev::EpiRestrict e{};
+        e.bc = C.b + D.ag_row0;
+        e.invd = nullptr;
+        e.d0 = nullptr;
+        e.c0 = kC0;
+        e.pushB = dev::Push{D.ag_ptr, D.ag_dst, D.d_base, (long long)((const char *)C.b - D.slab)};
+        launch_csr(D, L.R, L.r, e, st);
+    } else if (C.replicated && !L.replicated) {
+        // last distributed level (NCCL): each rank restricts its share of the coarse rows, then an
         // all-gather assembles the whole coarse right-hand side on every rank
         dev::EpiRestrict e{};
         e.bc = D.ag_send;
@@ -419,7 +463,8 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
                                                                                 D.ag_bounds, D.ag_recv, C.b);
         D.launches_total++;
         if (!coarse_is_last) {
-            dev::k_cheb_first<<<grid_for(D, C.n), dev::kBlock, 0, st>>>(C.n, C.b, C.invd, C.d[0], kC0);
+            dev::k_cheb_first<<<grid_for(D, C.n), dev::kBlock, 0, st>>>(C.n, C.b, C.invd, C.d[0], kC0, dev::Push{},
+                                                                       dev::P2P{});
             D.launches_total++;
         }
         CUDA_OK(cudaGetLastError());
@@ -429,6 +474,7 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         e.invd = coarse_is_last ? nullptr : C.invd;
         e.d0 = C.d[0];
         e.c0 = kC0;
+        e.pushD = push_of(D, C.K, C.d[0]);
         launch_csr(D, L.R, L.r, e, st);
     }
     vcycle_level(D, l + 1, C.b, C.x, st, dev::DOT_NONE);
@@ -437,6 +483,7 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         halo(D, L.P, C.x, st);
         dev::EpiProlong e{};
         e.x = x;
+        e.pushX = push_of(D, L.K, x);
         launch_csr(D, L.P, C.x, e, st);
     }
     // post-smoothing: r = b − K x; d0 = c0·r·invd
@@ -448,24 +495,29 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         e.invd = L.invd;
         e.d0 = L.d[0];
         e.c0 = kC0;
+        e.pushD = push_of(D, L.K, L.d[0]);
         launch_csr(D, L.K, x, e, st);
     }
     cur = 0;
     for (int i = 1; i < m; i++) {
-        const bool last = (i == m - 1) && final_dot != dev::DOT_NONE;
+        const bool lastd = (i == m - 1) && final_dot != dev::DOT_NONE;
         const double a = (double)(2 * i - 1) / (double)(2 * i + 3);
         const double bcf = (double)(8 * i + 4) / (double)(2 * i + 3);
+        const dev::Push pd = (i < m - 1) ? push_of(D, L.K, L.d[cur ^ 1]) : dev::Push{};
+        const dev::Push px = (i == m - 1 && Pabove) ? push_of(D, *Pabove, x) : dev::Push{};
         halo(D, L.K, L.d[cur], st);
         ProfScope ps(D, st, l == 0);
-        if (last) {
+        if (lastd) {
             dev::EpiCheb<true> e{};
             e.rin = L.r; e.rout = L.r; e.dold = L.d[cur]; e.dnew = L.d[cur ^ 1]; e.invd = L.invd;
             e.xin = x; e.dpend = (i == 1) ? L.d[cur] : nullptr; e.xout = x; e.bdot = b; e.a = a; e.bc = bcf;
+            e.pushD = pd; e.pushX = px;
             launch_csr(D, L.K, L.d[cur], e, st, final_dot);
         } else {
             dev::EpiCheb<false> e{};
             e.rin = L.r; e.rout = L.r; e.dold = L.d[cur]; e.dnew = L.d[cur ^ 1]; e.invd = L.invd;
             e.xin = x; e.dpend = (i == 1) ? L.d[cur] : nullptr; e.xout = x; e.bdot = nullptr; e.a = a; e.bc = bcf;
+            e.pushD = pd; e.pushX = px;
             launch_csr(D, L.K, L.d[cur], e, st);
         }
         cur ^= 1;
@@ -489,16 +541,34 @@ static void vcycle(DevState &D, const double *b, double *x, cudaStream_t st, int
         dev::k_dot<<<grid_for(D, n0), dev::kBlock, 0, st>>>(n0, b, x, dotctx(D, dotkind));
         D.launches_total++;
     }
-    if (dotkind == dev::DOT_RZ) allreduce_slot(D, &D.S->rz, st);
+    if (dotkind != dev::DOT_NONE) allreduce_dot(D, dotkind, st);
 }
 
 namespace {
-// Upload one rank's share of a distributed operator (local columns + halo plan).
-void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format) {
-    upload_op(D, op.A, out, false, format, false);
+// Upload one rank's share of a distributed operator (local columns + halo plan).  gshift moves the
+// ghost columns (and the ghost area) up by gshift slots: P̄_l's ghosts follow K_{l+1}'s in the coarse
+// vector, so the two gatherers' ghost values never share slots.
+void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int64_t gshift = 0) {
+    const int64_t nown = op.col_end - op.col_begin;
+    if (gshift > 0 && !op.full_cols && !op.ghost.empty()) {
+        HCsr A;
+        A.nrows = op.A.nrows;
+        A.ncols = op.A.ncols + gshift;
+        A.rp.alloc(A.nrows + 1);
+        std::memcpy(A.rp.data(), op.A.rp.data(), sizeof(int64_t) * (A.nrows + 1));
+        const int64_t nnz = op.A.nnz();
+        A.ci.alloc(nnz);
+        A.v.alloc(nnz);
+        std::memcpy(A.v.data(), op.A.v.data(), sizeof(double) * nnz);
+        for (int64_t k = 0; k < nnz; k++) A.ci[k] = op.A.ci[k] >= nown ? (int32_t)(op.A.ci[k] + gshift) : op.A.ci[k];
+        upload_op(D, A, out, false, format, false);
+    } else {
+        upload_op(D, op.A, out, false, format, false);
+    }
     if (op.full_cols || D.nranks == 1) return;
     out.halo = true;
-    out.nown = op.col_end - op.col_begin;
+    out.nown = nown;
+    out.gbase = nown + (op.ghost.empty() ? 0 : gshift);
     out.nghost = (int64_t)op.ghost.size();
     out.hs_count.assign(op.send_count.begin(), op.send_count.end());
     out.hs_off.assign(op.send_off.begin(), op.send_off.end());
@@ -510,6 +580,135 @@ void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format) {
         out.sbuf = D.alloc_n<double>(out.nsend);
         CUDA_OK(cudaMemcpy(out.sidx, op.send_idx.data(), sizeof(int) * out.nsend, cudaMemcpyHostToDevice));
     }
+}
+
+// All-gather of int64 host arrays (one per rank, equal length) over the NCCL communicator.
+std::vector<int64_t> nccl_allgather_i64(DevState &D, const std::vector<int64_t> &mine) {
+    const size_t n = mine.size();
+    int64_t *dbuf = nullptr;
+    CUDA_OK(cudaMalloc(&dbuf, sizeof(int64_t) * n * (D.nranks + 1)));
+    std::vector<int64_t> all(n * D.nranks);
+    CUDA_OK(cudaMemcpy(dbuf, mine.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    NCCL_OK(ncclAllGather(dbuf, dbuf + n, n, ncclInt64, D.comm, nullptr));
+    CUDA_OK(cudaStreamSynchronize(nullptr));
+    CUDA_OK(cudaMemcpy(all.data(), dbuf + n, sizeof(int64_t) * n * D.nranks, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    return all;
+}
+
+// Slab layout (identical on every rank): flags, epoch, ticket, dot slots, then the vectors.
+constexpr size_t kFlagsOff = 0, kEpochOff = 512, kTicketOff = 576, kDslotOff = 1024, kVecOff = 4096;
+
+// Push plan of operator A's gathered vector: for each owned index j, the (rank, slot) pairs of the
+// other ranks' ghost copies.  meta_of(q) = {gbase, recv_off[0..nranks)} of rank q's copy of A.
+void build_push(DevState &D, const LocalOp &op, DCsr &A, const std::vector<int64_t> &meta, size_t meta_stride,
+                size_t meta_pos) {
+    const int nr = D.nranks, me = D.rank;
+    const int64_t nown = op.col_end - op.col_begin;
+    std::vector<int> cnt(nown + 1, 0);
+    for (int q = 0; q < nr; q++)
+        for (int t = 0; t < op.send_count[q]; t++) cnt[op.send_idx[op.send_off[q] + t] + 1]++;
+    for (int64_t j = 0; j < nown; j++) cnt[j + 1] += cnt[j];
+    if (cnt[nown] == 0) return;
+    std::vector<int2> dst(cnt[nown]);
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int q = 0; q < nr; q++) {
+        if (q == me || op.send_count[q] == 0) continue;
+        const int64_t *mq = meta.data() + (size_t)q * meta_stride + meta_pos;  // {gbase, recv_off[...]}
+        const int64_t first = mq[0] + mq[1 + me];
+        for (int t = 0; t < op.send_count[q]; t++) {
+            const int j = op.send_idx[op.send_off[q] + t];
+            dst[fill[j]++] = make_int2(q, (int)(first + t));
+        }
+    }
+    A.push_ptr = D.alloc_n<int>(nown + 1);
+    A.push_dst = D.alloc_n<int2>((int64_t)dst.size());
+    CUDA_OK(cudaMemcpy(A.push_ptr, cnt.data(), sizeof(int) * (nown + 1), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(A.push_dst, dst.data(), sizeof(int2) * dst.size(), cudaMemcpyHostToDevice));
+}
+
+// P2P transport setup: IPC-export the slab, map every other rank's, build the push plans of every
+// distributed operator and of the all-gather into the first replicated level, mark the participating
+// operators.  Runs after autotuning (autotuning launches are local).
+void p2p_setup(DevState &D, const DistPlan &plan) {
+    const int nr = D.nranks, me = D.rank, ld = D.last_dist;
+    // 1. slab handles
+    {
+        cudaIpcMemHandle_t h;
+        CUDA_OK(cudaIpcGetMemHandle(&h, D.slab));
+        std::vector<int64_t> mine((sizeof(h) + 7) / 8, 0);
+        std::memcpy(mine.data(), &h, sizeof(h));
+        const std::vector<int64_t> all = nccl_allgather_i64(D, mine);
+        std::vector<char *> bases(nr, nullptr);
+        for (int q = 0; q < nr; q++) {
+            if (q == me) {
+                bases[q] = D.slab;
+                continue;
+            }
+            cudaIpcMemHandle_t hq;
+            std::memcpy(&hq, all.data() + (size_t)q * mine.size(), sizeof(hq));
+            void *ptr = nullptr;
+            CUDA_OK(cudaIpcOpenMemHandle(&ptr, hq, cudaIpcMemLazyEnablePeerAccess));
+            bases[q] = static_cast<char *>(ptr);
+            D.peer_slabs.push_back(bases[q]);
+        }
+        D.d_base = D.alloc_n<char *>(nr);
+        CUDA_OK(cudaMemcpy(D.d_base, bases.data(), sizeof(char *) * nr, cudaMemcpyHostToDevice));
+    }
+    // 2. every rank's ghost layout of every distributed operator: {gbase, recv_off[0..nr)}
+    const size_t per = (size_t)nr + 1, stride = per * 3 * (size_t)(ld + 1);
+    std::vector<int64_t> mine(stride, 0);
+    for (int l = 0; l <= ld; l++) {
+        const DCsr *ops[3] = {&D.lev[l].K, &D.lev[l].R, &D.lev[l].P};
+        const LocalOp *lops[3] = {&plan.lev[l].K, &plan.lev[l].R, &plan.lev[l].P};
+        for (int k = 0; k < 3; k++) {
+            int64_t *m = mine.data() + ((size_t)l * 3 + k) * per;
+            if (!ops[k]->halo) continue;
+            m[0] = ops[k]->gbase;
+            for (int q = 0; q < nr; q++) m[1 + q] = lops[k]->recv_off[q];
+        }
+    }
+    const std::vector<int64_t> meta = nccl_allgather_i64(D, mine);
+    for (int l = 0; l <= ld; l++) {
+        DCsr *ops[3] = {&D.lev[l].K, &D.lev[l].R, &D.lev[l].P};
+        const LocalOp *lops[3] = {&plan.lev[l].K, &plan.lev[l].R, &plan.lev[l].P};
+        for (int k = 0; k < 3; k++) {
+            if (k > 0 && l + 1 >= D.nlevels) continue;
+            ops[k]->part = true;
+            if (ops[k]->halo) build_push(D, *lops[k], *ops[k], meta, stride, ((size_t)l * 3 + k) * per);
+        }
+    }
+    // 3. all-gather push of the first replicated level's right-hand side: my coarse rows to every rank
+    if (ld + 1 < D.nlevels) {
+        const std::vector<int64_t> &bd = plan.lev[ld + 1].bounds;
+        const int64_t n = bd[me + 1] - bd[me];
+        D.ag_row0 = bd[me];
+        std::vector<int> ptr(n + 1);
+        std::vector<int2> dst;
+        for (int64_t i = 0; i < n; i++) {
+            ptr[i] = (int)dst.size();
+            for (int q = 0; q < nr; q++)
+                if (q != me) dst.push_back(make_int2(q, (int)(bd[me] + i)));
+        }
+        ptr[n] = (int)dst.size();
+        D.ag_ptr = D.alloc_n<int>(n + 1);
+        D.ag_dst = D.alloc_n<int2>((int64_t)dst.size());
+        CUDA_OK(cudaMemcpy(D.ag_ptr, ptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+        if (!dst.empty()) CUDA_OK(cudaMemcpy(D.ag_dst, dst.data(), sizeof(int2) * dst.size(), cudaMemcpyHostToDevice));
+    }
+    // 4. the transport descriptor
+    D.pp.nranks = nr;
+    D.pp.rank = me;
+    D.pp.base = D.d_base;
+    D.pp.flags = reinterpret_cast<unsigned long long *>(D.slab + kFlagsOff);
+    D.pp.epoch = reinterpret_cast<unsigned long long *>(D.slab + kEpochOff);
+    D.pp.ticket = reinterpret_cast<unsigned *>(D.slab + kTicketOff);
+    D.pp.flags_off = (long long)kFlagsOff;
+    D.pp.dslot_off = (long long)kDslotOff;
+    // every rank has mapped every slab before any kernel may store into one
+    std::vector<int64_t> one(1, 1);
+    (void)nccl_allgather_i64(D, one);
+    D.p2p = true;
 }
 }  // namespace
 
@@ -552,6 +751,24 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             D->last_dist = H.nlevels - 1;
         }
         const int fmt = H.prm.format;
+        // transport: P2P peer memory (default) unless AMG_TRANSPORT=nccl, a degree-1 smoother, or a rank
+        // that cannot map its peers — decided collectively so every rank uses the same one
+        bool want_p2p = false;
+        if (nr > 1) {
+            int ok = 1;
+            if (const char *e = std::getenv("AMG_TRANSPORT")) ok = std::strcmp(e, "nccl") != 0;
+            if (H.prm.cheb_degree < 2) ok = 0;
+            for (int q = 0; q < ndev && ok; q++) {
+                if (q == dev_id) continue;
+                int can = 0;
+                if (cudaDeviceCanAccessPeer(&can, dev_id, q) != cudaSuccess || !can) ok = 0;
+            }
+            std::vector<int64_t> v(1, ok);
+            const std::vector<int64_t> all = nccl_allgather_i64(*D, v);
+            want_p2p = true;
+            for (int q = 0; q < nr; q++) want_p2p = want_p2p && all[q] != 0;
+        }
+        std::vector<int64_t> caps(H.nlevels, 0);
         for (int l = 0; l < H.nlevels; l++) {
             const HLevel &h = H.lev[l];
             DLevel &L = D->lev[l];
@@ -566,7 +783,8 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                 L.n = P.K.row_end - P.K.row_begin;
                 upload_local(*D, P.K, L.K, fmt);
                 if (!coarsest) {
-                    upload_local(*D, P.P, L.P, fmt);
+                    const bool next_dist = !plan.lev[l + 1].replicated;
+                    upload_local(*D, P.P, L.P, fmt, next_dist ? (int64_t)plan.lev[l + 1].K.ghost.size() : 0);
                     upload_local(*D, P.R, L.R, fmt);
                 }
             } else {
@@ -581,14 +799,52 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             for (int64_t i = 0; i < L.n; i++) invd[i] = 1.0 / h.dhat[r0 + i];
             L.invd = D->alloc_n<double>(L.n);
             CUDA_OK(cudaMemcpy(L.invd, invd.data(), sizeof(double) * L.n, cudaMemcpyHostToDevice));
-            // vectors gathered by K_l, R_l (fine side) or P̄_{l-1} (coarse side) need ghost capacity
-            int64_t cap = L.n + std::max(L.K.nghost, L.R.nghost);
-            if (l > 0) cap = std::max(cap, L.n + D->lev[l - 1].P.nghost);
-            L.b = D->alloc_n<double>(cap);
-            L.x = D->alloc_n<double>(cap);
-            L.r = D->alloc_n<double>(cap);
-            L.d[0] = D->alloc_n<double>(cap);
-            L.d[1] = D->alloc_n<double>(cap);
+            // vectors gathered by K_l (ghosts at n), P̄_{l-1} (coarse side: after K_l's) or R_l (at n)
+            const int64_t gP = l > 0 ? D->lev[l - 1].P.nghost : 0;
+            caps[l] = L.n + std::max(L.K.nghost + gP, L.R.nghost);
+        }
+        const int64_t n00 = D->lev[0].n, cap00 = n00 + D->lev[0].K.nghost;
+        // level vectors b, x, r, d0, d1 and the PCG r, z, p, q: in the P2P slab (same offsets on every
+        // rank: capacities are maxima over ranks) or from the allocator
+        {
+            std::vector<int64_t> want(caps);
+            want.push_back(n00);
+            want.push_back(cap00);
+            if (want_p2p) {
+                const std::vector<int64_t> all = nccl_allgather_i64(*D, want);
+                for (size_t k = 0; k < want.size(); k++)
+                    for (int q = 0; q < nr; q++) want[k] = std::max(want[k], all[(size_t)q * want.size() + k]);
+                size_t bytes = kVecOff;
+                auto add = [&](int64_t n) { bytes += ((size_t)std::max<int64_t>(n, 1) * 8 + 255) / 256 * 256; };
+                for (int l = 0; l < H.nlevels; l++)
+                    for (int k = 0; k < 5; k++) add(want[l]);
+                add(want[H.nlevels]);
+                add(want[H.nlevels + 1]);
+                add(want[H.nlevels + 1]);
+                add(want[H.nlevels]);
+                CUDA_OK(cudaMalloc(&D->slab, bytes));
+                CUDA_OK(cudaMemset(D->slab, 0, bytes));
+                D->slab_bytes = bytes;
+                D->slab_used = kVecOff;
+            }
+            auto vec = [&](int64_t n) -> double * {
+                if (!want_p2p) return D->alloc_n<double>(n);
+                double *p = reinterpret_cast<double *>(D->slab + D->slab_used);
+                D->slab_used += ((size_t)std::max<int64_t>(n, 1) * 8 + 255) / 256 * 256;
+                return p;
+            };
+            for (int l = 0; l < H.nlevels; l++) {
+                DLevel &L = D->lev[l];
+                L.b = vec(want[l]);
+                L.x = vec(want[l]);
+                L.r = vec(want[l]);
+                L.d[0] = vec(want[l]);
+                L.d[1] = vec(want[l]);
+            }
+            D->r = vec(want[H.nlevels]);
+            D->z = vec(want[H.nlevels + 1]);
+            D->p = vec(want[H.nlevels + 1]);
+            D->q = vec(want[H.nlevels]);
         }
         const HLevel &hl = H.lev[H.nlevels - 1];
         if (hl.N > 3072) throw Error{AMG_EINVAL, "coarsest level larger than 3072 rows (raise max_levels)"};
@@ -606,11 +862,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             D->row_begin0 = 0;
             D->row_end0 = H.lev[0].N;
         }
-        const int64_t n0 = D->lev[0].n, cap0 = n0 + D->lev[0].K.nghost;
-        D->r = D->alloc_n<double>(n0);
-        D->z = D->alloc_n<double>(cap0);
-        D->p = D->alloc_n<double>(cap0);
-        D->q = D->alloc_n<double>(n0);
+        const int64_t n0 = D->lev[0].n;
         D->partials = D->alloc_n<double>(D->nsm * 32 + 32);  // >= any resident grid (<= 32 CTAs per SM)
         D->counter = D->alloc_n<unsigned>(4);
         D->S = D->alloc_n<dev::Scalars>(1);
@@ -646,6 +898,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         // format + 56 B/row of vectors (d_old, r in/out, x in/out, invd, d_new)
         D->bytes_dominant = D->lev[0].K.alg_bytes() + 56.0 * (double)n0;
         CUDA_OK(cudaDeviceSynchronize());
+        if (want_p2p) p2p_setup(*D, plan);
     } catch (...) {
         delete D;
         throw;
@@ -674,18 +927,19 @@ static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
     DLevel &L0 = D.lev[0];
     const int64_t n = L0.n;
     vcycle(D, D.r, D.z, st, dev::DOT_RZ);  // ρ = rᵀz (all-reduced)
-    dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0);
+    dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0,
+                                                           push_of(D, L0.K, D.p), p2p_of(D, true));
     dev::k_roll_rho<<<1, 1, 0, st>>>(D.S);
     D.launches_total += 2;
     {
         halo(D, L0.K, D.p, st);
         dev::EpiSpmvDot e{D.p, D.q};
         launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ);
-        allreduce_slot(D, &D.S->pq, st);
+        allreduce_dot(D, dev::DOT_PQ, st);
     }
     dev::k_pcg_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR));
     D.launches_total++;
-    allreduce_slot(D, &D.S->rr, st);
+    allreduce_dot(D, dev::DOT_RR, st);
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
 }
@@ -750,17 +1004,22 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     // ‖F‖²
     dev::k_dot<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, F, F, dotctx(D, dev::DOT_FF));
     D.launches_total++;
-    allreduce_slot(D, &D.S->ff, st);
+    allreduce_dot(D, dev::DOT_FF, st);
     // r = F − K u ; ‖r‖²   (u is copied into z, which has the ghost slots K_0 gathers)
     {
-        CUDA_OK(cudaMemcpyAsync(D.z, u, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+        if (D.p2p) {
+            dev::k_copy_push<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, u, D.z, push_of(D, L0.K, D.z), D.pp);
+            D.launches_total++;
+        } else {
+            CUDA_OK(cudaMemcpyAsync(D.z, u, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+        }
         halo(D, L0.K, D.z, st);
         dev::EpiResidualFrom e{F, D.r, nullptr, nullptr};
         launch_csr(D, L0.K, D.z, e, st);
     }
     dev::k_dot<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.r, D.r, dotctx(D, dev::DOT_RR));
     D.launches_total++;
-    allreduce_slot(D, &D.S->rr, st);
+    allreduce_dot(D, dev::DOT_RR, st);
     CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
     const double nF = std::sqrt(D.hS->ff);
@@ -866,7 +1125,15 @@ extern "C" amg_status amg_vcycle(amg_hierarchy *H, const double *r, double *z, v
     API_BEGIN
     DevState *D = need_dev(H);
     if (!r || !z) throw Error{AMG_EINVAL, "bad argument"};
-    vcycle(*D, r, z, (cudaStream_t)stream, dev::DOT_NONE);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (D->p2p) {  // pushes address slab vectors: run on the PCG's r/z and copy in/out
+        const size_t bytes = sizeof(double) * (size_t)D->lev[0].n;
+        CUDA_OK(cudaMemcpyAsync(D->r, r, bytes, cudaMemcpyDeviceToDevice, st));
+        vcycle(*D, D->r, D->z, st, dev::DOT_NONE);
+        CUDA_OK(cudaMemcpyAsync(z, D->z, bytes, cudaMemcpyDeviceToDevice, st));
+    } else {
+        vcycle(*D, r, z, st, dev::DOT_NONE);
+    }
     CUDA_OK(cudaGetLastError());
     return AMG_OK;
     API_END

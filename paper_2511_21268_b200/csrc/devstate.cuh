@@ -52,9 +52,16 @@ struct DCsr {
         return 8.0 * (double)nnz + idx + 8.0 * (double)(nrows + 1);
     }
     float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
-    // halo plan (multi-GPU): ghost slots [nown, nown + nghost) of the gathered vector
+    // halo plan (multi-GPU): ghost slots [gbase, gbase + nghost) of the gathered vector (gbase = nown,
+    // except P̄_l whose ghosts follow K_{l+1}'s in the coarse vector)
     bool halo = false;
-    int64_t nown = 0, nghost = 0, nsend = 0;
+    int64_t nown = 0, nghost = 0, nsend = 0, gbase = 0;
+    // P2P transport: part = this operator's kernels take part in the cross-GPU lock-step; push_ptr /
+    // push_dst = where this rank's owned entries of the vector this operator GATHERS go on other ranks
+    // (rank, slot), CSR over the owned index
+    bool part = false;
+    int *push_ptr = nullptr;
+    int2 *push_dst = nullptr;
     int *sidx = nullptr;     // device: local owned indices to send, by destination rank
     double *sbuf = nullptr;  // device: packed send buffer
     std::vector<int> hs_count, hs_off, hr_count, hr_off;  // halo send/recv counts and offsets per rank
@@ -81,6 +88,17 @@ struct DevState {
     int rank = 0, nranks = 1, last_dist = 0;
     ncclComm_t comm = nullptr;
     int64_t row_begin0 = 0, row_end0 = 0;  // this rank's rows of level 0 (global ids)
+    // P2P transport (default when nranks > 1; AMG_TRANSPORT=nccl selects NCCL halos): own slab
+    // (cudaMalloc, IPC-exported: flags, dot slots, every vector), the other ranks' slabs mapped
+    bool p2p = false;
+    dev::P2P pp{};
+    char *slab = nullptr;
+    size_t slab_bytes = 0, slab_used = 0;
+    std::vector<char *> peer_slabs;  // opened IPC mappings (closed in the destructor)
+    char **d_base = nullptr;         // device array [nranks] of slab bases
+    int *ag_ptr = nullptr;           // all-gather push plan of the first replicated level's b
+    int64_t ag_row0 = 0;             // this rank's first row of that level
+    int2 *ag_dst = nullptr;
     double *ag_send = nullptr, *ag_recv = nullptr;  // all-gather into the first replicated level
     int64_t ag_stride = 0;
     int64_t *ag_bounds = nullptr;                   // device copy of that level's row partition
@@ -120,7 +138,17 @@ struct DevState {
 };
 
 
-inline dev::DotCtx dotctx(DevState &D, int kind) { return dev::DotCtx{D.partials, D.counter, D.S, kind}; }
+// P2P lock-step descriptor for a kernel: participating kernels get the transport, others none
+inline dev::P2P p2p_of(const DevState &D, bool part) { return (D.p2p && part) ? D.pp : dev::P2P{}; }
+// dot products of the PCG are global: with P2P every rank deposits into every rank's slots
+inline dev::DotCtx dotctx(DevState &D, int kind) {
+    return dev::DotCtx{D.partials, D.counter, D.S, kind, (kind != dev::DOT_NONE) ? p2p_of(D, true) : dev::P2P{}};
+}
+// push descriptor of `buf` (a vector in the own slab) along operator A's push plan
+inline dev::Push push_of(const DevState &D, const DCsr &A, const double *buf) {
+    if (!D.p2p || !A.push_ptr || !buf) return dev::Push{};
+    return dev::Push{A.push_ptr, A.push_dst, D.d_base, (long long)((const char *)buf - D.slab)};
+}
 
 // y-side epilogue applied to A·g for a CSR-layout (autotuned kernel / column source) or SELL2 operator.
 template <class Epi>

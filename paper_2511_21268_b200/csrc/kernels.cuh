@@ -34,11 +34,96 @@ struct Scalars {
 
 enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ };
 
+// ------------------------------------------------------------------------------------------------
+// P2P transport of the multi-GPU path (one process per GPU; every rank's "slab" of vectors, flags and
+// dot slots is mapped into every other rank's address space over NVLink/NVSwitch).  There is no
+// separate communication step: a kernel that produces values another rank gathers STORES them straight
+// into that rank's ghost slots from its epilogue (Push), and the kernels run in a cross-GPU lock-step:
+// every participating kernel waits at its start until every rank has completed the previous
+// participating kernel (flags[q] >= my completed count) and, when its last CTA finishes, publishes its
+// own completed count to every rank (release, system scope).  No kernel pushes into the buffer it
+// gathers, so this ordering makes every ghost read see the values of the previous kernel and no push
+// overwrite a value still being read.
+// ------------------------------------------------------------------------------------------------
+struct P2P {
+    int nranks;                  // 0: no cross-GPU traffic (1 GPU, NCCL transport, or a local-only kernel)
+    int rank;
+    char *const *base;           // [nranks] slab base of every rank, mapped (base[rank] = own slab)
+    unsigned long long *flags;   // own slab: flags[q] = participating kernels completed by rank q
+    unsigned long long *epoch;   // own slab: participating kernels completed by this rank
+    unsigned *ticket;            // own slab: CTA completion ticket (zero between launches)
+    long long flags_off;         // byte offset of flags[] in every slab
+    long long dslot_off;         // byte offset of the dot slots dslot[kind][rank] in every slab
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Kernel prologue: wait until every rank has completed as many participating kernels as this one.
+// Bounded: a peer that never arrives (a dead rank) traps after ~10 s instead of hanging the GPU.
+__device__ __forceinline__ void peer_wait(const P2P &pp) {
+    if (pp.nranks == 0) return;
+    if (threadIdx.x == 0) {
+        const unsigned long long e = *(volatile unsigned long long *)pp.epoch;
+        for (int q = 0; q < pp.nranks; q++) {
+            long long spins = 0;
+            while (ld_acquire_sys(pp.flags + q) < e) {
+                __nanosleep(100);
+                if (++spins > (1ll << 26)) __trap();
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Kernel epilogue (every CTA, after all its stores): the last CTA to finish publishes the new count.
+__device__ __forceinline__ void peer_signal(const P2P &pp) {
+    if (pp.nranks == 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned t = atomicAdd(pp.ticket, 1u);
+        if (t == gridDim.x - 1) {
+            __threadfence_system();
+            const unsigned long long e = *(volatile unsigned long long *)pp.epoch + 1ull;
+            *(volatile unsigned long long *)pp.epoch = e;
+            *(volatile unsigned *)pp.ticket = 0u;
+            for (int q = 0; q < pp.nranks; q++)
+                st_release_sys(reinterpret_cast<unsigned long long *>(pp.base[q] + pp.flags_off) + pp.rank, e);
+        }
+    }
+}
+
+// Ghost-value push list of one gathered vector: owned row i goes to (rank, slot) for
+// t in [ptr[i], ptr[i+1]); the destination is base[rank] + voff + 8·slot (the gathering rank's ghost
+// area of that vector).  ptr == nullptr: nothing to push.
+struct Push {
+    const int *ptr;
+    const int2 *dst;
+    char *const *base;
+    long long voff;
+    __device__ __forceinline__ void put(int64_t i, double v) const {
+        if (!ptr) return;
+        const int b = ptr[i], e = ptr[i + 1];
+        for (int t = b; t < e; t++) {
+            const int2 d = dst[t];
+            *reinterpret_cast<double *>(base[d.x] + voff + 8ll * d.y) = v;
+        }
+    }
+};
+
 struct DotCtx {
     double *partials;    // >= gridDim.x
     unsigned *counter;   // zero between launches
     Scalars *S;
     int kind;
+    P2P pp;              // nranks > 0: deposit the rank's sum in every rank's dslot[kind][rank] instead
 };
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -78,6 +163,13 @@ __device__ __forceinline__ void block_dot_finalize_n(double v, const DotCtx &dc)
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int w = 0; w < BS / 32; w++) s += red[w];
+        if (dc.pp.nranks > 0) {  // P2P: every rank sums the slots in rank order (k_dot_collect)
+            for (int q = 0; q < dc.pp.nranks; q++)
+                *reinterpret_cast<double *>(dc.pp.base[q] + dc.pp.dslot_off +
+                                            8ll * (dc.kind * dc.pp.nranks + dc.pp.rank)) = s;
+            *dc.counter = 0u;
+            return;
+        }
         Scalars *S = dc.S;
         switch (dc.kind) {
             case DOT_FF: S->ff = s; break;
@@ -127,10 +219,13 @@ struct EpiResidualFrom {  // r = b − K x  (also: r −= K d with b == r);  opt
     double *r;
     const double *dpend;  // nullable: x = dpend (degree-1 pre-smoothing)
     double *x;
+    Push pushR;           // r to the ranks whose restriction gathers it
     __device__ __forceinline__ Pre load(int64_t i) const { return {b[i], dpend ? dpend[i] : 0.0}; }
     __device__ __forceinline__ double operator()(int64_t i, double s, const Pre &pr) const {
-        r[i] = pr.b - s;
+        const double rr = pr.b - s;
+        r[i] = rr;
         if (dpend) x[i] = pr.dp;
+        pushR.put(i, rr);
         return 0.0;
     }
 };
@@ -151,6 +246,7 @@ struct EpiCheb {
     double *xout;
     const double *bdot;   // kDotRZ: returns bdot[i]·x_new[i]
     double a, bc;
+    Push pushD, pushX;    // d_new (gathered by the next step) / x (gathered by the coarse-to-fine P̄)
     __device__ __forceinline__ Pre load(int64_t i) const {
         Pre p;
         p.rin = rin[i];
@@ -170,6 +266,8 @@ struct EpiCheb {
         rout[i] = r;
         dnew[i] = dn;
         xout[i] = x;
+        pushD.put(i, dn);
+        pushX.put(i, x);
         return kDotRZ ? p.bd * x : 0.0;
     }
 };
@@ -182,11 +280,14 @@ struct EpiPostFirst {  // a9: r = b − K x;  d0 = c0·(r·invd)  (x += d0 is fo
     const double *invd;
     double *d0;
     double c0;
+    Push pushD;
     __device__ __forceinline__ Pre load(int64_t i) const { return {b[i], invd[i]}; }
     __device__ __forceinline__ double operator()(int64_t i, double s, const Pre &p) const {
         const double rr = p.b - s;
+        const double d = c0 * (rr * p.invd);
         r[i] = rr;
-        d0[i] = c0 * (rr * p.invd);
+        d0[i] = d;
+        pushD.put(i, d);
         return 0.0;
     }
 };
@@ -198,10 +299,16 @@ struct EpiRestrict {  // a6 (+a3 of the coarse level): b_c = R r;  d0_c = c0·(b
     const double *invd;  // nullable (coarsest level: no smoother)
     double *d0;
     double c0;
+    Push pushB, pushD;  // b_c to every rank (replicated coarse level) / d0_c to the coarse halo
     __device__ __forceinline__ Pre load(int64_t i) const { return {invd ? invd[i] : 0.0}; }
     __device__ __forceinline__ double operator()(int64_t i, double s, const Pre &p) const {
         bc[i] = s;
-        if (invd) d0[i] = c0 * (s * p.invd);
+        pushB.put(i, s);
+        if (invd) {
+            const double d = c0 * (s * p.invd);
+            d0[i] = d;
+            pushD.put(i, d);
+        }
         return 0.0;
     }
 };
@@ -210,9 +317,12 @@ struct EpiProlong {  // a8: x += P̄ e
     static constexpr bool kDot = false;
     struct Pre { double x; };
     double *x;
+    Push pushX;
     __device__ __forceinline__ Pre load(int64_t i) const { return {x[i]}; }
     __device__ __forceinline__ double operator()(int64_t i, double s, const Pre &p) const {
-        x[i] = p.x + s;
+        const double xn = p.x + s;
+        x[i] = xn;
+        pushX.put(i, xn);
         return 0.0;
     }
 };
@@ -306,7 +416,8 @@ struct ColsD16 {
 template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp, Cols cols,
                                                  const double *__restrict__ v, const double *__restrict__ g,
-                                                 int64_t nrows, Epi epi, DotCtx dc) {
+                                                 int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
+    peer_wait(pp);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -365,6 +476,7 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
         if (lane < nr) dacc += epi(r0 + lane, mine, pre);
     }
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+    peer_signal(pp);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -422,7 +534,8 @@ struct TmaCfg {
 template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ rp, Cols cols,
                                                    const double *__restrict__ v, const double *__restrict__ g,
-                                                   int64_t nrows, Epi epi, DotCtx dc) {
+                                                   int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
+    peer_wait(pp);
     using C = TmaCfg<U, Cols::kStaged>;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -547,6 +660,7 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         s ^= 1;
     }
     if constexpr (Epi::kDot) block_dot_finalize_n<kBlockT>(dacc, dc);
+    peer_signal(pp);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -558,7 +672,8 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
 template <class Epi>
 __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ soff, const int2 *__restrict__ ci2,
                                                   const double2 *__restrict__ v2, const double *__restrict__ g,
-                                                  int64_t nrows, Epi epi, DotCtx dc) {
+                                                  int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
+    peer_wait(pp);
     constexpr int U = 4;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -601,6 +716,7 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
         if (row < nrows) dacc += epi(row, (acc[0] + acc[1]) + (acc[2] + acc[3]), pre);
     }
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+    peer_signal(pp);
 }
 
 // Non-template kernels are defined in device.cu only (AMGB_PLAIN_KERNELS); the inst_*.cu units see
@@ -611,9 +727,45 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock) k_cheb_first(int64_t n, const double *__restrict__ b,
                                                         const double *__restrict__ invd, double *__restrict__ d0,
-                                                        double c0) {
-    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
-        d0[i] = c0 * (b[i] * invd[i]);
+                                                        double c0, Push push, P2P pp) {
+    peer_wait(pp);
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double d = c0 * (b[i] * invd[i]);
+        d0[i] = d;
+        push.put(i, d);
+    }
+    peer_signal(pp);
+}
+
+// y = x (owned rows) and the ghost push of y (P2P: the initial residual's copy of u)
+__global__ void __launch_bounds__(kBlock) k_copy_push(int64_t n, const double *__restrict__ x, double *__restrict__ y,
+                                                       Push push, P2P pp) {
+    peer_wait(pp);
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double v = x[i];
+        y[i] = v;
+        push.put(i, v);
+    }
+    peer_signal(pp);
+}
+
+// P2P all-reduce of one dot product: every rank deposited its sum in dslot[kind][q] of every rank
+// (block_dot_finalize); each rank adds them in rank order (identical on every rank).
+__global__ void k_dot_collect(int kind, Scalars *S, P2P pp) {
+    peer_wait(pp);
+    if (threadIdx.x == 0) {
+        const double *slot = reinterpret_cast<const double *>(pp.base[pp.rank] + pp.dslot_off) + kind * pp.nranks;
+        double s = 0.0;
+        for (int q = 0; q < pp.nranks; q++) s += *(volatile const double *)(slot + q);
+        switch (kind) {
+            case DOT_FF: S->ff = s; break;
+            case DOT_RR: S->rr = s; break;
+            case DOT_PQ: S->pq = s; break;
+            case DOT_RZ: S->rz = s; break;
+            default: break;
+        }
+    }
+    peer_signal(pp);
 }
 
 // autotuning scratch: a smooth positive pattern
@@ -630,16 +782,19 @@ __global__ void __launch_bounds__(kBlock) k_axpy1(int64_t n, const double *__res
 // dot(a, b) -> scalar of kind dc.kind
 __global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
                                                  DotCtx dc) {
+    peer_wait(dc.pp);
     double s = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
         s += a[i] * b[i];
     block_dot_finalize(s, dc);
+    peer_signal(dc.pp);
 }
 
 // a2: u += α p; r −= α q; ‖r‖² with α = ρ/pᵀq from the (all-reduced) device scalars
 __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *__restrict__ p,
                                                         const double *__restrict__ q, double *__restrict__ u,
                                                         double *__restrict__ r, DotCtx dc) {
+    peer_wait(dc.pp);
     const double alpha = dc.S->rz / dc.S->pq;
     double s = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
@@ -649,14 +804,20 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *
         s += ri * ri;
     }
     block_dot_finalize(s, dc);
+    peer_signal(dc.pp);
 }
 
 // a11: p = z + β p with β = ρ/ρ_prev  (first iteration: p = z)
 __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__restrict__ z, double *__restrict__ p,
-                                                      const Scalars *__restrict__ S, int first) {
+                                                      const Scalars *__restrict__ S, int first, Push push, P2P pp) {
+    peer_wait(pp);
     const double beta = first ? 0.0 : S->rz / S->rz_prev;
-    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
-        p[i] = first ? z[i] : z[i] + beta * p[i];
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double v = first ? z[i] : z[i] + beta * p[i];
+        p[i] = v;
+        push.put(i, v);
+    }
+    peer_signal(pp);
 }
 
 // end of a PCG iteration: ρ_prev <- ρ (one thread; after every consumer of ρ in this iteration)
@@ -684,7 +845,8 @@ __global__ void __launch_bounds__(kBlock) k_unpack_allgather(int nranks, int64_t
 __global__ void __launch_bounds__(1024) k_coarse_solve(int n, const int64_t *__restrict__ rp,
                                                         const int *__restrict__ ci, const double *__restrict__ v,
                                                         const double *__restrict__ invd, const double *__restrict__ b,
-                                                        double *__restrict__ x, int sweeps) {
+                                                        double *__restrict__ x, int sweeps, P2P pp) {
+    peer_wait(pp);
     extern __shared__ double sm[];
     double *xa = sm, *xb = sm + n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) xa[i] = 0.0;
@@ -699,6 +861,7 @@ __global__ void __launch_bounds__(1024) k_coarse_solve(int n, const int64_t *__r
         double *tmp = xa; xa = xb; xb = tmp;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xa[i];
+    peer_signal(pp);
 }
 
 #endif  // AMGB_PLAIN_KERNELS

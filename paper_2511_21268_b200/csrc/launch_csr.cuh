@@ -23,7 +23,8 @@ void launch_csr4t_gu(DevState &D, const DCsr &A, const Cols &cols, const double 
     }
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-    dev::k_csr4t<G, U, Epi, Cols><<<grid, dev::kBlockT, smem, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind));
+    dev::k_csr4t<G, U, Epi, Cols><<<grid, dev::kBlockT, smem, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
+                                                                      p2p_of(D, A.part));
 }
 
 template <int G, int U, class Epi, class Cols>
@@ -39,8 +40,8 @@ void launch_csr2_gu(DevState &D, const DCsr &A, const Cols &cols, const double *
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, (int64_t)per_sm * D.nsm));
-    dev::k_csr2<G, U, Epi, Cols><<<grid, dev::kBlock, 0, st>>>(A.rp, cols, A.v, g,
-                                                               A.nrows, epi, dotctx(D, dotkind));
+    dev::k_csr2<G, U, Epi, Cols><<<grid, dev::kBlock, 0, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
+                                                               p2p_of(D, A.part));
 }
 
 template <class Epi, class Cols>
@@ -74,7 +75,8 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
             per_sm = std::max(per_sm, 1);
         }
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-        dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind));
+        dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind),
+                                                         p2p_of(D, A.part));
     } else if (A.kern & 2) {
         launch_csr_cols(D, A, dev::ColsD16{reinterpret_cast<const unsigned short *>(A.off16), A.rbase}, g, epi, st, dotkind);
     } else {

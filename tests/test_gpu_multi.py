@@ -26,11 +26,12 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, case, rep_nnz, q):
+def _worker(rank, world, port, case, rep_nnz, transport, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         os.environ["AMG_REPLICATE_NNZ"] = str(rep_nnz)
+        os.environ["AMG_TRANSPORT"] = transport
         torch.cuda.set_device(rank)
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
         import paper_2511_21268_b200 as amg
@@ -65,18 +66,21 @@ def _worker(rank, world, port, case, rep_nnz, q):
             dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case,rep_nnz", [((3, 3, 12), 100000), ((3, 2, 32), 200000), ((3, 2, 20), 10 ** 12)])
-def test_distributed_solve_matches_single_gpu(world, case, rep_nnz):
+def test_distributed_solve_matches_single_gpu(world, case, rep_nnz, transport):
+    """transport p2p: ghost values pushed from the producing kernels' epilogues into peer memory and a
+    cross-GPU kernel lock-step (no NCCL in the solve); nccl: NCCL send/recv halos and all-reduces."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, rep_nnz, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, rep_nnz, transport, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    status, out, ref, N = q.get(timeout=600)
+    status, out, ref, N = q.get(timeout=300)
     for pr in procs:
         pr.join(timeout=120)
     assert status == "ok", out
