@@ -123,17 +123,45 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
 
 
-def ncu_traffic(cfg: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+def ncu_traffic(cfg: str, key: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/ncu_dominant.json, written by tools/ncu_dominant.py) if it profiled this kernel variant."""
     path = os.path.join(ROOT, "profiles", "ncu_dominant.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        if d.get("workload") == cfg:
+        if d.get("workload") == cfg and d.get("kernel_key") == key:
             return d.get("dram_bytes_per_launch")
     except Exception:  # noqa: BLE001
         pass
     return None
+
+
+def sustained_copy_gbps(torch, stream, seconds: float = 2.0):
+    """Device-to-device copy of 2 GiB back to back for ~`seconds` (read + write bytes / time), measured
+    with CUDA events on the bench stream: the copy rate the GPU sustains under its power cap."""
+    try:
+        n = 1 << 28  # 2 GiB of fp64
+        a = torch.empty(n, dtype=torch.float64, device="cuda").fill_(1.0)
+        b = torch.empty_like(a)
+        b.copy_(a)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        reps = 0
+        e0.record(stream)
+        while time.perf_counter() - t0 < seconds:
+            for _ in range(10):
+                b.copy_(a)
+            reps += 10
+            torch.cuda.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        del a, b
+        return round(2.0 * 8 * n * reps / (ms * 1e-3) / 1e9, 1)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 # ------------------------------------------------------------------------------------------------
@@ -153,6 +181,9 @@ def run_gpu(args) -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # kernel choices per operator: the committed tuning cache (same variants as the committed ncu
+    # capture); operators missing from it are autotuned at setup and appended
+    os.environ.setdefault("AMG_TUNE_CACHE", os.path.join(ROOT, "profiles", f"tune_{args.config}.txt"))
 
     wl = workload_desc(args.config)
     dim, p, n, m = wl["dim"], wl["p"], wl["n"], wl["m"]
@@ -177,8 +208,9 @@ def run_gpu(args) -> None:
     op_cfg = [ops[(l, 0)] for l in range(info["levels"])]
     k0 = op_cfg[0]
     cols = "ColsD16" if k0["kernel"].endswith("_d16") else "ColsI32"
-    kname = (f"{'k_csr4t' if k0['kernel'].startswith('csr_tma') else 'k_csr2'}<G={k0['G']},U={k0['U']},"
-             f"EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0)")
+    family = "k_csr4t" if k0["kernel"].startswith("csr_tma") else "k_csr2"
+    kname = f"{family}<G={k0['G']},U={k0['U']},EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0)"
+    kkey = f"{family}<{k0['G']},{k0['U']},{cols}>"
     stream = torch.cuda.current_stream()
     Fd = torch.from_numpy(F).cuda()
     u = torch.zeros_like(Fd)
@@ -245,12 +277,13 @@ def run_gpu(args) -> None:
         ms_e2e = t.item()
 
     peak, peak_src = load_peaks()
+    sustained = sustained_copy_gbps(torch, stream) if rank == 0 else None
     bm = byte_model(info, m, ops)
     iters = iters_seen[-1]
     solve_s = ms / 1e3
     per_launch_ms = ks["total_ms"] / max(ks["launches"], 1)
     achieved = ks["bytes_per_launch"] / (per_launch_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config, kkey)
     vcyc_gbs = bm["iter_bytes"] * iters / solve_s / 1e9
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -303,6 +336,10 @@ def run_gpu(args) -> None:
                 "algorithmic_bytes_per_launch": ks["bytes_per_launch"],
                 "launch_ms": round(per_launch_ms, 5),
                 "launches_timed": ks["launches"],
+                # context: a plain device copy run back to back for ~2 s right after the timed region
+                # (same power-capped, hot state as the solve), read + write bytes
+                "sustained_copy_GBps": sustained,
+                "frac_of_sustained_copy": round(achieved / sustained, 4) if sustained else None,
             },
             "e2e": {
                 "value": round(ms_e2e / 1e3, 6), "unit": "s",

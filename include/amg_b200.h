@@ -96,7 +96,7 @@ typedef struct {
     int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30)                */
     int64_t coarse_size;    /* coarsest when N_l <= coarse_size (50)                 */
     int max_levels;         /* 20                                                                 */
-    int format;             /* device matrix format: 0 auto (rows padded to 4; autotuned kernel and column
+    int format;             /* device matrix format: 0 auto (rows padded to 8; autotuned kernel and column
                                source per operator), 1 CSR warp-per-row, 2 SELL-32 (row per lane),
                                3 TMA-staged CSR, 4 CSR with 16-bit column offsets (register core),
                                5 CSR with 16-bit column offsets (TMA-staged values) */
@@ -201,7 +201,7 @@ amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_confi
 /* Force the kernel configuration of one CSR-layout operator (experiments and the kernel-equivalence
  * tests): kernel as in the amg_op_config struct: bit 1 needs the 16-bit encoding (formats 0, 3, 4, 5, and
  * only where every 64-entry chunk spans < 65536 columns);
- * bit 0 = TMA needs rows padded to 4 and U <= 4; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
+ * bit 0 = TMA needs rows padded to 8 and U <= 4; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
  * sums each row in the same order, so results are bitwise unchanged.  Drops captured PCG graphs.
  * AMG_EINVAL for a bad level/op or an unavailable configuration. */
 amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);

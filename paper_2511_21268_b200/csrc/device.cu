@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -97,7 +98,8 @@ inline int32_t pad_col(const HCsr &A, int64_t i, bool square) {
 bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out);
 
 // Upload a host CSR as CSR2 (rows padded to a multiple of `mult` entries with (pad column, 0.0);
-// mult = 2 for CSR2, 4 for the TMA-staged CSR4T whose bulk copies need 16-byte aligned ranges).
+// mult = 2 for format 1, 8 for the autotuned layouts: the TMA-staged core's bulk copies need 16-byte
+// aligned value, int32 and 16-bit column ranges).
 void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 2) {
     const int64_t n = A.nrows;
     Buf<int64_t> rp(n + 1);
@@ -126,6 +128,7 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
         }
     }
     out.fmt = 0;
+    out.mult = mult;
     out.stored = nnz2;
     out.rp = D.alloc_n<int64_t>(n + 1);
     out.ci = D.alloc_n<int32_t>(nnz2);
@@ -135,7 +138,7 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
     CUDA_OK(cudaMemcpy(out.rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.ci, ci.data(), sizeof(int32_t) * nnz2, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * nnz2, cudaMemcpyHostToDevice));
-    if (mult == 4) encode_d16(D, rp.data(), ci.data(), n, out);
+    if (mult >= 4) encode_d16(D, rp.data(), ci.data(), n, out);
 }
 
 // 16-bit column offsets (ColsD16, kernels.cuh): base = the row's smallest stored column, offsets
@@ -220,9 +223,9 @@ void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, b
     out.ncols = A.ncols;
     out.nnz = A.nnz();
     if (format == 0 || format >= 3) {
-        // rows padded to 4 entries: runnable by both the register-batched CSR2 core and the
-        // TMA-staged CSR4T core (format 0 autotunes between them after the upload)
-        upload_csr2(D, A, out, square, 4);
+        // rows padded to 8 entries (16-byte aligned value, int32 and 16-bit column ranges): runnable by
+        // both the register-batched CSR2 core and the TMA-staged CSR4T core (format 0 autotunes)
+        upload_csr2(D, A, out, square, 8);
         out.kern = (format == 3) ? 1 : (format == 4 && out.off16) ? 2 : (format == 5 && out.off16) ? 3 : 0;
         return;
     }
@@ -257,11 +260,53 @@ float time_op(DevState &D, DCsr &A, const double *x, const Epi &e, cudaEvent_t e
     return best;
 }
 
-void autotune_op(DevState &D, DCsr &A, int role, double *x, double *y1, double *y2, double *y3) {
+// Tuning cache (env AMG_TUNE_CACHE = path): one line per tuned operator,
+//   "<rank> <nranks> <level> <role> <nrows> <nnz> <kern> <G> <U> <us>".
+// A hit (same rank, ranks, level, role and operator shape) reuses the stored choice, so separate runs
+// (the bench, its ncu capture) execute the same kernel variants; misses are tuned and appended.
+struct TuneKey {
+    int rank, nranks, level, role;
+    int64_t nrows, nnz;
+};
+bool tune_lookup(const TuneKey &k, DCsr &A) {
+    const char *path = std::getenv("AMG_TUNE_CACHE");
+    if (!path) return false;
+    FILE *f = std::fopen(path, "r");
+    if (!f) return false;
+    int r, nr, l, ro, kern, G, U;
+    long long n, z;
+    float us;
+    bool hit = false;
+    while (std::fscanf(f, "%d %d %d %d %lld %lld %d %d %d %f", &r, &nr, &l, &ro, &n, &z, &kern, &G, &U, &us) == 10) {
+        if (r == k.rank && nr == k.nranks && l == k.level && ro == k.role && n == k.nrows && z == k.nnz) {
+            if ((kern & 2) && !A.off16) continue;  // stale entry for this operator's encodings
+            A.kern = kern;
+            A.G = G;
+            A.U = U;
+            A.tuned_us = us;
+            hit = true;
+        }
+    }
+    std::fclose(f);
+    return hit;
+}
+void tune_store(const TuneKey &k, const DCsr &A) {
+    const char *path = std::getenv("AMG_TUNE_CACHE");
+    if (!path) return;
+    if (FILE *f = std::fopen(path, "a")) {
+        std::fprintf(f, "%d %d %d %d %lld %lld %d %d %d %.2f\n", k.rank, k.nranks, k.level, k.role, (long long)k.nrows,
+                     (long long)k.nnz, A.kern, A.G, A.U, A.tuned_us);
+        std::fclose(f);
+    }
+}
+
+void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y1, double *y2, double *y3) {
     if (A.fmt != 0 || A.nnz < 2000000) return;
     if (std::getenv("AMG_CSR_G") || std::getenv("AMG_CSR_U")) return;
     if (const char *e = std::getenv("AMG_AUTOTUNE"))
         if (std::atoi(e) == 0) return;
+    const TuneKey key{D.rank, D.nranks, level, role, A.nrows, A.nnz};
+    if (tune_lookup(key, A)) return;
     cudaEvent_t e0, e1;
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
@@ -305,6 +350,7 @@ void autotune_op(DevState &D, DCsr &A, int role, double *x, double *y1, double *
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     D.launches_total = 0;
+    tune_store(key, A);
 }
 
 // Profiling: events around the dominant kernel (level-0 fused Chebyshev step).
@@ -365,7 +411,7 @@ void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
 void allreduce_dot(DevState &D, int kind, cudaStream_t st) {
     if (D.nranks == 1) return;
     if (D.p2p) {
-        dev::k_dot_collect<<<1, 32, 0, st>>>(kind, D.S, D.pp);
+        dev::k_dot_collect<<<1, 32, 0, st>>>(kind, D.S, p2p_of(D, true));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
         return;
@@ -388,8 +434,17 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
     const bool first_rep = D.nranks > 1 && L.replicated && !D.lev[l - 1].replicated;
     if (l == D.nlevels - 1) {
         const int n = (int)L.N;
-        const size_t smem = sizeof(double) * 2 * (size_t)n;
-        dev::k_coarse_solve<<<1, 1024, smem, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps,
+        // stage the operator in shared memory when it fits (the coarsest level is tiny by design)
+        const size_t base = sizeof(double) * 4 * (size_t)n;
+        const size_t full = base + (size_t)L.K.stored * 12 + sizeof(int) * (size_t)(n + 1);
+        const int staged = full <= 200 * 1024 ? 1 : 0;
+        const size_t smem = staged ? full : base;
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            CUDA_OK(cudaFuncSetAttribute(dev::k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = smem;
+        }
+        dev::k_coarse_solve<<<1, 1024, smem, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps, staged,
                                                   p2p_of(D, first_rep));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
@@ -403,7 +458,8 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
     if (l == 0 || first_rep) {
         dev::k_cheb_first<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, b, L.invd, L.d[0], kC0,
                                                                    push_of(D, L.K, L.d[0]),
-                                                                   p2p_of(D, l == 0 || first_rep));
+                                                                   p2p_of(D, l == 0 || first_rep,
+                                                                          first_rep ? ~0u : L.K.wmask));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
     }
@@ -620,6 +676,7 @@ void build_push(DevState &D, const LocalOp &op, DCsr &A, const std::vector<int64
             const int j = op.send_idx[op.send_off[q] + t];
             dst[fill[j]++] = make_int2(q, (int)(first + t));
         }
+        A.pmask |= 1u << q;
     }
     A.push_ptr = D.alloc_n<int>(nown + 1);
     A.push_dst = D.alloc_n<int2>((int64_t)dst.size());
@@ -678,7 +735,26 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
             if (ops[k]->halo) build_push(D, *lops[k], *ops[k], meta, stride, ((size_t)l * 3 + k) * per);
         }
     }
-    // 3. all-gather push of the first replicated level's right-hand side: my coarse rows to every rank
+    // 3. wait masks: the kernels of level l gather from / push to the ranks of K_l, R_l, P̄_l, P̄_{l−1}
+    //    and K_{l+1} (restriction pushes d0 of the coarse level); the last distributed level's
+    //    restriction pushes to everyone
+    auto recv_mask = [&](const DCsr &A) {
+        unsigned m = 0;
+        if (A.halo)
+            for (int q = 0; q < nr; q++)
+                if (A.hr_count[q] > 0) m |= 1u << q;
+        return m;
+    };
+    for (int l = 0; l <= ld; l++) {
+        unsigned m = 1u << me;
+        const DCsr *ops[5] = {&D.lev[l].K, &D.lev[l].R, &D.lev[l].P, l > 0 ? &D.lev[l - 1].P : nullptr,
+                              (l + 1 <= ld) ? &D.lev[l + 1].K : nullptr};
+        for (const DCsr *A : ops)
+            if (A) m |= recv_mask(*A) | A->pmask;
+        D.lev[l].K.wmask = D.lev[l].P.wmask = m;
+        D.lev[l].R.wmask = (l == ld) ? ~0u : m;
+    }
+    // 4. all-gather push of the first replicated level's right-hand side: my coarse rows to every rank
     if (ld + 1 < D.nlevels) {
         const std::vector<int64_t> &bd = plan.lev[ld + 1].bounds;
         const int64_t n = bd[me + 1] - bd[me];
@@ -696,7 +772,7 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
         CUDA_OK(cudaMemcpy(D.ag_ptr, ptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
         if (!dst.empty()) CUDA_OK(cudaMemcpy(D.ag_dst, dst.data(), sizeof(int2) * dst.size(), cudaMemcpyHostToDevice));
     }
-    // 4. the transport descriptor
+    // 5. the transport descriptor
     D.pp.nranks = nr;
     D.pp.rank = me;
     D.pp.base = D.d_base;
@@ -705,6 +781,7 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
     D.pp.ticket = reinterpret_cast<unsigned *>(D.slab + kTicketOff);
     D.pp.flags_off = (long long)kFlagsOff;
     D.pp.dslot_off = (long long)kDslotOff;
+    D.pp.wait_mask = ~0u;
     // every rank has mapped every slab before any kernel may store into one
     std::vector<int64_t> one(1, 1);
     (void)nccl_allgather_i64(D, one);
@@ -757,7 +834,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         if (nr > 1) {
             int ok = 1;
             if (const char *e = std::getenv("AMG_TRANSPORT")) ok = std::strcmp(e, "nccl") != 0;
-            if (H.prm.cheb_degree < 2) ok = 0;
+            if (H.prm.cheb_degree < 2 || nr > 32) ok = 0;  // wait masks are 32-bit
             for (int q = 0; q < ndev && ok; q++) {
                 if (q == dev_id) continue;
                 int can = 0;
@@ -847,7 +924,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             D->q = vec(want[H.nlevels]);
         }
         const HLevel &hl = H.lev[H.nlevels - 1];
-        if (hl.N > 3072) throw Error{AMG_EINVAL, "coarsest level larger than 3072 rows (raise max_levels)"};
+        if (hl.N > 6144) throw Error{AMG_EINVAL, "coarsest level larger than 6144 rows (raise max_levels)"};
         if (nr > 1) {
             const int lr = D->last_dist + 1;  // first replicated level
             const std::vector<int64_t> &bd = plan.lev[lr].bounds;
@@ -882,10 +959,10 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             double *sx = scr, *y1 = scr + big, *y2 = scr + 2 * big, *y3 = scr + 3 * big;
             try {
                 for (int l = 0; l < D->nlevels; l++) {
-                    autotune_op(*D, D->lev[l].K, 0, sx, y1, y2, y3);
+                    autotune_op(*D, D->lev[l].K, l, 0, sx, y1, y2, y3);
                     if (l + 1 < D->nlevels) {
-                        autotune_op(*D, D->lev[l].P, 1, sx, y1, y2, y3);
-                        autotune_op(*D, D->lev[l].R, 2, sx, y1, y2, y3);
+                        autotune_op(*D, D->lev[l].P, l, 1, sx, y1, y2, y3);
+                        autotune_op(*D, D->lev[l].R, l, 2, sx, y1, y2, y3);
                     }
                 }
             } catch (...) {
@@ -928,7 +1005,7 @@ static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
     const int64_t n = L0.n;
     vcycle(D, D.r, D.z, st, dev::DOT_RZ);  // ρ = rᵀz (all-reduced)
     dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0,
-                                                           push_of(D, L0.K, D.p), p2p_of(D, true));
+                                                           push_of(D, L0.K, D.p), p2p_of(D, L0.K));
     dev::k_roll_rho<<<1, 1, 0, st>>>(D.S);
     D.launches_total += 2;
     {
@@ -1008,7 +1085,7 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     // r = F − K u ; ‖r‖²   (u is copied into z, which has the ghost slots K_0 gathers)
     {
         if (D.p2p) {
-            dev::k_copy_push<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, u, D.z, push_of(D, L0.K, D.z), D.pp);
+            dev::k_copy_push<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, u, D.z, push_of(D, L0.K, D.z), p2p_of(D, L0.K));
             D.launches_total++;
         } else {
             CUDA_OK(cudaMemcpyAsync(D.z, u, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
@@ -1209,7 +1286,7 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
     DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
     if (A.fmt != 0) throw Error{AMG_EINVAL, "operator is not in a CSR layout"};
     if (kernel < 0 || kernel > 3 || ((kernel & 2) && !A.off16)) throw Error{AMG_EINVAL, "kernel not available for this operator"};
-    if ((kernel & 1) && (A.stored % 4 != 0 || U > 4)) throw Error{AMG_EINVAL, "TMA core needs rows padded to 4 and U <= 4"};
+    if ((kernel & 1) && (A.mult < 8 || U > 4)) throw Error{AMG_EINVAL, "TMA core needs rows padded to 8 and U <= 4"};
     if (!(G == 1 || G == 4 || G == 8 || G == 32) || !(U == 2 || U == 4 || U == 6 || U == 8))
         throw Error{AMG_EINVAL, "G must be 1, 4, 8 or 32 and U 2, 4, 6 or 8"};
     CUDA_OK(cudaDeviceSynchronize());

@@ -33,6 +33,7 @@ struct DevBuf {
 struct DCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
     int fmt = 0;
+    int mult = 2;  // CSR layouts: every row padded to a multiple of `mult` entries
     int64_t *rp = nullptr;    // CSR2 row pointers (entries)
     int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
     int32_t *ci = nullptr;
@@ -60,6 +61,8 @@ struct DCsr {
     // push_dst = where this rank's owned entries of the vector this operator GATHERS go on other ranks
     // (rank, slot), CSR over the owned index
     bool part = false;
+    unsigned wmask = 0;  // ranks the kernels of this operator wait for (its level's neighbourhood)
+    unsigned pmask = 0;  // ranks this operator's push plan sends to
     int *push_ptr = nullptr;
     int2 *push_dst = nullptr;
     int *sidx = nullptr;     // device: local owned indices to send, by destination rank
@@ -139,7 +142,13 @@ struct DevState {
 
 
 // P2P lock-step descriptor for a kernel: participating kernels get the transport, others none
-inline dev::P2P p2p_of(const DevState &D, bool part) { return (D.p2p && part) ? D.pp : dev::P2P{}; }
+inline dev::P2P p2p_of(const DevState &D, bool part, unsigned mask = ~0u) {
+    if (!(D.p2p && part)) return dev::P2P{};
+    dev::P2P p = D.pp;
+    p.wait_mask = mask;
+    return p;
+}
+inline dev::P2P p2p_of(const DevState &D, const DCsr &A) { return p2p_of(D, A.part, A.wmask); }
 // dot products of the PCG are global: with P2P every rank deposits into every rank's slots
 inline dev::DotCtx dotctx(DevState &D, int kind) {
     return dev::DotCtx{D.partials, D.counter, D.S, kind, (kind != dev::DOT_NONE) ? p2p_of(D, true) : dev::P2P{}};

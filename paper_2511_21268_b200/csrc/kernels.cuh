@@ -54,6 +54,7 @@ struct P2P {
     unsigned *ticket;            // own slab: CTA completion ticket (zero between launches)
     long long flags_off;         // byte offset of flags[] in every slab
     long long dslot_off;         // byte offset of the dot slots dslot[kind][rank] in every slab
+    unsigned wait_mask;          // ranks this kernel reads from or writes to (bit q): the ones it waits for
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -65,13 +66,16 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Kernel prologue: wait until every rank has completed as many participating kernels as this one.
+// Kernel prologue: wait until every rank in wait_mask has completed as many participating kernels as
+// this one.  A kernel that gathers ghosts pushed by rank q, or pushes into rank q's ghost slots, has q in
+// its mask (RAW and WAR across ranks); dot products and the all-gather wait for every rank.
 // Bounded: a peer that never arrives (a dead rank) traps after ~10 s instead of hanging the GPU.
 __device__ __forceinline__ void peer_wait(const P2P &pp) {
     if (pp.nranks == 0) return;
     if (threadIdx.x == 0) {
         const unsigned long long e = *(volatile unsigned long long *)pp.epoch;
         for (int q = 0; q < pp.nranks; q++) {
+            if (!((pp.wait_mask >> q) & 1u)) continue;
             long long spins = 0;
             while (ld_acquire_sys(pp.flags + q) < e) {
                 __nanosleep(100);
@@ -388,10 +392,14 @@ __device__ __forceinline__ double ld_gather(const double *p) {
 //
 // ColsI32: plain int32 columns (4 B per entry), streamed like the values.
 struct ColsI32 {
-    static constexpr bool kStaged = true;
+    static constexpr int kIdxBytes = 4;  // bytes per entry of the staged column stream
     const int *ci;
     __device__ __forceinline__ int row(int64_t) const { return 0; }
     __device__ __forceinline__ int col(int64_t k, int, uint64_t pol) const { return ld_stream(ci + k, pol); }
+    __device__ __forceinline__ const void *stream(int64_t k) const { return ci + k; }
+    __device__ __forceinline__ int staged(const unsigned char *sidx, int j, int) const {
+        return reinterpret_cast<const int *>(sidx)[j];
+    }
 };
 
 // ColsD16: 16-bit column offsets ("CSR-D16").  base[i] = the first (smallest) column of row i and every
@@ -399,15 +407,19 @@ struct ColsI32 {
 // qualifies — the C3 levels span ≤ 57,624 (fine) and ≤ 33,325 (coarse) columns per row — and its column
 // stream shrinks from 4 to 2 B per entry (12 → 10 B per non-zero with the value).
 struct ColsD16 {
-    static constexpr bool kStaged = false;
+    static constexpr int kIdxBytes = 2;
     const unsigned short *off;
     const int *base;  // per row
     __device__ __forceinline__ int row(int64_t i) const { return __ldg(base + i); }
     __device__ __forceinline__ int col(int64_t k, int b, uint64_t pol) const { return b + (int)ld_stream(off + k, pol); }
+    __device__ __forceinline__ const void *stream(int64_t k) const { return off + k; }
+    __device__ __forceinline__ int staged(const unsigned char *sidx, int j, int b) const {
+        return b + (int)reinterpret_cast<const unsigned short *>(sidx)[j];
+    }
 };
 
 // The streaming CSR core: one warp owns a group of G consecutive rows and reduces one row at a time.
-// Rows are padded to a multiple of 4 entries (32-byte aligned).  A row is walked in windows of 64
+// Rows are padded to a multiple of 8 entries (64-byte aligned).  A row is walked in windows of 64
 // entries; lane l multiplies entries l and l+32 of each window (two 256-byte value loads per warp
 // instruction, and the x-gathers of one instruction hit ≈ 6 cache lines instead of ≈ 11 for an
 // (2l, 2l+1) pairing, measured on the C3 levels), accumulating them in two separate chains.  U windows
@@ -480,12 +492,13 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
 }
 
 // ------------------------------------------------------------------------------------------------
-// TMA-staged CSR core ("CSR4T"): rows padded to a multiple of 4 entries, so every row's value and
-// column ranges are 16-byte aligned multiples of 16 bytes.  Each warp walks its rows in chunks of
-// 64·U entries; one elected lane streams the NEXT chunk's values (and int32 columns) into a 2-stage
-// shared-memory ring with cp.async.bulk (TMA, completion on an mbarrier) while the warp reduces the
-// current chunk from shared memory and gathers x through L1/L2.  Lane l takes entries l and l+32 of
-// every 64-entry window, in the same two chains as k_csr2 (bitwise-equal row sums).
+// TMA-staged CSR core ("CSR4T"): rows padded to a multiple of 8 entries, so every row's value and
+// column-stream ranges are 16-byte aligned multiples of 16 bytes.  Each warp walks its rows in chunks of
+// 64·U entries; one elected lane keeps the next NS−1 chunks' values and column data (int32 or 16-bit
+// offsets) in flight into an NS-stage shared-memory ring with cp.async.bulk (TMA, completion on an
+// mbarrier per stage) while the warp reduces the current chunk from shared memory and gathers x through
+// L1/L2: the HBM stream never waits for the gathers or for registers.  Lane l takes entries l and l+32
+// of every 64-entry window, in the same two chains as k_csr2 (bitwise-equal row sums).
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -523,11 +536,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 
 constexpr int kBlockT = 128;  // 4 warps per CTA for the TMA-staged core
 
-template <int U, bool kStaged = true>
+constexpr int kTmaStages = 3;
+
+template <int U, int kIdxBytes>
 struct TmaCfg {
-    static constexpr int CH = 64 * U;                        // entries per chunk
-    static constexpr int STAGE = CH * (kStaged ? 12 : 8);     // bytes per stage (8 B value [+ 4 B column] per entry)
-    static constexpr int WARP = 2 * STAGE + 16;               // 2 stages + 2 mbarriers
+    static constexpr int NS = kTmaStages;
+    static constexpr int CH = 64 * U;                         // entries per chunk
+    static constexpr int IDX = CH * 8;                        // offset of the column data in a stage
+    static constexpr int STAGE = CH * (8 + kIdxBytes);        // bytes per stage
+    static constexpr int WARP = (NS * STAGE + 8 * NS + 127) / 128 * 128;  // NS stages + NS mbarriers, 128-B aligned
     static constexpr int SMEM = (kBlockT / 32) * WARP;        // dynamic shared memory per CTA
 };
 
@@ -536,14 +553,14 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
                                                    const double *__restrict__ v, const double *__restrict__ g,
                                                    int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
     peer_wait(pp);
-    using C = TmaCfg<U, Cols::kStaged>;
+    using C = TmaCfg<U, Cols::kIdxBytes>;
+    constexpr int NS = C::NS;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned char *wb = smem + wib * C::WARP;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + 2 * C::STAGE);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + NS * C::STAGE);
     if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int k = 0; k < NS; k++) mbar_init(&bar[k], 1);
         fence_mbar_init();
     }
     __syncwarp();
@@ -564,16 +581,8 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         c.e = __ldg(rp + row + 1);
         c.gfirst = (c.t == 0);
     };
-    auto first = [&](Cur &c) {
-        c.grp = warp;
-        c.t = 0;
-        c.valid = c.grp < ngroups;
-        if (c.valid) {
-            c.nr = (int)(nrows - c.grp * G < (int64_t)G ? nrows - c.grp * G : (int64_t)G);
-            row_start(c);
-        }
-    };
     auto advance = [&](Cur &c) {
+        if (!c.valid) return;
         if (c.k0 + C::CH < c.e) {
             c.k0 += C::CH;
             c.gfirst = false;
@@ -591,52 +600,59 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         row_start(c);
     };
     auto issue = [&](const Cur &c, int s) {
-        if (lane == 0) {
+        if (lane == 0 && c.valid) {
             const int64_t ne = (c.e - c.k0 < (int64_t)C::CH ? c.e - c.k0 : (int64_t)C::CH);
             unsigned char *st = wb + s * C::STAGE;
             fence_proxy_async();
-            mbar_arrive_expect_tx(&bar[s], (uint32_t)(ne * (Cols::kStaged ? 12 : 8)));
+            mbar_arrive_expect_tx(&bar[s], (uint32_t)(ne * (8 + Cols::kIdxBytes)));
             if (ne > 0) {
                 bulk_g2s(st, v + c.k0, (uint32_t)(ne * 8), &bar[s], pol);
-                if constexpr (Cols::kStaged)
-                    bulk_g2s(st + C::CH * 8, cols.ci + c.k0, (uint32_t)(ne * 4), &bar[s], pol);
+                bulk_g2s(st + C::IDX, cols.stream(c.k0), (uint32_t)(ne * Cols::kIdxBytes), &bar[s], pol);
             }
         }
     };
 
     double dacc = 0.0, acc = 0.0, acc1 = 0.0, mine = 0.0;
     typename Epi::Pre pre{};
-    int rs = 0;  // column-source row state of the current row
     uint32_t phase = 0;  // bit s = parity of stage s
-    Cur cur, nxt;
-    first(cur);
-    if (cur.valid) issue(cur, 0);
-    nxt = cur;
-    if (nxt.valid) advance(nxt);
+    // cur = chunk being reduced; ahead = the last chunk issued (NS−1 chunks in flight ahead of cur)
+    Cur cur;
+    cur.grp = warp;
+    cur.t = 0;
+    cur.valid = cur.grp < ngroups;
+    if (cur.valid) {
+        cur.nr = (int)(nrows - cur.grp * G < (int64_t)G ? nrows - cur.grp * G : (int64_t)G);
+        row_start(cur);
+    }
+    Cur ahead = cur;
+    issue(ahead, 0);
+    for (int k = 1; k < NS - 1; k++) {
+        advance(ahead);
+        issue(ahead, k);
+    }
     int s = 0;
     while (cur.valid) {
-        if (nxt.valid) issue(nxt, s ^ 1);
+        advance(ahead);
+        issue(ahead, (s + NS - 1) % NS);
         if (cur.gfirst && lane < cur.nr) pre = epi.load(cur.grp * G + lane);
-        if constexpr (!Cols::kStaged) rs = cols.row(cur.grp * G + cur.t);
+        const int rs = cols.row(cur.grp * G + cur.t);
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
         const int ne = (int)(cur.e - cur.k0 < (int64_t)C::CH ? cur.e - cur.k0 : (int64_t)C::CH);
         const double *sv = reinterpret_cast<const double *>(wb + s * C::STAGE);
-        const int *sc = reinterpret_cast<const int *>(wb + s * C::STAGE + C::CH * 8);
+        const unsigned char *sidx = wb + s * C::STAGE + C::IDX;
         double xa[U], xb[U], va[U], vb[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int ja = lane + 64 * u, jb = ja + 32;
             va[u] = vb[u] = xa[u] = xb[u] = 0.0;
             if (ja < ne) {
-                const int c = Cols::kStaged ? sc[ja] : cols.col(cur.k0 + ja, rs, pol);
                 va[u] = sv[ja];
-                xa[u] = __ldg(g + c);
+                xa[u] = __ldg(g + cols.staged(sidx, ja, rs));
             }
             if (jb < ne) {
-                const int c = Cols::kStaged ? sc[jb] : cols.col(cur.k0 + jb, rs, pol);
                 vb[u] = sv[jb];
-                xb[u] = __ldg(g + c);
+                xb[u] = __ldg(g + cols.staged(sidx, jb, rs));
             }
         }
 #pragma unroll
@@ -655,9 +671,8 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
             }
         }
         __syncwarp();
-        cur = nxt;
-        if (nxt.valid) advance(nxt);
-        s ^= 1;
+        advance(cur);
+        s = (s + 1) % NS;
     }
     if constexpr (Epi::kDot) block_dot_finalize_n<kBlockT>(dacc, dc);
     peer_signal(pp);
@@ -841,24 +856,50 @@ __global__ void __launch_bounds__(kBlock) k_unpack_allgather(int nranks, int64_t
     }
 }
 
-// a7: coarsest level, `sweeps` ℓ1-Jacobi sweeps from x = 0, one CTA, x double-buffered in shared memory.
+// a7: coarsest level, `sweeps` ℓ1-Jacobi sweeps from x = 0 in ONE CTA (the coarsest level has ≤ 50
+// rows at the default coarse size): the operator (when it fits), b, invd and the double-buffered x live
+// in shared memory; warp w reduces rows w, w+32, … with its lanes striding over the row (shuffle tree),
+// and a __syncthreads separates the sweeps.
 __global__ void __launch_bounds__(1024) k_coarse_solve(int n, const int64_t *__restrict__ rp,
                                                         const int *__restrict__ ci, const double *__restrict__ v,
                                                         const double *__restrict__ invd, const double *__restrict__ b,
-                                                        double *__restrict__ x, int sweeps, P2P pp) {
+                                                        double *__restrict__ x, int sweeps, int staged, P2P pp) {
     peer_wait(pp);
     extern __shared__ double sm[];
-    double *xa = sm, *xb = sm + n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) xa[i] = 0.0;
+    double *xa = sm, *xb = sm + n, *sb = sm + 2 * n, *sd = sm + 3 * n;
+    const int nnz = (int)rp[n];
+    double *sv = sm + 4 * n;
+    int *sc = reinterpret_cast<int *>(sv + (staged ? nnz : 0));
+    int *srp = sc + (staged ? nnz : 0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        xa[i] = 0.0;
+        sb[i] = b[i];
+        sd[i] = invd[i];
+    }
+    if (staged) {
+        for (int k = threadIdx.x; k < nnz; k += blockDim.x) {
+            sv[k] = v[k];
+            sc[k] = ci[k];
+        }
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) srp[i] = (int)rp[i];
+    }
     __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int s = 0; s < sweeps; s++) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i = wid; i < n; i += nw) {
             double t = 0.0;
-            for (int64_t k = rp[i]; k < rp[i + 1]; k++) t = fma(v[k], xa[ci[k]], t);
-            xb[i] = xa[i] + (b[i] - t) * invd[i];
+            if (staged) {
+                for (int k = srp[i] + lane; k < srp[i + 1]; k += 32) t = fma(sv[k], xa[sc[k]], t);
+            } else {
+                for (int64_t k = rp[i] + lane; k < rp[i + 1]; k += 32) t = fma(v[k], xa[ci[k]], t);
+            }
+            t = warp_sum(t);
+            if (lane == 0) xb[i] = xa[i] + (sb[i] - t) * sd[i];
         }
         __syncthreads();
-        double *tmp = xa; xa = xb; xb = tmp;
+        double *tmp = xa;
+        xa = xb;
+        xb = tmp;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xa[i];
     peer_signal(pp);

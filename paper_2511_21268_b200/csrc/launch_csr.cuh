@@ -8,7 +8,7 @@ namespace amgb {
 template <int G, int U, class Epi, class Cols>
 void launch_csr4t_gu(DevState &D, const DCsr &A, const Cols &cols, const double *g, Epi epi, cudaStream_t st,
                      int dotkind) {
-    constexpr int smem = dev::TmaCfg<U, Cols::kStaged>::SMEM;
+    constexpr int smem = dev::TmaCfg<U, Cols::kIdxBytes>::SMEM;
     static bool attr_set = false;  // per instantiation; device-independent attribute
     if (!attr_set) {
         CUDA_OK(cudaFuncSetAttribute(dev::k_csr4t<G, U, Epi, Cols>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -24,7 +24,7 @@ void launch_csr4t_gu(DevState &D, const DCsr &A, const Cols &cols, const double 
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
     dev::k_csr4t<G, U, Epi, Cols><<<grid, dev::kBlockT, smem, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
-                                                                      p2p_of(D, A.part));
+                                                                      (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));
 }
 
 template <int G, int U, class Epi, class Cols>
@@ -41,7 +41,7 @@ void launch_csr2_gu(DevState &D, const DCsr &A, const Cols &cols, const double *
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, (int64_t)per_sm * D.nsm));
     dev::k_csr2<G, U, Epi, Cols><<<grid, dev::kBlock, 0, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
-                                                               p2p_of(D, A.part));
+                                                               (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));
 }
 
 template <class Epi, class Cols>
@@ -76,7 +76,7 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
         }
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
         dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind),
-                                                         p2p_of(D, A.part));
+                                                         (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));
     } else if (A.kern & 2) {
         launch_csr_cols(D, A, dev::ColsD16{reinterpret_cast<const unsigned short *>(A.off16), A.rbase}, g, epi, st, dotkind);
     } else {

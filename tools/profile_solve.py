@@ -24,6 +24,7 @@ def main():
     args = ap.parse_args()
     import torch
     import paper_2511_21268_b200 as amg
+    os.environ.setdefault("AMG_TUNE_CACHE", os.path.join(ROOT, "profiles", f"tune_{args.config}.txt"))
     c = amg_inputs.CONFIGS[args.config]
     K, F = amg.iga_poisson(c["dim"], c["p"], c["n"])
     H = amg.Hierarchy(K, amg.params(c["p"], format=args.format))
