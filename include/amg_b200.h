@@ -185,7 +185,8 @@ amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
 
 /* Device kernel chosen for operator op (0 K_l, 1 P̄_l, 2 R_l) of level l: layout (0 padded CSR,
  * 1 SELL-32), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
- * source, 0 int32 columns, 1 16-bit column offsets per 64-entry chunk), rows per warp group G, pairs per lane per round trip
+ * source, 0 int32 columns, 1 16-bit column offsets from a per-row base; bit 2: register core with an L2
+ * bulk prefetch of the next row), rows per warp group G, pairs per lane per round trip
  * U, stored entries (with padding), the autotuned y = A·x time in microseconds (0 if the heuristic
  * choice was kept), the bytes one application streams for the operator in that format (8 B per value
  * of the nnz entries + the column data actually stored + 8 B row pointers; vectors excluded) and nnz.
@@ -200,22 +201,25 @@ typedef struct {
 amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
 /* Force the kernel configuration of one CSR-layout operator (experiments and the kernel-equivalence
  * tests): kernel as in the amg_op_config struct: bit 1 needs the 16-bit encoding (formats 0, 3, 4, 5, and
- * only where every 64-entry chunk spans < 65536 columns);
- * bit 0 = TMA needs rows padded to 8 and U <= 4; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
+ * only where every row spans < 65536 columns); bit 0 = TMA needs rows padded to 8 and U <= 4; bit 2
+ * (prefetch) needs the register core and rows padded to 8; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
  * sums each row in the same order, so results are bitwise unchanged.  Drops captured PCG graphs.
  * AMG_EINVAL for a bad level/op or an unavailable configuration. */
 amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);
 
 /* Host view of this rank's share of operator op (0 K_l, 1 P̄_l, 2 R_l) on level l, for hierarchies
- * set up with an amg_dist of nranks > 1 (host_only or not).  Local columns are
- * [owned: global col_begin..col_end-1 | ghosts: ghost[0..n_ghost-1]]; ghost values are received from
- * rank q at offsets recv_off[q] .. recv_off[q]+recv_count[q]; this rank sends the owned entries
- * send_idx[send_off[q] .. send_off[q]+send_count[q]) (local indices) to rank q.  All arrays are
- * library-owned and valid until amg_hierarchy_free.  replicated = 1: the level is held whole by every
- * rank (no view).  AMG_EINVAL if the hierarchy is not distributed or level/op is bad. */
+ * set up with an amg_dist of nranks > 1 (host_only or not).  Local column indices keep the global
+ * order: ghost[0..n_ghost-1] holds the ghost columns' global ids ascending, the first n_ghost_lo of them
+ * (owned by lower ranks) have local indices g − n_ghost_lo (negative), owned global column
+ * col_begin + j has local index j, and upper ghost g ≥ n_ghost_lo has col_end − col_begin + g − n_ghost_lo.
+ * Ghost values are received from rank q for ghost positions recv_off[q] .. recv_off[q]+recv_count[q];
+ * this rank sends the owned entries send_idx[send_off[q] .. send_off[q]+send_count[q]) (local indices)
+ * to rank q.  All arrays are library-owned and valid until amg_hierarchy_free.  replicated = 1: the
+ * level is held whole by every rank (no view).  AMG_EINVAL if the hierarchy is not distributed or
+ * level/op is bad. */
 typedef struct {
     int nranks, replicated, full_cols;
-    int64_t row_begin, row_end, col_begin, col_end, n_ghost;
+    int64_t row_begin, row_end, col_begin, col_end, n_ghost, n_ghost_lo;
     const int64_t *ghost;
     const int32_t *send_count, *send_off, *send_idx, *recv_count, *recv_off;
     amg_csr local;

@@ -276,7 +276,7 @@ class Hierarchy:
             return np.ctypeslib.as_array(ptr, shape=(n,)).copy()
         rp, ci, val, shape = _lib.csr_to_numpy(v.local)
         out.update(full_cols=bool(v.full_cols), row_begin=v.row_begin, row_end=v.row_end,
-                   col_begin=v.col_begin, col_end=v.col_end, ghost=arr(v.ghost, v.n_ghost),
+                   col_begin=v.col_begin, col_end=v.col_end, ghost=arr(v.ghost, v.n_ghost), n_ghost_lo=v.n_ghost_lo,
                    send_count=arr(v.send_count, nr), send_off=arr(v.send_off, nr + 1),
                    recv_count=arr(v.recv_count, nr), recv_off=arr(v.recv_off, nr + 1),
                    local=HostCsr(rp, ci, val, shape))
@@ -287,7 +287,7 @@ class Hierarchy:
         c = _lib.amg_op_config()
         check(lib().amg_operator_config(self._h, level, op, C.byref(c)))
         return dict(layout=("csr", "sell32")[c.layout],
-                    kernel=("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")[c.kernel], G=c.G, U=c.U,
+                    kernel=("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")[c.kernel], G=c.G, U=c.U,
                     stored=c.stored, nnz=c.nnz, alg_bytes=c.alg_bytes, tuned_us=round(c.tuned_us, 2))
 
     def set_op_config(self, level: int, op: int, kernel: int, G: int, U: int) -> None:

@@ -65,7 +65,7 @@ class amg_op_config(C.Structure):
 class amg_dist_view(C.Structure):
     _fields_ = [("nranks", C.c_int), ("replicated", C.c_int), ("full_cols", C.c_int),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("col_begin", C.c_int64), ("col_end", C.c_int64),
-                ("n_ghost", C.c_int64), ("ghost", C.POINTER(C.c_int64)),
+                ("n_ghost", C.c_int64), ("n_ghost_lo", C.c_int64), ("ghost", C.POINTER(C.c_int64)),
                 ("send_count", C.POINTER(C.c_int32)), ("send_off", C.POINTER(C.c_int32)),
                 ("send_idx", C.POINTER(C.c_int32)), ("recv_count", C.POINTER(C.c_int32)),
                 ("recv_off", C.POINTER(C.c_int32)), ("local", amg_csr)]

@@ -218,6 +218,7 @@ amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist
     v->col_begin = L.col_begin;
     v->col_end = L.col_end;
     v->n_ghost = (int64_t)L.ghost.size();
+    v->n_ghost_lo = L.nlo;
     v->ghost = L.ghost.data();
     v->send_count = L.send_count.data();
     v->send_off = L.send_off.data();

@@ -82,15 +82,18 @@ struct HHierarchy {
 };
 
 // ---- multi-GPU plumbing (dist.cpp) ------------------------------------------------------------
-// One rank's share of a distributed operator: its rows [row_begin, row_end), columns renumbered as
-// [owned columns (global col_begin..col_end-1) | ghost columns (ascending global ids)], and the halo
-// plan that fills the ghost slots.  Ghosts owned by rank q are contiguous (global order = rank order).
+// One rank's share of a distributed operator: its rows [row_begin, row_end), columns renumbered in
+// GLOBAL order: lower ghosts −nlo..−1, owned columns 0..nown−1 (global col_begin..col_end−1), upper
+// ghosts nown.. (so a row's local column span equals its global span up to the gaps, which keeps the
+// 16-bit column encoding available), and the halo plan that fills the ghost slots.  Ghosts owned by
+// rank q are contiguous (global order = rank order).
 struct LocalOp {
     int64_t row_begin = 0, row_end = 0;
     int64_t col_begin = 0, col_end = 0;  // owned column range; full_cols: [0, ncols)
     bool full_cols = false;              // columns index a replicated (whole) vector: no ghosts
     HCsr A;                              // local rows x (owned + ghost) columns
-    std::vector<int64_t> ghost;          // global ids of the ghost columns
+    std::vector<int64_t> ghost;          // global ids of the ghost columns, ascending
+    int64_t nlo = 0;                     // ghosts below col_begin (lower ranks): local indices −nlo..−1
     std::vector<int32_t> send_count, send_off, send_idx;  // per destination rank; local owned indices
     std::vector<int32_t> recv_count, recv_off;            // per source rank; offsets into the ghost area
 };

@@ -111,6 +111,8 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
     const int64_t nnz2 = rp[n];
     Buf<int32_t> ci(nnz2);
     Buf<double> v(nnz2);
+    int32_t maxc = 0;
+    for (int64_t k = 0; k < A.nnz(); k++) maxc = std::max(maxc, A.ci[k]);
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) {
         int64_t o = rp[i];
@@ -119,11 +121,13 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
             v[o] = A.v[k];
         }
         // padding continues the row's last run of columns where possible (stays inside the row's
-        // column window); the padded products are 0.0·x[col] for a valid column
-        const int32_t last = A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i + 1] - 1] : -1;
+        // column window and below the largest column present, so inside every gathered vector's
+        // owned + ghost extent); the padded products are 0.0·x[col] for a valid column
+        const bool has = A.rp[i + 1] > A.rp[i];
+        const int32_t last = has ? A.ci[A.rp[i + 1] - 1] : 0;
         for (int32_t t = 1; o < rp[i + 1]; o++, t++) {
             const int64_t c = (int64_t)last + t;
-            ci[o] = (last >= 0 && c < A.ncols) ? (int32_t)c : pad_col(A, i, square);
+            ci[o] = (has && c <= maxc) ? (int32_t)c : pad_col(A, i, square);
             v[o] = 0.0;
         }
     }
@@ -261,7 +265,7 @@ float time_op(DevState &D, DCsr &A, const double *x, const Epi &e, cudaEvent_t e
 }
 
 // Tuning cache (env AMG_TUNE_CACHE = path): one line per tuned operator,
-//   "<rank> <nranks> <level> <role> <nrows> <nnz> <kern> <G> <U> <us>".
+//   "<rank> <nranks> <level> <role> <nrows> <nnz> <kern> <G> <U> <pf> <us>".
 // A hit (same rank, ranks, level, role and operator shape) reuses the stored choice, so separate runs
 // (the bench, its ncu capture) execute the same kernel variants; misses are tuned and appended.
 struct TuneKey {
@@ -273,16 +277,17 @@ bool tune_lookup(const TuneKey &k, DCsr &A) {
     if (!path) return false;
     FILE *f = std::fopen(path, "r");
     if (!f) return false;
-    int r, nr, l, ro, kern, G, U;
+    int r, nr, l, ro, kern, G, U, pf;
     long long n, z;
     float us;
     bool hit = false;
-    while (std::fscanf(f, "%d %d %d %d %lld %lld %d %d %d %f", &r, &nr, &l, &ro, &n, &z, &kern, &G, &U, &us) == 10) {
+    while (std::fscanf(f, "%d %d %d %d %lld %lld %d %d %d %d %f", &r, &nr, &l, &ro, &n, &z, &kern, &G, &U, &pf, &us) == 11) {
         if (r == k.rank && nr == k.nranks && l == k.level && ro == k.role && n == k.nrows && z == k.nnz) {
             if ((kern & 2) && !A.off16) continue;  // stale entry for this operator's encodings
             A.kern = kern;
             A.G = G;
             A.U = U;
+            A.pf = pf;
             A.tuned_us = us;
             hit = true;
         }
@@ -294,8 +299,8 @@ void tune_store(const TuneKey &k, const DCsr &A) {
     const char *path = std::getenv("AMG_TUNE_CACHE");
     if (!path) return;
     if (FILE *f = std::fopen(path, "a")) {
-        std::fprintf(f, "%d %d %d %d %lld %lld %d %d %d %.2f\n", k.rank, k.nranks, k.level, k.role, (long long)k.nrows,
-                     (long long)k.nnz, A.kern, A.G, A.U, A.tuned_us);
+        std::fprintf(f, "%d %d %d %d %lld %lld %d %d %d %d %.2f\n", k.rank, k.nranks, k.level, k.role,
+                     (long long)k.nrows, (long long)k.nnz, A.kern, A.G, A.U, A.pf, A.tuned_us);
         std::fclose(f);
     }
 }
@@ -313,16 +318,19 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
     const int Gs[] = {1, 4, 8, 32};
     const int Us[] = {2, 4, 6, 8};
     float best = 1e30f;
-    int bk = A.kern, bg = A.G, bu = A.U;
+    int bk = A.kern, bg = A.G, bu = A.U, bp = A.pf;
     const int nkern = A.off16 ? 4 : 2;  // kern bit 1 (16-bit column offsets) needs the encoding
     for (int kern = 0; kern < nkern; kern++)
         for (int G : Gs)
-            for (int U : Us) {
+            for (int U : Us)
+                for (int pf = 0; pf < 2; pf++) {
                 if ((kern & 1) && U > 4) continue;
+                if (pf && ((kern & 1) || G == 1)) continue;  // prefetch: register core, groups of > 1 row
                 if ((A.nrows + G - 1) / G < 4 * D.nsm) continue;  // too few warp groups to fill the GPU
                 A.kern = kern;
                 A.G = G;
                 A.U = U;
+                A.pf = pf;
                 float ms;
                 if (role == 0) {
                     dev::EpiCheb<false> e{};
@@ -341,11 +349,13 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
                     bk = kern;
                     bg = G;
                     bu = U;
+                    bp = pf;
                 }
             }
     A.kern = bk;
     A.G = bg;
     A.U = bu;
+    A.pf = bp;
     A.tuned_us = best / 3.f * 1000.f;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -401,7 +411,7 @@ void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
     NCCL_OK(ncclGroupStart());
     for (int q = 0; q < D.nranks; q++) {
         if (A.hs_count[q]) NCCL_OK(ncclSend(A.sbuf + A.hs_off[q], (size_t)A.hs_count[q], ncclFloat64, q, D.comm, st));
-        if (A.hr_count[q]) NCCL_OK(ncclRecv(x + A.gbase + A.hr_off[q], (size_t)A.hr_count[q], ncclFloat64, q, D.comm, st));
+        if (A.hr_count[q]) NCCL_OK(ncclRecv(x + A.slot(A.hr_off[q]), (size_t)A.hr_count[q], ncclFloat64, q, D.comm, st));
     }
     NCCL_OK(ncclGroupEnd());
 }
@@ -601,22 +611,25 @@ static void vcycle(DevState &D, const double *b, double *x, cudaStream_t st, int
 }
 
 namespace {
-// Upload one rank's share of a distributed operator (local columns + halo plan).  gshift moves the
-// ghost columns (and the ghost area) up by gshift slots: P̄_l's ghosts follow K_{l+1}'s in the coarse
-// vector, so the two gatherers' ghost values never share slots.
-void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int64_t gshift = 0) {
+// Upload one rank's share of a distributed operator (local columns + halo plan).  Local columns keep
+// the global order (lower ghosts negative, dist.cpp); lo_shift / hi_shift move the lower / upper ghost
+// columns further out, past another gatherer's ghosts of the same vector (P̄_l's beyond K_{l+1}'s).
+void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int64_t lo_shift = 0, int64_t hi_shift = 0) {
     const int64_t nown = op.col_end - op.col_begin;
-    if (gshift > 0 && !op.full_cols && !op.ghost.empty()) {
+    if ((lo_shift > 0 || hi_shift > 0) && !op.full_cols && !op.ghost.empty()) {
         HCsr A;
         A.nrows = op.A.nrows;
-        A.ncols = op.A.ncols + gshift;
+        A.ncols = op.A.ncols + lo_shift + hi_shift;
         A.rp.alloc(A.nrows + 1);
         std::memcpy(A.rp.data(), op.A.rp.data(), sizeof(int64_t) * (A.nrows + 1));
         const int64_t nnz = op.A.nnz();
         A.ci.alloc(nnz);
         A.v.alloc(nnz);
         std::memcpy(A.v.data(), op.A.v.data(), sizeof(double) * nnz);
-        for (int64_t k = 0; k < nnz; k++) A.ci[k] = op.A.ci[k] >= nown ? (int32_t)(op.A.ci[k] + gshift) : op.A.ci[k];
+        for (int64_t k = 0; k < nnz; k++) {
+            const int32_t c = op.A.ci[k];
+            A.ci[k] = c < 0 ? (int32_t)(c - lo_shift) : c >= nown ? (int32_t)(c + hi_shift) : c;
+        }
         upload_op(D, A, out, false, format, false);
     } else {
         upload_op(D, op.A, out, false, format, false);
@@ -624,8 +637,10 @@ void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int64_t
     if (op.full_cols || D.nranks == 1) return;
     out.halo = true;
     out.nown = nown;
-    out.gbase = nown + (op.ghost.empty() ? 0 : gshift);
     out.nghost = (int64_t)op.ghost.size();
+    out.nlo = op.nlo;
+    out.lo_base = -op.nlo - lo_shift;
+    out.hi_base = nown + hi_shift;
     out.hs_count.assign(op.send_count.begin(), op.send_count.end());
     out.hs_off.assign(op.send_off.begin(), op.send_off.end());
     out.hr_count.assign(op.recv_count.begin(), op.recv_count.end());
@@ -656,7 +671,8 @@ std::vector<int64_t> nccl_allgather_i64(DevState &D, const std::vector<int64_t> 
 constexpr size_t kFlagsOff = 0, kEpochOff = 512, kTicketOff = 576, kDslotOff = 1024, kVecOff = 4096;
 
 // Push plan of operator A's gathered vector: for each owned index j, the (rank, slot) pairs of the
-// other ranks' ghost copies.  meta_of(q) = {gbase, recv_off[0..nranks)} of rank q's copy of A.
+// other ranks' ghost copies.  meta_of(q) = {lo_base, hi_base, nlo, recv_off[0..nranks)} of rank q's
+// copy of A: my t-th value for q lands in q's ghost position recv_off[me] + t.
 void build_push(DevState &D, const LocalOp &op, DCsr &A, const std::vector<int64_t> &meta, size_t meta_stride,
                 size_t meta_pos) {
     const int nr = D.nranks, me = D.rank;
@@ -670,18 +686,45 @@ void build_push(DevState &D, const LocalOp &op, DCsr &A, const std::vector<int64
     std::vector<int> fill(cnt.begin(), cnt.end() - 1);
     for (int q = 0; q < nr; q++) {
         if (q == me || op.send_count[q] == 0) continue;
-        const int64_t *mq = meta.data() + (size_t)q * meta_stride + meta_pos;  // {gbase, recv_off[...]}
-        const int64_t first = mq[0] + mq[1 + me];
+        const int64_t *mq = meta.data() + (size_t)q * meta_stride + meta_pos;
+        const int64_t lo_base = mq[0], hi_base = mq[1], nlo = mq[2], g0 = mq[3 + me];
         for (int t = 0; t < op.send_count[q]; t++) {
             const int j = op.send_idx[op.send_off[q] + t];
-            dst[fill[j]++] = make_int2(q, (int)(first + t));
+            const int64_t g = g0 + t;
+            dst[fill[j]++] = make_int2(q, (int)(g < nlo ? lo_base + g : hi_base + (g - nlo)));
         }
         A.pmask |= 1u << q;
     }
+    A.pushed.assign(nown, 0);
+    for (int64_t j = 0; j < nown; j++) A.pushed[j] = cnt[j + 1] > cnt[j];
     A.push_ptr = D.alloc_n<int>(nown + 1);
     A.push_dst = D.alloc_n<int2>((int64_t)dst.size());
     CUDA_OK(cudaMemcpy(A.push_ptr, cnt.data(), sizeof(int) * (nown + 1), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(A.push_dst, dst.data(), sizeof(int2) * dst.size(), cudaMemcpyHostToDevice));
+}
+
+// Row-group order of a CSR operator for its current G: interior groups (no boundary row) first.
+void build_gorder(DevState &D, DCsr &A) {
+    if (A.bnd.empty() || A.fmt != 0) return;
+    if (const char *e = std::getenv("AMG_P2P_INTERIOR"))  // 0: every kernel waits at its start (debug)
+        if (std::atoi(e) == 0) return;
+    const int64_t G = A.G, ng = (A.nrows + G - 1) / G;
+    std::vector<int> order;
+    order.reserve(ng);
+    std::vector<int> tail;
+    for (int64_t g = 0; g < ng; g++) {
+        bool b = false;
+        for (int64_t i = g * G; i < std::min(A.nrows, (g + 1) * G) && !b; i++) b = A.bnd[i] != 0;
+        (b ? tail : order).push_back((int)g);
+    }
+    A.nint = (int64_t)order.size();
+    order.insert(order.end(), tail.begin(), tail.end());
+    if (!A.gorder || A.gorder_cap < ng) {
+        A.gorder = D.alloc_n<int>(ng);
+        A.gorder_cap = ng;
+    }
+    CUDA_OK(cudaMemcpy(A.gorder, order.data(), sizeof(int) * ng, cudaMemcpyHostToDevice));
+    A.gorder_G = G;
 }
 
 // P2P transport setup: IPC-export the slab, map every other rank's, build the push plans of every
@@ -712,8 +755,8 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
         D.d_base = D.alloc_n<char *>(nr);
         CUDA_OK(cudaMemcpy(D.d_base, bases.data(), sizeof(char *) * nr, cudaMemcpyHostToDevice));
     }
-    // 2. every rank's ghost layout of every distributed operator: {gbase, recv_off[0..nr)}
-    const size_t per = (size_t)nr + 1, stride = per * 3 * (size_t)(ld + 1);
+    // 2. every rank's ghost layout of every distributed operator: {lo_base, hi_base, nlo, recv_off[0..nr)}
+    const size_t per = (size_t)nr + 3, stride = per * 3 * (size_t)(ld + 1);
     std::vector<int64_t> mine(stride, 0);
     for (int l = 0; l <= ld; l++) {
         const DCsr *ops[3] = {&D.lev[l].K, &D.lev[l].R, &D.lev[l].P};
@@ -721,8 +764,10 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
         for (int k = 0; k < 3; k++) {
             int64_t *m = mine.data() + ((size_t)l * 3 + k) * per;
             if (!ops[k]->halo) continue;
-            m[0] = ops[k]->gbase;
-            for (int q = 0; q < nr; q++) m[1 + q] = lops[k]->recv_off[q];
+            m[0] = ops[k]->lo_base;
+            m[1] = ops[k]->hi_base;
+            m[2] = ops[k]->nlo;
+            for (int q = 0; q < nr; q++) m[3 + q] = lops[k]->recv_off[q];
         }
     }
     const std::vector<int64_t> meta = nccl_allgather_i64(D, mine);
@@ -751,8 +796,41 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
                               (l + 1 <= ld) ? &D.lev[l + 1].K : nullptr};
         for (const DCsr *A : ops)
             if (A) m |= recv_mask(*A) | A->pmask;
+        if (const char *e = std::getenv("AMG_P2P_MASK"))  // 0: wait for every rank (debug)
+            if (std::atoi(e) == 0) m = ~0u;
         D.lev[l].K.wmask = D.lev[l].P.wmask = m;
         D.lev[l].R.wmask = (l == ld) ? ~0u : m;
+    }
+    // boundary rows (touch a ghost value or are pushed somewhere) of every distributed operator; the
+    // CSR cores run the other row groups before waiting for any peer
+    auto ghost_rows = [&](const LocalOp &op, std::vector<char> &b) {
+        const int64_t nown = op.col_end - op.col_begin;
+        b.assign(op.A.nrows, 0);
+        if (op.full_cols) return;
+        for (int64_t i = 0; i < op.A.nrows; i++)
+            for (int64_t k = op.A.rp[i]; k < op.A.rp[i + 1] && !b[i]; k++) b[i] = op.A.ci[k] < 0 || op.A.ci[k] >= nown;
+    };
+    auto add_pushed = [](std::vector<char> &b, const DCsr *A) {
+        if (!A) return;
+        for (size_t i = 0; i < A->pushed.size() && i < b.size(); i++) b[i] |= A->pushed[i];
+    };
+    for (int l = 0; l <= ld; l++) {
+        DLevel &L = D.lev[l];
+        const DCsr *Pab = l > 0 ? &D.lev[l - 1].P : nullptr;
+        ghost_rows(plan.lev[l].K, L.K.bnd);
+        add_pushed(L.K.bnd, &L.K);
+        add_pushed(L.K.bnd, &L.R);
+        add_pushed(L.K.bnd, Pab);
+        build_gorder(D, L.K);
+        if (l + 1 < D.nlevels) {
+            ghost_rows(plan.lev[l].P, L.P.bnd);
+            add_pushed(L.P.bnd, &L.K);
+            build_gorder(D, L.P);
+            ghost_rows(plan.lev[l].R, L.R.bnd);
+            if (l == ld) std::fill(L.R.bnd.begin(), L.R.bnd.end(), 1);  // all-gather: every row pushed
+            else add_pushed(L.R.bnd, &D.lev[l + 1].K);
+            build_gorder(D, L.R);
+        }
     }
     // 4. all-gather push of the first replicated level's right-hand side: my coarse rows to every rank
     if (ld + 1 < D.nlevels) {
@@ -845,7 +923,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             want_p2p = true;
             for (int q = 0; q < nr; q++) want_p2p = want_p2p && all[q] != 0;
         }
-        std::vector<int64_t> caps(H.nlevels, 0);
+        std::vector<int64_t> vlo(H.nlevels, 0), vhi(H.nlevels, 0);  // ghost extents of the level vectors
         for (int l = 0; l < H.nlevels; l++) {
             const HLevel &h = H.lev[l];
             DLevel &L = D->lev[l];
@@ -860,8 +938,11 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                 L.n = P.K.row_end - P.K.row_begin;
                 upload_local(*D, P.K, L.K, fmt);
                 if (!coarsest) {
+                    // P̄_l's ghosts of the coarse x lie beyond K_{l+1}'s on both sides
+                    const LocalOp &Kc = plan.lev[l + 1].K;
                     const bool next_dist = !plan.lev[l + 1].replicated;
-                    upload_local(*D, P.P, L.P, fmt, next_dist ? (int64_t)plan.lev[l + 1].K.ghost.size() : 0);
+                    const int64_t klo = next_dist ? Kc.nlo : 0, khi = next_dist ? (int64_t)Kc.ghost.size() - Kc.nlo : 0;
+                    upload_local(*D, P.P, L.P, fmt, klo, khi);
                     upload_local(*D, P.R, L.R, fmt);
                 }
             } else {
@@ -876,52 +957,74 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             for (int64_t i = 0; i < L.n; i++) invd[i] = 1.0 / h.dhat[r0 + i];
             L.invd = D->alloc_n<double>(L.n);
             CUDA_OK(cudaMemcpy(L.invd, invd.data(), sizeof(double) * L.n, cudaMemcpyHostToDevice));
-            // vectors gathered by K_l (ghosts at n), P̄_{l-1} (coarse side: after K_l's) or R_l (at n)
-            const int64_t gP = l > 0 ? D->lev[l - 1].P.nghost : 0;
-            caps[l] = L.n + std::max(L.K.nghost + gP, L.R.nghost);
+            // ghost extents below / above the owned block over the gatherers of the level's vectors:
+            // K_l (d, x), P̄_{l-1} (x, beyond K_l's ghosts) and R_l (r)
+            const DCsr *gathers[3] = {&L.K, &L.R, l > 0 ? &D->lev[l - 1].P : nullptr};
+            for (const DCsr *A : gathers) {
+                if (!A || !A->halo) continue;
+                vlo[l] = std::max(vlo[l], -A->lo_base);
+                vhi[l] = std::max(vhi[l], A->hi_base - A->nown + (A->nghost - A->nlo));
+            }
         }
-        const int64_t n00 = D->lev[0].n, cap00 = n00 + D->lev[0].K.nghost;
+        const int64_t n00 = D->lev[0].n;
         // level vectors b, x, r, d0, d1 and the PCG r, z, p, q: in the P2P slab (same offsets on every
         // rank: capacities are maxima over ranks) or from the allocator
         {
-            std::vector<int64_t> want(caps);
+            // (lower extent, owned + upper extent) per vector group: every level, then the PCG vectors
+            // (r, q: no ghosts; z, p: gathered by K_0)
+            std::vector<int64_t> want;
+            for (int l = 0; l < H.nlevels; l++) {
+                want.push_back(vlo[l]);
+                want.push_back(D->lev[l].n + vhi[l]);
+            }
+            want.push_back(0);
             want.push_back(n00);
-            want.push_back(cap00);
-            if (want_p2p) {
+            const DCsr &K0 = D->lev[0].K;
+            want.push_back(K0.halo ? -K0.lo_base : 0);
+            want.push_back(n00 + (K0.halo ? K0.hi_base - K0.nown + (K0.nghost - K0.nlo) : 0));
+            if (want_p2p) {  // identical offsets on every rank: maxima over ranks
                 const std::vector<int64_t> all = nccl_allgather_i64(*D, want);
                 for (size_t k = 0; k < want.size(); k++)
                     for (int q = 0; q < nr; q++) want[k] = std::max(want[k], all[(size_t)q * want.size() + k]);
                 size_t bytes = kVecOff;
-                auto add = [&](int64_t n) { bytes += ((size_t)std::max<int64_t>(n, 1) * 8 + 255) / 256 * 256; };
+                auto add = [&](int64_t lo, int64_t rest) {
+                    bytes += ((size_t)std::max<int64_t>(lo + rest, 1) * 8 + 255) / 256 * 256;
+                };
                 for (int l = 0; l < H.nlevels; l++)
-                    for (int k = 0; k < 5; k++) add(want[l]);
-                add(want[H.nlevels]);
-                add(want[H.nlevels + 1]);
-                add(want[H.nlevels + 1]);
-                add(want[H.nlevels]);
+                    for (int k = 0; k < 5; k++) add(want[2 * l], want[2 * l + 1]);
+                const size_t g = 2 * (size_t)H.nlevels;
+                for (int k = 0; k < 2; k++) add(want[g], want[g + 1]);
+                for (int k = 0; k < 2; k++) add(want[g + 2], want[g + 3]);
                 CUDA_OK(cudaMalloc(&D->slab, bytes));
                 CUDA_OK(cudaMemset(D->slab, 0, bytes));
                 D->slab_bytes = bytes;
                 D->slab_used = kVecOff;
             }
-            auto vec = [&](int64_t n) -> double * {
-                if (!want_p2p) return D->alloc_n<double>(n);
-                double *p = reinterpret_cast<double *>(D->slab + D->slab_used);
-                D->slab_used += ((size_t)std::max<int64_t>(n, 1) * 8 + 255) / 256 * 256;
-                return p;
+            // a vector with `lo` ghost slots below its owned block: the returned pointer is owned[0]
+            auto vec = [&](int64_t lo, int64_t rest) -> double * {
+                double *p;
+                if (!want_p2p) {
+                    p = D->alloc_n<double>(lo + rest);
+                } else {
+                    p = reinterpret_cast<double *>(D->slab + D->slab_used);
+                    D->slab_used += ((size_t)std::max<int64_t>(lo + rest, 1) * 8 + 255) / 256 * 256;
+                }
+                return p + lo;
             };
             for (int l = 0; l < H.nlevels; l++) {
                 DLevel &L = D->lev[l];
-                L.b = vec(want[l]);
-                L.x = vec(want[l]);
-                L.r = vec(want[l]);
-                L.d[0] = vec(want[l]);
-                L.d[1] = vec(want[l]);
+                const int64_t lo = want[2 * l], rest = want[2 * l + 1];
+                L.b = vec(lo, rest);
+                L.x = vec(lo, rest);
+                L.r = vec(lo, rest);
+                L.d[0] = vec(lo, rest);
+                L.d[1] = vec(lo, rest);
             }
-            D->r = vec(want[H.nlevels]);
-            D->z = vec(want[H.nlevels + 1]);
-            D->p = vec(want[H.nlevels + 1]);
-            D->q = vec(want[H.nlevels]);
+            const size_t g = 2 * (size_t)H.nlevels;
+            D->r = vec(want[g], want[g + 1]);
+            D->q = vec(want[g], want[g + 1]);
+            D->z = vec(want[g + 2], want[g + 3]);
+            D->p = vec(want[g + 2], want[g + 3]);
         }
         const HLevel &hl = H.lev[H.nlevels - 1];
         if (hl.N > 6144) throw Error{AMG_EINVAL, "coarsest level larger than 6144 rows (raise max_levels)"};
@@ -947,16 +1050,18 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         CUDA_OK(cudaMemset(D->S, 0, sizeof(dev::Scalars)));
         CUDA_OK(cudaMallocHost(&D->hS, sizeof(dev::Scalars)));
         if (fmt == 0) {  // autotune every large operator on scratch vectors
-            int64_t big = 1;
+            int64_t big = 1, lomax = 0;
             for (int l = 0; l < D->nlevels; l++)
-                for (const DCsr *A : {&D->lev[l].K, &D->lev[l].P, &D->lev[l].R})
+                for (const DCsr *A : {&D->lev[l].K, &D->lev[l].P, &D->lev[l].R}) {
                     big = std::max(big, std::max(A->nrows, A->ncols));
-            double *scr = nullptr;  // x, y1, y2, y3 scratch vectors
-            CUDA_OK(cudaMalloc(&scr, sizeof(double) * big * 4));
+                    if (A->halo) lomax = std::max(lomax, -A->lo_base);
+                }
+            double *scr = nullptr;  // x (with room for negative ghost columns), y1, y2, y3 scratch vectors
+            CUDA_OK(cudaMalloc(&scr, sizeof(double) * (big * 4 + lomax)));
             // non-trivial data (not zeros): data-dependent power draw changes the clocks under the cap
-            dev::k_fill_pattern<<<grid_for(*D, big * 4), dev::kBlock>>>(big * 4, scr);
+            dev::k_fill_pattern<<<grid_for(*D, big * 4 + lomax), dev::kBlock>>>(big * 4 + lomax, scr);
             CUDA_OK(cudaGetLastError());
-            double *sx = scr, *y1 = scr + big, *y2 = scr + 2 * big, *y3 = scr + 3 * big;
+            double *sx = scr + lomax, *y1 = sx + big, *y2 = sx + 2 * big, *y3 = sx + 3 * big;
             try {
                 for (int l = 0; l < D->nlevels; l++) {
                     autotune_op(*D, D->lev[l].K, l, 0, sx, y1, y2, y3);
@@ -1203,7 +1308,8 @@ extern "C" amg_status amg_vcycle(amg_hierarchy *H, const double *r, double *z, v
     DevState *D = need_dev(H);
     if (!r || !z) throw Error{AMG_EINVAL, "bad argument"};
     cudaStream_t st = (cudaStream_t)stream;
-    if (D->p2p) {  // pushes address slab vectors: run on the PCG's r/z and copy in/out
+    if (D->nranks > 1) {  // gathered x needs ghost slots (and P2P pushes address slab vectors): run
+                          // on the PCG's r/z and copy in/out
         const size_t bytes = sizeof(double) * (size_t)D->lev[0].n;
         CUDA_OK(cudaMemcpyAsync(D->r, r, bytes, cudaMemcpyDeviceToDevice, st));
         vcycle(*D, D->r, D->z, st, dev::DOT_NONE);
@@ -1285,15 +1391,18 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
     DLevel &L = D->lev[level];
     DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
     if (A.fmt != 0) throw Error{AMG_EINVAL, "operator is not in a CSR layout"};
-    if (kernel < 0 || kernel > 3 || ((kernel & 2) && !A.off16)) throw Error{AMG_EINVAL, "kernel not available for this operator"};
+    if (kernel < 0 || kernel > 7 || ((kernel & 2) && !A.off16) || ((kernel & 4) && ((kernel & 1) || A.mult < 8)))
+        throw Error{AMG_EINVAL, "kernel not available for this operator"};
     if ((kernel & 1) && (A.mult < 8 || U > 4)) throw Error{AMG_EINVAL, "TMA core needs rows padded to 8 and U <= 4"};
     if (!(G == 1 || G == 4 || G == 8 || G == 32) || !(U == 2 || U == 4 || U == 6 || U == 8))
         throw Error{AMG_EINVAL, "G must be 1, 4, 8 or 32 and U 2, 4, 6 or 8"};
     CUDA_OK(cudaDeviceSynchronize());
-    A.kern = kernel;
+    A.kern = kernel & 3;
+    A.pf = (kernel >> 2) & 1;
     A.G = G;
     A.U = U;
     A.tuned_us = 0.f;
+    build_gorder(*D, A);
     for (auto &sg : D->seg)  // captured graphs hold the old launch configuration
         if (sg.exec) {
             cudaGraphExecDestroy(sg.exec);
@@ -1312,7 +1421,7 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     const DLevel &L = D->lev[level];
     const DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
     cfg->layout = A.fmt;
-    cfg->kernel = A.kern;
+    cfg->kernel = A.kern | (A.pf << 2);
     cfg->G = A.G;
     cfg->U = A.U;
     cfg->stored = A.stored;

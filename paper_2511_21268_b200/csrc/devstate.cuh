@@ -34,6 +34,7 @@ struct DCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
     int fmt = 0;
     int mult = 2;  // CSR layouts: every row padded to a multiple of `mult` entries
+    int pf = 0;    // register CSR core: L2 bulk prefetch of the next row (autotuned)
     int64_t *rp = nullptr;    // CSR2 row pointers (entries)
     int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
     int32_t *ci = nullptr;
@@ -53,10 +54,12 @@ struct DCsr {
         return 8.0 * (double)nnz + idx + 8.0 * (double)(nrows + 1);
     }
     float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
-    // halo plan (multi-GPU): ghost slots [gbase, gbase + nghost) of the gathered vector (gbase = nown,
-    // except P̄_l whose ghosts follow K_{l+1}'s in the coarse vector)
+    // halo plan (multi-GPU): ghost g (ascending global id) sits at slot lo_base + g of the gathered
+    // vector if g < nlo (lower ranks, negative slots) and at hi_base + g − nlo otherwise.  K_l's ghosts
+    // are adjacent to the owned block; P̄_{l−1}'s (the other gatherer of a coarse x) lie beyond them.
     bool halo = false;
-    int64_t nown = 0, nghost = 0, nsend = 0, gbase = 0;
+    int64_t nown = 0, nghost = 0, nsend = 0, nlo = 0, lo_base = 0, hi_base = 0;
+    int64_t slot(int64_t g) const { return g < nlo ? lo_base + g : hi_base + (g - nlo); }
     // P2P transport: part = this operator's kernels take part in the cross-GPU lock-step; push_ptr /
     // push_dst = where this rank's owned entries of the vector this operator GATHERS go on other ranks
     // (rank, slot), CSR over the owned index
@@ -65,6 +68,10 @@ struct DCsr {
     unsigned pmask = 0;  // ranks this operator's push plan sends to
     int *push_ptr = nullptr;
     int2 *push_dst = nullptr;
+    std::vector<char> pushed;   // host: owned index i has a push destination
+    std::vector<char> bnd;      // host: row i touches a ghost value or is pushed (P2P boundary row)
+    int *gorder = nullptr;      // device: row groups (of the current G) interior-first
+    int64_t nint = 0, gorder_G = 0, gorder_cap = 0;
     int *sidx = nullptr;     // device: local owned indices to send, by destination rank
     double *sbuf = nullptr;  // device: packed send buffer
     std::vector<int> hs_count, hs_off, hr_count, hr_off;  // halo send/recv counts and offsets per rank
@@ -148,7 +155,14 @@ inline dev::P2P p2p_of(const DevState &D, bool part, unsigned mask = ~0u) {
     p.wait_mask = mask;
     return p;
 }
-inline dev::P2P p2p_of(const DevState &D, const DCsr &A) { return p2p_of(D, A.part, A.wmask); }
+inline dev::P2P p2p_of(const DevState &D, const DCsr &A) {
+    dev::P2P p = p2p_of(D, A.part, A.wmask);
+    if (p.nranks > 0 && A.fmt == 0 && A.gorder && A.gorder_G == A.G) {
+        p.gorder = A.gorder;
+        p.nint = A.nint;
+    }
+    return p;
+}
 // dot products of the PCG are global: with P2P every rank deposits into every rank's slots
 inline dev::DotCtx dotctx(DevState &D, int kind) {
     return dev::DotCtx{D.partials, D.counter, D.S, kind, (kind != dev::DOT_NONE) ? p2p_of(D, true) : dev::P2P{}};

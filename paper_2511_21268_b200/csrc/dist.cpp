@@ -71,11 +71,16 @@ void make_local(const HCsr &A, const std::vector<int64_t> &rb, const std::vector
         L.ghost.swap(g);
     }
     L.A.ncols = nown + (int64_t)L.ghost.size();
+    L.nlo = std::lower_bound(L.ghost.begin(), L.ghost.end(), c0) - L.ghost.begin();
     for (int64_t t = 0; t < nnz; t++) {
         const int64_t c = A.ci[base + t];
         int64_t lc;
-        if (c >= c0 && c < c1) lc = c - c0;
-        else lc = nown + (std::lower_bound(L.ghost.begin(), L.ghost.end(), c) - L.ghost.begin());
+        if (c >= c0 && c < c1) {
+            lc = c - c0;
+        } else {
+            const int64_t g = std::lower_bound(L.ghost.begin(), L.ghost.end(), c) - L.ghost.begin();
+            lc = g < L.nlo ? g - L.nlo : nown + (g - L.nlo);
+        }
         L.A.ci[t] = (int32_t)lc;
     }
     // receive segments: ghosts owned by rank q are contiguous

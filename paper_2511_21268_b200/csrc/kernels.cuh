@@ -55,6 +55,11 @@ struct P2P {
     long long flags_off;         // byte offset of flags[] in every slab
     long long dslot_off;         // byte offset of the dot slots dslot[kind][rank] in every slab
     unsigned wait_mask;          // ranks this kernel reads from or writes to (bit q): the ones it waits for
+    // CSR cores: row groups in the order interior-first.  Groups at positions < nint touch no ghost value
+    // and push nothing, so they run WITHOUT waiting; each warp waits once, before its first boundary
+    // group (gorder == nullptr: wait at the kernel start).
+    const int *gorder;
+    long long nint;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -84,6 +89,23 @@ __device__ __forceinline__ void peer_wait(const P2P &pp) {
         }
     }
     __syncthreads();
+}
+
+// Warp-level wait of the interior-first CSR cores (lane 0 polls; __syncwarp orders the warp's loads).
+__device__ __forceinline__ void peer_wait_warp(const P2P &pp) {
+    if (pp.nranks == 0) return;
+    if ((threadIdx.x & 31) == 0) {
+        const unsigned long long e = *(volatile unsigned long long *)pp.epoch;
+        for (int q = 0; q < pp.nranks; q++) {
+            if (!((pp.wait_mask >> q) & 1u)) continue;
+            long long spins = 0;
+            while (ld_acquire_sys(pp.flags + q) < e) {
+                __nanosleep(100);
+                if (++spins > (1ll << 26)) __trap();
+            }
+        }
+    }
+    __syncwarp();
 }
 
 // Kernel epilogue (every CTA, after all its stores): the last CTA to finish publishes the new count.
@@ -378,6 +400,11 @@ __device__ __forceinline__ unsigned ld_stream(const unsigned *p, uint64_t pol) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
+// L2 prefetch of a contiguous byte range by one thread (bulk async copy engine; no registers held).
+// Address and size must be multiples of 16.
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 // Gather of the multiplied vector through the read-only path (L1-allocating).
 __device__ __forceinline__ double ld_gather(const double *p) {
     double r;
@@ -425,18 +452,27 @@ struct ColsD16 {
 // (2l, 2l+1) pairing, measured on the C3 levels), accumulating them in two separate chains.  U windows
 // are loaded back to back before any is consumed.  The row sum is a fixed xor-shuffle tree of the
 // 32 lanes' (chain0 + chain1); all CSR kernel variants use exactly this order (bitwise-equal results).
+// pf = 1: while reducing row t of a group, lane 0 has the bulk-copy engine prefetch row t+1's values
+// and column data into L2, so the next row's loads hit L2 instead of DRAM (more bytes in flight per
+// warp without holding registers).
 template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp, Cols cols,
                                                  const double *__restrict__ v, const double *__restrict__ g,
-                                                 int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
-    peer_wait(pp);
+                                                 int64_t nrows, Epi epi, DotCtx dc, P2P pp, int pf) {
+    if (!pp.gorder) peer_wait(pp);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t ngroups = (nrows + G - 1) / G;
     const uint64_t pol = stream_policy();
     double dacc = 0.0;
-    for (int64_t grp = warp; grp < ngroups; grp += nwarps) {
+    bool waited = pp.gorder == nullptr;
+    for (int64_t pos = warp; pos < ngroups; pos += nwarps) {
+        if (!waited && pos >= pp.nint) {
+            peer_wait_warp(pp);
+            waited = true;
+        }
+        const int64_t grp = pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos;
         const int64_t r0 = grp * G;
         const int nr = (int)(nrows - r0 < (int64_t)G ? nrows - r0 : (int64_t)G);
         // group prologue, one round trip for the whole group: lane t fetches row r0+t's pointers and
@@ -454,15 +490,24 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
         for (int t = 0; t < nr; t++) {
             const int64_t b = __shfl_sync(0xffffffffu, gb, t), e = __shfl_sync(0xffffffffu, ge, t);
             const int rs = __shfl_sync(0xffffffffu, grs, t);
+            if (pf && t + 1 < nr) {
+                const int64_t nb = __shfl_sync(0xffffffffu, gb, t + 1), ne = __shfl_sync(0xffffffffu, ge, t + 1);
+                if (lane == 0 && ne > nb && ((nb * Cols::kIdxBytes) & 15) == 0 && (((ne - nb) * Cols::kIdxBytes) & 15) == 0) {
+                    prefetch_l2(v + nb, (uint32_t)((ne - nb) * 8));
+                    prefetch_l2(cols.stream(nb), (uint32_t)((ne - nb) * Cols::kIdxBytes));
+                }
+            }
             double s0 = 0.0, s1 = 0.0;
             for (int64_t k0 = b + lane; k0 < e; k0 += 64 * U) {
                 double va[U], vb[U];
                 int ca[U], cb[U];
+                // past the row end: column 0 (always a valid index) with value 0.0 — no sentinel, since
+                // distributed operators have negative (lower-ghost) columns
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int64_t ka = k0 + 64 * u, kb = ka + 32;
-                    ca[u] = ka < e ? cols.col(ka, rs, pol) : -1;
-                    cb[u] = kb < e ? cols.col(kb, rs, pol) : -1;
+                    ca[u] = ka < e ? cols.col(ka, rs, pol) : 0;
+                    cb[u] = kb < e ? cols.col(kb, rs, pol) : 0;
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
@@ -473,8 +518,8 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
                 double xa[U], xb[U];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    xa[u] = ca[u] >= 0 ? ld_gather(g + ca[u]) : 0.0;
-                    xb[u] = cb[u] >= 0 ? ld_gather(g + cb[u]) : 0.0;
+                    xa[u] = ld_gather(g + ca[u]);
+                    xb[u] = ld_gather(g + cb[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
@@ -552,7 +597,7 @@ template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ rp, Cols cols,
                                                    const double *__restrict__ v, const double *__restrict__ g,
                                                    int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
-    peer_wait(pp);
+    if (!pp.gorder) peer_wait(pp);
     using C = TmaCfg<U, Cols::kIdxBytes>;
     constexpr int NS = C::NS;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -569,12 +614,13 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
     const int64_t ngroups = (nrows + G - 1) / G;
     const uint64_t pol = stream_policy();
 
-    // chunk cursor: group, row-in-group, entry range [k0, min(k0 + CH, e)) of the row
+    // chunk cursor: position in the group order, group, row-in-group, entry range [k0, min(k0+CH, e))
     struct Cur {
-        int64_t grp, k0, e;
+        int64_t pos, grp, k0, e;
         int t, nr;
         bool valid, gfirst;  // gfirst: first chunk of the group's first row
     };
+    auto group_of = [&](int64_t pos) -> int64_t { return pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos; };
     auto row_start = [&](Cur &c) {
         const int64_t row = c.grp * G + c.t;
         c.k0 = __ldg(rp + row);
@@ -589,12 +635,13 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
             return;
         }
         if (++c.t >= c.nr) {
-            c.grp += nwarps;
+            c.pos += nwarps;
             c.t = 0;
-            if (c.grp >= ngroups) {
+            if (c.pos >= ngroups) {
                 c.valid = false;
                 return;
             }
+            c.grp = group_of(c.pos);
             c.nr = (int)(nrows - c.grp * G < (int64_t)G ? nrows - c.grp * G : (int64_t)G);
         }
         row_start(c);
@@ -617,10 +664,11 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
     uint32_t phase = 0;  // bit s = parity of stage s
     // cur = chunk being reduced; ahead = the last chunk issued (NS−1 chunks in flight ahead of cur)
     Cur cur;
-    cur.grp = warp;
+    cur.pos = warp;
     cur.t = 0;
-    cur.valid = cur.grp < ngroups;
+    cur.valid = cur.pos < ngroups;
     if (cur.valid) {
+        cur.grp = group_of(cur.pos);
         cur.nr = (int)(nrows - cur.grp * G < (int64_t)G ? nrows - cur.grp * G : (int64_t)G);
         row_start(cur);
     }
@@ -631,9 +679,14 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         issue(ahead, k);
     }
     int s = 0;
+    bool waited = pp.gorder == nullptr;
     while (cur.valid) {
         advance(ahead);
         issue(ahead, (s + NS - 1) % NS);
+        if (!waited && cur.pos >= pp.nint) {  // first boundary group of this warp
+            peer_wait_warp(pp);
+            waited = true;
+        }
         if (cur.gfirst && lane < cur.nr) pre = epi.load(cur.grp * G + lane);
         const int rs = cols.row(cur.grp * G + cur.t);
         mbar_wait(&bar[s], (phase >> s) & 1u);

@@ -57,14 +57,21 @@ def _worker(rank, world, port, case, rep_nnz, q):
                 allb = [t.tolist() for t in allb]
                 assert allb[0][0] == 0 and allb[-1][1] == A.shape[0]
                 assert all(allb[k][1] == allb[k + 1][0] for k in range(world - 1))
-                loc = v["local"].to_scipy()
+                loc = v["local"]
                 nown = v["col_end"] - v["col_begin"]
                 ghost = v["ghost"]
                 # local -> global column map reproduces the global rows bitwise
-                gmap = np.concatenate([np.arange(v["col_begin"], v["col_end"]), ghost]) if not v["full_cols"] \
-                    else np.arange(A.shape[1])
+                nlo = v["n_ghost_lo"]
+                if v["full_cols"]:
+                    gmap, shift = np.arange(A.shape[1]), 0
+                else:  # local index li -> gmap[li + nlo]: [lower ghosts | owned | upper ghosts]
+                    gmap = np.concatenate([ghost[:nlo], np.arange(v["col_begin"], v["col_end"]), ghost[nlo:]])
+                    shift = nlo
+                    assert np.all(ghost[:nlo] < v["col_begin"]) and np.all(ghost[nlo:] >= v["col_end"])
                 Ar = A[v["row_begin"]:v["row_end"]]
-                assert np.array_equal(gmap[loc.indices], Ar.indices) and np.array_equal(loc.indptr, Ar.indptr)
+                assert np.array_equal(gmap[loc.indices + shift], Ar.indices) and np.array_equal(loc.indptr, Ar.indptr)
+                # global order kept: every local row is ascending
+                assert all(np.all(np.diff(loc.indices[loc.indptr[i]:loc.indptr[i + 1]]) > 0) for i in range(loc.shape[0]))
                 assert np.array_equal(loc.data.view(np.uint64), Ar.data.view(np.uint64))
                 # halo exchange over gloo
                 x = amg_inputs.uniform_pm1(A.shape[1], seed=100 + 10 * l + op)
@@ -91,8 +98,10 @@ def _worker(rank, world, port, case, rep_nnz, q):
                         o = v["recv_off"][r]
                         ghosts[o:o + len(rbuf)] = rbuf.numpy()
                     assert np.array_equal(ghosts, x[ghost])
-                    xl = np.concatenate([xown, ghosts])
-                y = loc @ xl
+                    xl = np.concatenate([ghosts[:nlo], xown, ghosts[nlo:]])
+                y = np.array([np.dot(loc.data[loc.indptr[i]:loc.indptr[i + 1]],
+                                     xl[loc.indices[loc.indptr[i]:loc.indptr[i + 1]] + shift])
+                              for i in range(loc.shape[0])]) if loc.shape[0] else np.zeros(0)
                 yref = Ar @ x
                 assert np.abs(y - yref).max() <= 1e-14 * (abs(Ar) @ np.abs(x)).max()
                 checked += 1

@@ -41,6 +41,12 @@ def _worker(rank, world, port, case, rep_nnz, transport, q):
         H = amg.Hierarchy(K, amg.params(p), dist=amg.make_dist(rank, world, device=rank))
         b, e = H.local_rows()
         out = {}
+        # one V-cycle on a random residual: every rank's slice of the distributed output
+        rv = amg_inputs.uniform_pm1(K.shape[0], seed=17)
+        zv = H.vcycle(torch.from_numpy(np.ascontiguousarray(rv[b:e])).cuda()).cpu().numpy()
+        vparts = [None] * world
+        dist.all_gather_object(vparts, (b, e, zv))
+        out["vcycle"] = vparts
         for name, rhs in (("sine", F), ("random", amg_inputs.uniform_pm1(K.shape[0]))):
             Fl = torch.from_numpy(np.ascontiguousarray(rhs[b:e])).cuda()
             u, it, rr, hist, st = H.solve(Fl, rtol=1e-6)
@@ -51,6 +57,7 @@ def _worker(rank, world, port, case, rep_nnz, transport, q):
         if rank == 0:
             ref = {}
             H1 = amg.Hierarchy(K, amg.params(p))
+            ref["vcycle"] = H1.vcycle(torch.from_numpy(amg_inputs.uniform_pm1(K.shape[0], seed=17)).cuda()).cpu().numpy()
             for name, rhs in (("sine", F), ("random", amg_inputs.uniform_pm1(K.shape[0]))):
                 Fd = torch.from_numpy(rhs).cuda()
                 u, it, rr, hist, st = H1.solve(Fd, rtol=1e-6)
@@ -84,6 +91,12 @@ def test_distributed_solve_matches_single_gpu(world, case, rep_nnz, transport):
     for pr in procs:
         pr.join(timeout=120)
     assert status == "ok", out
+    # the distributed V-cycle equals the single-GPU one: every row sum is bitwise the same, only the
+    # coarse all-gather / halo data paths differ
+    zv = np.zeros(N)
+    for b, e, zl in out["vcycle"]:
+        zv[b:e] = zl
+    assert np.abs(zv - ref["vcycle"]).max() <= 1e-12 * np.abs(ref["vcycle"]).max()
     for name in ("sine", "random"):
         it, st, hist, parts = out[name]
         it1, u1, u1_8, hist1 = ref[name]

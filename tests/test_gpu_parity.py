@@ -89,7 +89,7 @@ def test_kernel_configs_bitwise_equal(case):
             keep = H.op_config(l, op)
             x = dev(rng.uniform(-1, 1, A.shape[1]))
             ref = None
-            for kern in range(4):
+            for kern in (0, 1, 2, 3, 4, 6):  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch
                 for G in (1, 4, 8, 32):
                     for U in (2, 4, 6, 8):
                         if (kern & 1) and U > 4:
@@ -105,7 +105,7 @@ def test_kernel_configs_bitwise_equal(case):
                             assert np.all(np.abs(y - oracle.spmv(A, xo)) <= 1e-13 * bound + 1e-300)
                         else:
                             assert np.array_equal(y, ref), (l, op, kern, G, U)
-            kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")
+            kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")
             H.set_op_config(l, op, kinds.index(keep["kernel"]), keep["G"], keep["U"])
 
 
@@ -118,7 +118,7 @@ def test_d16_encoding_bytes():
     d16 = H.op_config(0, 0)
     H.set_op_config(0, 0, 0, c["G"], c["U"])
     i32 = H.op_config(0, 0)["alg_bytes"]
-    kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")
+    kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")
     H.set_op_config(0, 0, kinds.index(c["kernel"]), c["G"], c["U"])
     nnz, N = c["nnz"], K.shape[0]
     assert i32 == 12 * nnz + 8 * (N + 1)

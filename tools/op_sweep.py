@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 
 import amg_inputs  # noqa: E402
 
-KINDS = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16")
+KINDS = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")
 
 
 def main():
@@ -42,7 +42,7 @@ def main():
             ncol = info["N"][l] if op != 1 else info["N"][l + 1]
             x = torch.rand(ncol, dtype=torch.float64, device="cuda")
             y = torch.empty(nr, dtype=torch.float64, device="cuda")
-            for kern in range(4):
+            for kern in (0, 1, 2, 3, 4, 6):  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch
                 for G in (1, 4, 8, 32):
                     for U in (2, 4, 6, 8):
                         if (kern & 1) and U > 4:
