@@ -212,9 +212,10 @@ def run_gpu(args) -> None:
            if k == 0 or l + 1 < info["levels"]}
     op_cfg = [ops[(l, 0)] for l in range(info["levels"])]
     k0 = op_cfg[0]
-    cols = "ColsD16" if k0["kernel"].endswith("_d16") else "ColsI32"
+    cols = "ColsD16" if "_d16" in k0["kernel"] else "ColsI32"
     family = "k_csr4t" if k0["kernel"].startswith("csr_tma") else "k_csr2"
-    kname = f"{family}<G={k0['G']},U={k0['U']},EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0)"
+    pf = ", L2 prefetch of the next row" if k0["kernel"].endswith("_pf") else ""
+    kname = f"{family}<G={k0['G']},U={k0['U']},EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0{pf})"
     kkey = f"{family}<{k0['G']},{k0['U']},{cols}>"
     stream = torch.cuda.current_stream()
     Fd = torch.from_numpy(F).cuda()
