@@ -23,6 +23,7 @@ from .core import (  # noqa: F401
     assemble,
     build_liboracle,
     cij,
+    fcg,
     pairwise,
     pcg,
     setup,

@@ -36,7 +36,8 @@ class _CSR(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("agg_steps", C.c_int), ("smooth_prolong", C.c_int), ("match_threshold", C.c_double),
                 ("filter_theta", C.c_double), ("cheb_degree", C.c_int), ("coarse_sweeps", C.c_int),
-                ("coarse_size", C.c_int64), ("max_levels", C.c_int)]
+                ("coarse_size", C.c_int64), ("max_levels", C.c_int), ("coarse_solver", C.c_int),
+                ("coarse_tol", C.c_double), ("coarse_maxit", C.c_int)]
 
 
 class _Level(C.Structure):
@@ -63,6 +64,7 @@ def lib():
         L.or_vcycle.argtypes = [C.c_void_p, dp, dp]
         L.or_smooth.argtypes = [C.c_void_p, C.c_int, dp, dp, C.c_int]
         L.or_pcg.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp, dp]
+        L.or_fcg.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp, dp]
         L.or_cij.argtypes = [C.c_double] * 5
         L.or_cij.restype = C.c_double
         L.or_pairwise.argtypes = [C.POINTER(_CSR), dp, C.c_double, C.POINTER(C.c_int32),
@@ -156,6 +158,9 @@ class OParams:
     coarse_sweeps: int = 30
     coarse_size: int = 50
     max_levels: int = 20
+    coarse_solver: int = 0      # 0: ℓ1-Jacobi sweeps (§4, c.17); 1: diagonal-PCG to coarse_tol (§5.1)
+    coarse_tol: float = 1e-4
+    coarse_maxit: int = 30
 
     @staticmethod
     def for_degree(p: int, **kw) -> "OParams":
@@ -214,7 +219,8 @@ def setup(K: sp.csr_matrix, prm: OParams | None = None) -> OHierarchy:
     prm = prm or OParams()
     b = _Borrowed(K)
     cp = _Params(prm.agg_steps, prm.smooth_prolong, prm.match_threshold, prm.filter_theta,
-                 prm.cheb_degree, prm.coarse_sweeps, prm.coarse_size, prm.max_levels)
+                 prm.cheb_degree, prm.coarse_sweeps, prm.coarse_size, prm.max_levels,
+                 prm.coarse_solver, prm.coarse_tol, prm.coarse_maxit)
     h = C.c_void_p()
     rc = lib().or_setup(C.byref(b.c), C.byref(cp), C.byref(h))
     if rc:
@@ -246,4 +252,15 @@ def pcg(H: OHierarchy, F: np.ndarray, rtol: float = 1e-6, maxit: int = 200, u0: 
     rr = C.c_double(0.0)
     hist = np.full(maxit + 1, np.nan)
     rc = lib().or_pcg(H._h, _dptr(F), _dptr(u), rtol, maxit, C.byref(it), C.byref(rr), _dptr(hist))
+    return u, it.value, rr.value, hist[: it.value + 1], rc
+
+
+def fcg(H: OHierarchy, F: np.ndarray, rtol: float = 1e-6, maxit: int = 200, u0: np.ndarray | None = None):
+    """Flexible CG, Notay's FCG(1) → (u, iters, relres, history, status)."""
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    u = np.zeros_like(F) if u0 is None else np.array(u0, dtype=np.float64)
+    it = C.c_int(0)
+    rr = C.c_double(0.0)
+    hist = np.full(maxit + 1, np.nan)
+    rc = lib().or_fcg(H._h, _dptr(F), _dptr(u), rtol, maxit, C.byref(it), C.byref(rr), _dptr(hist))
     return u, it.value, rr.value, hist[: it.value + 1], rc

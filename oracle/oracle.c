@@ -50,6 +50,12 @@ typedef struct {
     int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30) */
     int64_t coarse_size;    /* stop when N_l <= coarse_size (50) */
     int max_levels;         /* 20 */
+    /* coarsest-level solver: 0 = coarse_sweeps ℓ1-Jacobi sweeps (§4; c.17);
+     * 1 = CG preconditioned by one weighted-Jacobi sweep, to coarse_tol relative or coarse_maxit
+     *     iterations (§5.1) */
+    int coarse_solver;
+    double coarse_tol;      /* 1e-4 */
+    int coarse_maxit;       /* 30 */
 } oparams;
 
 typedef struct {
@@ -682,6 +688,58 @@ static void coarse_solve(const olevel *L, int sweeps, const double *b, double *x
     }
 }
 
+/* §5.1 coarsest solver ("the CG preconditioned by a single sweep of weighted Jacobi as coarse
+ * solver set to achieve a tolerance of 10^{-4} or stop in 30 iterations"): PCG from x = 0 with
+ * z = D⁻¹ r, D = diag(K_L).  One weighted-Jacobi sweep from 0 is ω D⁻¹ r; CG is invariant under the
+ * scalar ω, so the (unstated) weight does not matter.  Stops when ‖r‖₂ <= tol·‖b‖₂ or after maxit. */
+static void coarse_cg(const olevel *L, double tol, int maxit, const double *b, double *x) {
+    const int64_t N = L->N;
+    double *r = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
+    double *z = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
+    double *p = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
+    double *q = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
+    double *dg = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
+    for (int64_t i = 0; i < N; i++) {
+        int found = 0;
+        dg[i] = csr_get(&L->K, i, (int32_t)i, &found);
+        x[i] = 0.0;
+        r[i] = b[i];
+    }
+    double bn = 0.0, rz = 0.0;
+    for (int64_t i = 0; i < N; i++) bn = bn + b[i] * b[i];
+    bn = sqrt(bn);
+    if (bn > 0.0) {
+        for (int64_t i = 0; i < N; i++) {
+            z[i] = r[i] / dg[i];
+            p[i] = z[i];
+            rz = rz + r[i] * z[i];
+        }
+        for (int k = 0; k < maxit; k++) {
+            or_spmv(&L->K, p, q);
+            double pq = 0.0;
+            for (int64_t i = 0; i < N; i++) pq = pq + p[i] * q[i];
+            if (!(pq > 0.0)) break;
+            const double alpha = rz / pq;
+            double rn = 0.0;
+            for (int64_t i = 0; i < N; i++) {
+                x[i] = x[i] + alpha * p[i];
+                r[i] = r[i] - alpha * q[i];
+                rn = rn + r[i] * r[i];
+            }
+            if (sqrt(rn) <= tol * bn) break;
+            double rz_new = 0.0;
+            for (int64_t i = 0; i < N; i++) {
+                z[i] = r[i] / dg[i];
+                rz_new = rz_new + r[i] * z[i];
+            }
+            const double beta = rz_new / rz;
+            for (int64_t i = 0; i < N; i++) p[i] = z[i] + beta * p[i];
+            rz = rz_new;
+        }
+    }
+    free(r); free(z); free(p); free(q); free(dg);
+}
+
 /* c.18: V(l, b): l = L: coarse solve.  Else x = S(b, 0); r = b − K x; e = V(l+1, R r);
  * x += P̄ e; x = S(b, x). */
 static void vcycle_level(const ohier *H, int l, const double *b, double *x) {
@@ -689,7 +747,8 @@ static void vcycle_level(const ohier *H, int l, const double *b, double *x) {
     const int64_t N = L->N;
     double *t = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
     if (l == H->nlevels - 1) {
-        coarse_solve(L, H->prm.coarse_sweeps, b, x, t);
+        if (H->prm.coarse_solver == 1) coarse_cg(L, H->prm.coarse_tol, H->prm.coarse_maxit, b, x);
+        else coarse_solve(L, H->prm.coarse_sweeps, b, x, t);
         free(t);
         return;
     }
@@ -769,6 +828,60 @@ int or_pcg(const ohier *H, const double *F, double *u, double rtol, int maxit, i
         double beta = rho_new / rho;
         for (int64_t i = 0; i < N; i++) p[i] = z[i] + beta * p[i];
         rho = rho_new;
+    }
+done:
+    free(r); free(z); free(p); free(q);
+    return rc;
+}
+
+/* Flexible CG (the paper's outer solver: "the flexible variant of the CG algorithm"), in
+ * Notay's FCG(1) form (truncation 1): α_k = (p_kᵀ r_k)/(p_kᵀ q_k), p_{k+1} = z_{k+1} − ((z_{k+1}ᵀ q_k)/
+ * (p_kᵀ q_k)) p_k.  With a fixed SPD preconditioner it generates the CG iterates; it stays a descent
+ * method when the preconditioner varies (the §5.1 coarse CG makes the V-cycle nonlinear).  Same
+ * stopping test, history and return codes as or_pcg; breakdown if pᵀKp <= 0. */
+int or_fcg(const ohier *H, const double *F, double *u, double rtol, int maxit, int *iters,
+           double *relres, double *hist) {
+    const olevel *L = &H->lev[0];
+    const int64_t N = L->N;
+    double *r = (double *)malloc((size_t)N * sizeof(double));
+    double *z = (double *)malloc((size_t)N * sizeof(double));
+    double *p = (double *)malloc((size_t)N * sizeof(double));
+    double *q = (double *)malloc((size_t)N * sizeof(double));
+    int rc = 0;
+    double nF = sqrt(dot(N, F, F));
+    *iters = 0;
+    if (nF == 0.0) {
+        for (int64_t i = 0; i < N; i++) u[i] = 0.0;
+        *relres = 0.0;
+        if (hist) hist[0] = 0.0;
+        goto done;
+    }
+    or_spmv(&L->K, u, q);
+    for (int64_t i = 0; i < N; i++) r[i] = F[i] - q[i];
+    double rn = sqrt(dot(N, r, r));
+    if (hist) hist[0] = rn / nF;
+    *relres = rn / nF;
+    if (rn <= rtol * nF) goto done;
+    or_vcycle(H, r, z);
+    for (int64_t i = 0; i < N; i++) p[i] = z[i];
+    rc = 1;
+    for (int k = 1; k <= maxit; k++) {
+        or_spmv(&L->K, p, q);
+        const double pq = dot(N, p, q);
+        if (!(pq > 0.0)) { rc = -5; break; }
+        const double alpha = dot(N, p, r) / pq;
+        for (int64_t i = 0; i < N; i++) {
+            u[i] = u[i] + alpha * p[i];
+            r[i] = r[i] - alpha * q[i];
+        }
+        rn = sqrt(dot(N, r, r));
+        *iters = k;
+        *relres = rn / nF;
+        if (hist) hist[k] = rn / nF;
+        if (rn <= rtol * nF) { rc = 0; break; }
+        or_vcycle(H, r, z);
+        const double beta = -dot(N, z, q) / pq;
+        for (int64_t i = 0; i < N; i++) p[i] = z[i] + beta * p[i];
     }
 done:
     free(r); free(z); free(p); free(q);

@@ -1,0 +1,67 @@
+"""Pins of the oracle's paper-cube data path:
+inhomogeneous Dirichlet data by the joint L2 boundary projection, Neumann face loads, lifting.
+
+* the separable fast path equals plain volume/face quadrature with callables (independent routes);
+* a polynomial solution inside the spline space is reproduced to round-off (Galerkin with exactly
+  projected boundary data is exact there) — this fails for a dropped/mis-signed Neumann term, a wrong
+  lifting sign or a wrong projection;
+* the paper's solution u = e^{x+z} sin y converges at rate ≥ p + 0.5 in L2 under refinement.
+"""
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+import oracle
+from oracle import cube_paper as cp
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 4), (2, 5)])
+def test_separable_route_equals_generic_quadrature(p, n):
+    F1, u1 = cp.paper_cube_rhs(p, n)
+    F2, u2 = cp.paper_cube_generic(p, n)
+    assert np.abs(u1 - u2).max() <= 1e-12 * np.abs(u2).max()
+    assert np.abs(F1 - F2).max() <= 1e-12 * np.abs(F2).max()
+
+
+def _poly_problem():
+    ux = lambda x: 1 + x + x * x  # noqa: E731
+    uy = lambda y: 2 + y + y * y  # noqa: E731
+    uz = lambda z: 1 + z * z  # noqa: E731
+    u = lambda x, y, z: ux(x) * uy(y) * uz(z)  # noqa: E731
+    f = lambda x, y, z: -(2 * uy(y) * uz(z) + ux(x) * 2 * uz(z) + ux(x) * uy(y) * 2)  # noqa: E731
+    gN = {4: lambda x, y, z: ux(x) * (1 + 2 * y) * uz(z),      # +∂u/∂y at y = 1
+          5: lambda x, y, z: -ux(x) * uy(y) * 2 * z,           # −∂u/∂z at z = 0
+          6: lambda x, y, z: ux(x) * uy(y) * 2 * z}            # +∂u/∂z at z = 1
+    return u, f, gN
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 3), (2, 4)])
+def test_polynomial_in_the_space_is_reproduced(p, n):
+    u, f, gN = _poly_problem()
+    F, uD = cp.generic_rhs(p, n, f, u, gN)
+    K = oracle.assemble(3, p, n)
+    uf = spla.spsolve(K.tocsc(), F)
+    assert cp.l2_error_full(p, n, uf, uD, exact=u) <= 1e-10
+
+
+def test_lifting_sign_matters():
+    """Sanity of the pin above: dropping the Neumann side 4 or flipping the lifting breaks it."""
+    u, f, gN = _poly_problem()
+    p, n = 2, 3
+    K = oracle.assemble(3, p, n)
+    gN_bad = dict(gN)
+    del gN_bad[4]
+    F, uD = cp.generic_rhs(p, n, f, u, gN_bad)
+    assert cp.l2_error_full(p, n, spla.spsolve(K.tocsc(), F), uD, exact=u) > 1e-3
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_paper_solution_converges_at_order(p):
+    errs = []
+    for n in (4, 8, 16):
+        F, uD = cp.paper_cube_rhs(p, n)
+        K = oracle.assemble(3, p, n)
+        uf = spla.spsolve(K.tocsc(), F)
+        errs.append(cp.l2_error_full(p, n, uf, uD))
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(rates >= p + 0.5), (errs, rates)

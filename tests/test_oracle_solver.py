@@ -6,6 +6,7 @@ import scipy.sparse.linalg as spl
 
 import oracle
 from oracle import bspline
+import amg_inputs
 
 
 def dense_smoother(Kd, dhat, m):
@@ -144,3 +145,55 @@ def test_pcg_deterministic(c1):
     a = oracle.pcg(H, F)
     b = oracle.pcg(H, F)
     assert a[1] == b[1] and np.array_equal(a[0], b[0])
+
+
+# --- NEXT-1 solvers: §5.1 coarse CG and the flexible outer CG ------------------
+def test_coarse_cg_finite_termination():
+    """Coarse solver 1 (CG preconditioned by one weighted-Jacobi sweep) with tolerance 0 and N
+    iterations reaches K⁻¹b (CG finite termination); with the paper's 1e-4 it meets that tolerance."""
+    import scipy.sparse.linalg as spla  # noqa: F401
+    K = oracle.assemble(2, 2, 4)
+    N = K.shape[0]
+    b = amg_inputs.uniform_pm1(N, seed=21)
+    H = oracle.setup(K, oracle.OParams(cheb_degree=4, coarse_size=10 ** 6, coarse_solver=1, coarse_tol=0.0,
+                                       coarse_maxit=N))
+    assert H.nlevels == 1
+    x = oracle.vcycle(H, b)
+    xs = np.linalg.solve(K.toarray(), b)
+    assert np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(xs)
+    H2 = oracle.setup(K, oracle.OParams(cheb_degree=4, coarse_size=10 ** 6, coarse_solver=1))
+    x2 = oracle.vcycle(H2, b)
+    assert np.linalg.norm(b - K @ x2) <= 1e-4 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("case", [(2, 2, 16), (3, 3, 6)])
+def test_fcg_equals_pcg_for_a_fixed_preconditioner(case):
+    """With the linear SPD V-cycle (ℓ1-Jacobi coarse sweeps) Notay's FCG(1) — a different α and β —
+    generates the CG iterates: same iteration count, same solution to round-off."""
+    dim, p, n = case
+    K = oracle.assemble(dim, p, n)
+    F = amg_inputs.uniform_pm1(K.shape[0], seed=22)
+    H = oracle.setup(K, oracle.OParams.for_degree(p))
+    u1, it1, rr1, h1, rc1 = oracle.pcg(H, F, rtol=1e-8)
+    u2, it2, rr2, h2, rc2 = oracle.fcg(H, F, rtol=1e-8)
+    assert rc1 == rc2 == 0 and abs(it1 - it2) <= 1
+    assert np.linalg.norm(u1 - u2) <= 1e-7 * np.linalg.norm(u1)
+    k = min(len(h1), len(h2))
+    assert np.allclose(h1[:k], h2[:k], rtol=1e-5)
+
+
+def test_fcg_with_the_variable_coarse_cg_is_a_descent_method():
+    """With the §5.1 coarse CG (a nonlinear preconditioner) FCG still reduces the energy norm of the
+    error monotonically (α minimises along p) and converges."""
+    K = oracle.assemble(3, 3, 6)
+    F = amg_inputs.uniform_pm1(K.shape[0], seed=23)
+    us = np.linalg.solve(K.toarray(), F)
+    H = oracle.setup(K, oracle.OParams.for_degree(3, coarse_solver=1))
+    energies = []
+    for k in range(1, 12):
+        u, it, rr, h, rc = oracle.fcg(H, F, rtol=0.0, maxit=k)
+        e = u - us
+        energies.append(float(e @ (K @ e)))
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(energies, energies[1:]))
+    u, it, rr, h, rc = oracle.fcg(H, F, rtol=1e-6)
+    assert rc == 0 and np.linalg.norm(F - K @ u) <= 1.01e-6 * np.linalg.norm(F)
