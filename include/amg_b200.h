@@ -60,7 +60,10 @@ typedef struct {
  * binary128 and rounded once (c.3, Remark P:L570-573), in the canonical order of DESIGN.md §3 (c.4).
  *
  * rhs = 0: F = load of the manufactured solution u* = sin(πx) sin(πy/2) [cos(πz)] (c.5);
- * rhs = 1: F = 0.
+ * rhs = 1: F = 0;
+ * rhs = 2: the paper's own cube data (dim 3, Dirichlet sides 1,2,3 only):
+ *          f = −e^{x+z} sin y, g_D = e^{x+z} sin y by one L2 projection onto the Dirichlet faces' trace
+ *          space, Neumann g_N on sides 4-6; F = (source + Neumann load)_free − K_fD u_D (lifting).
  * Outputs: *K (free with amg_csr_free) and *F (length K->n_rows, free with amg_free).
  * Errors: AMG_EINVAL for dim ∉ {2,3}, degree ∉ [1,8], n_elem < 1, sides out of range, or more
  * than 2^31-1 free DOFs; AMG_ENOMEM.
@@ -102,6 +105,14 @@ typedef struct {
                                5 CSR with 16-bit column offsets (TMA-staged values) */
     int host_only;          /* 1: build the hierarchy on the host only (export/inspection; no CUDA call) */
     int num_threads;        /* host setup threads (OpenMP); 0 = runtime default                     */
+    int krylov;             /* outer solver: 0 = PCG (c.19); 1 = flexible CG, Notay's FCG(1)
+                               ("the flexible variant of the CG"): α = pᵀr/pᵀq, β = −zᵀq_prev/pᵀq_prev */
+    int coarse_solver;      /* coarsest level: 0 = coarse_sweeps ℓ1-Jacobi sweeps (§4); 1 = CG
+                               preconditioned by one weighted-Jacobi sweep (D = diag K_L) to coarse_tol
+                               or coarse_maxit iterations (§5.1; a nonlinear preconditioner:
+                               use krylov = 1) */
+    double coarse_tol;      /* 1e-4 */
+    int coarse_maxit;       /* 30 */
 } amg_params;
 
 /* Defaults for spline degree p (sets cheb_degree from the table above). EINVAL for p ∉ [1,8]. */

@@ -45,7 +45,8 @@ class amg_params(C.Structure):
     _fields_ = [("agg_steps", C.c_int), ("smooth_prolong", C.c_int), ("match_threshold", C.c_double),
                 ("filter_theta", C.c_double), ("cheb_degree", C.c_int), ("coarse_sweeps", C.c_int),
                 ("coarse_size", C.c_int64), ("max_levels", C.c_int), ("format", C.c_int),
-                ("host_only", C.c_int), ("num_threads", C.c_int)]
+                ("host_only", C.c_int), ("num_threads", C.c_int), ("krylov", C.c_int), ("coarse_solver", C.c_int),
+                ("coarse_tol", C.c_double), ("coarse_maxit", C.c_int)]
 
 
 class amg_dist(C.Structure):

@@ -83,7 +83,7 @@ amg_status amg_iga_poisson(const amg_iga_desc *d, amg_csr **K, double **F) {
     if (d->degree < 1 || d->degree > 8) throw Error{AMG_EINVAL, "degree must be in [1, 8]"};
     if (d->n_elem < 1) throw Error{AMG_EINVAL, "n_elem must be >= 1"};
     if (d->dirichlet_sides >> (2 * d->dim)) throw Error{AMG_EINVAL, "dirichlet_sides names a side > 2*dim"};
-    if (d->rhs != 0 && d->rhs != 1) throw Error{AMG_EINVAL, "rhs must be 0 or 1"};
+    if (d->rhs < 0 || d->rhs > 2) throw Error{AMG_EINVAL, "rhs must be 0, 1 or 2"};
     HCsr A;
     Buf<double> f;
     iga_assemble(*d, A, f);
@@ -115,6 +115,10 @@ amg_status amg_params_default(amg_params *prm, int p) {
     prm->format = 0;
     prm->host_only = 0;
     prm->num_threads = 0;
+    prm->krylov = 0;
+    prm->coarse_solver = 0;
+    prm->coarse_tol = 1e-4;
+    prm->coarse_maxit = 30;
     return AMG_OK;
     API_END
 }
@@ -127,7 +131,9 @@ amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist 
     if (prm_in) prm = *prm_in;
     else amg_params_default(&prm, 2);
     if (prm.agg_steps < 1 || prm.cheb_degree < 1 || prm.coarse_sweeps < 0 || prm.max_levels < 1 ||
-        prm.coarse_size < 1 || !(prm.filter_theta >= 0.0))
+        prm.coarse_size < 1 || !(prm.filter_theta >= 0.0) || prm.krylov < 0 || prm.krylov > 1 ||
+        prm.coarse_solver < 0 || prm.coarse_solver > 1 || !(prm.coarse_tol >= 0.0) || prm.coarse_maxit < 0 ||
+        prm.format < 0 || prm.format > 5)
         throw Error{AMG_EINVAL, "bad parameter"};
     if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
         throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};

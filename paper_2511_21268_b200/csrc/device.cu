@@ -418,16 +418,21 @@ void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
 
 // a12: sum a per-rank dot product across ranks into the device scalar block: NCCL all-reduce, or (P2P)
 // a one-thread kernel adding the ranks' deposited sums in rank order.
-void allreduce_dot(DevState &D, int kind, cudaStream_t st) {
+void allreduce_dot(DevState &D, int dotkind, cudaStream_t st) {
     if (D.nranks == 1) return;
+    const int kind = dotkind & 255, kind2 = dotkind >> 8;
     if (D.p2p) {
-        dev::k_dot_collect<<<1, 32, 0, st>>>(kind, D.S, p2p_of(D, true));
+        dev::k_dot_collect<<<1, 32, 0, st>>>(kind, kind2, D.S, p2p_of(D, true));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
         return;
     }
-    double *slot = kind == dev::DOT_FF ? &D.S->ff : kind == dev::DOT_RR ? &D.S->rr : kind == dev::DOT_PQ ? &D.S->pq : &D.S->rz;
-    NCCL_OK(ncclAllReduce(slot, slot, 1, ncclFloat64, ncclSum, D.comm, st));
+    for (int k : {kind, kind2}) {
+        if (k == dev::DOT_NONE) continue;
+        double *slot = k == dev::DOT_FF ? &D.S->ff : k == dev::DOT_RR ? &D.S->rr : k == dev::DOT_PQ ? &D.S->pq
+                     : k == dev::DOT_RZ ? &D.S->rz : k == dev::DOT_PR ? &D.S->pr : &D.S->zq;
+        NCCL_OK(ncclAllReduce(slot, slot, 1, ncclFloat64, ncclSum, D.comm, st));
+    }
 }
 
 const double kC0 = 4.0 / 3.0;
@@ -437,7 +442,8 @@ const double kC0 = 4.0 / 3.0;
 // (this rank's rows).  Ghost values reach the gathering kernels either by halo() (NCCL) right before
 // them, or (P2P) by the producing epilogues' pushes (push_of: d_new/d0 along K_l's plan, r along R_l's,
 // x after prolongation along K_l's, the final x of a coarse level along P̄_{l-1}'s).
-void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot) {
+void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot,
+                  const double *final_bdot = nullptr) {
     DLevel &L = D.lev[l];
     const int m = D.m;
     // the first replicated level waits (P2P) for every rank's share of its right-hand side
@@ -449,6 +455,22 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         const size_t full = base + (size_t)L.K.stored * 12 + sizeof(int) * (size_t)(n + 1);
         const int staged = full <= 200 * 1024 ? 1 : 0;
         const size_t smem = staged ? full : base;
+        if (D.coarse_solver == 1) {  // §5.1: CG preconditioned by one weighted-Jacobi sweep
+            const size_t base2 = sizeof(double) * 6 * (size_t)n;
+            const size_t full2 = base2 + (size_t)L.K.stored * 12 + sizeof(int) * (size_t)(n + 1);
+            const int staged2 = full2 <= 200 * 1024 ? 1 : 0;
+            const size_t smem2 = staged2 ? full2 : base2;
+            static size_t attr2 = 0;
+            if (smem2 > 48 * 1024 && smem2 > attr2) {
+                CUDA_OK(cudaFuncSetAttribute(dev::k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+                attr2 = smem2;
+            }
+            dev::k_coarse_cg<<<1, 1024, smem2, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.diag, b, x, D.coarse_tol,
+                                                    D.coarse_maxit, staged2, p2p_of(D, first_rep));
+            D.launches_total++;
+            CUDA_OK(cudaGetLastError());
+            return;
+        }
         static size_t attr = 0;
         if (smem > 48 * 1024 && smem > attr) {
             CUDA_OK(cudaFuncSetAttribute(dev::k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -576,7 +598,8 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         if (lastd) {
             dev::EpiCheb<true> e{};
             e.rin = L.r; e.rout = L.r; e.dold = L.d[cur]; e.dnew = L.d[cur ^ 1]; e.invd = L.invd;
-            e.xin = x; e.dpend = (i == 1) ? L.d[cur] : nullptr; e.xout = x; e.bdot = b; e.a = a; e.bc = bcf;
+            e.xin = x; e.dpend = (i == 1) ? L.d[cur] : nullptr; e.xout = x; e.bdot = final_bdot ? final_bdot : b;
+            e.a = a; e.bc = bcf;
             e.pushD = pd; e.pushX = px;
             launch_csr(D, L.K, L.d[cur], e, st, final_dot);
         } else {
@@ -599,12 +622,13 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
 
 // V-cycle with the rᵀz dot (kind) fused into the last level-0 post-smoothing step (then summed
 // across ranks).
-static void vcycle(DevState &D, const double *b, double *x, cudaStream_t st, int dotkind) {
+// bdot: the vector dotted with the V-cycle output (nullptr: b, giving rᵀz; FCG passes q_prev → zᵀq_prev).
+static void vcycle(DevState &D, const double *b, double *x, cudaStream_t st, int dotkind, const double *bdot = nullptr) {
     const int64_t n0 = D.lev[0].n;
     const bool fused = dotkind != dev::DOT_NONE && D.m > 1 && D.nlevels > 1;
-    vcycle_level(D, 0, b, x, st, fused ? dotkind : dev::DOT_NONE);
+    vcycle_level(D, 0, b, x, st, fused ? dotkind : dev::DOT_NONE, bdot);
     if (dotkind != dev::DOT_NONE && !fused) {
-        dev::k_dot<<<grid_for(D, n0), dev::kBlock, 0, st>>>(n0, b, x, dotctx(D, dotkind));
+        dev::k_dot<<<grid_for(D, n0), dev::kBlock, 0, st>>>(n0, bdot ? bdot : b, x, dotctx(D, dotkind));
         D.launches_total++;
     }
     if (dotkind != dev::DOT_NONE) allreduce_dot(D, dotkind, st);
@@ -890,6 +914,10 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         D->nlevels = H.nlevels;
         D->m = H.prm.cheb_degree;
         D->sweeps = H.prm.coarse_sweeps;
+        D->krylov = H.prm.krylov;
+        D->coarse_solver = H.prm.coarse_solver;
+        D->coarse_tol = H.prm.coarse_tol;
+        D->coarse_maxit = H.prm.coarse_maxit;
         if (const char *e = std::getenv("AMG_GRAPHS")) D->graphs = std::atoi(e) != 0;
         const int nr = dist ? dist->nranks : 1;
         D->rank = dist ? dist->rank : 0;
@@ -952,6 +980,16 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                     upload_op(*D, h.P, L.P, false, fmt, false);
                     upload_op(*D, h.R, L.R, false, fmt, false);
                 }
+            }
+            if (coarsest) {  // diag(K_L) for the §5.1 coarse CG (the coarsest level is whole on every rank)
+                Buf<double> dg(h.N);
+                for (int64_t i = 0; i < h.N; i++) {
+                    dg[i] = 0.0;
+                    for (int64_t k = h.K.rp[i]; k < h.K.rp[i + 1]; k++)
+                        if (h.K.ci[k] == i) dg[i] = h.K.v[k];
+                }
+                L.diag = D->alloc_n<double>(h.N);
+                CUDA_OK(cudaMemcpy(L.diag, dg.data(), sizeof(double) * h.N, cudaMemcpyHostToDevice));
             }
             Buf<double> invd(L.n);
             for (int64_t i = 0; i < L.n; i++) invd[i] = 1.0 / h.dhat[r0 + i];
@@ -1043,7 +1081,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             D->row_end0 = H.lev[0].N;
         }
         const int64_t n0 = D->lev[0].n;
-        D->partials = D->alloc_n<double>(D->nsm * 32 + 32);  // >= any resident grid (<= 32 CTAs per SM)
+        D->partials = D->alloc_n<double>(D->nsm * 64 + 64);  // 2 dots x any resident grid (<= 32 CTAs per SM)
         D->counter = D->alloc_n<unsigned>(4);
         D->S = D->alloc_n<dev::Scalars>(1);
         CUDA_OK(cudaMemset(D->counter, 0, 4 * sizeof(unsigned)));
@@ -1108,18 +1146,26 @@ static void prof_collect(DevState &D, size_t ev0 = 0, size_t ev1 = (size_t)-1, b
 static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
     DLevel &L0 = D.lev[0];
     const int64_t n = L0.n;
-    vcycle(D, D.r, D.z, st, dev::DOT_RZ);  // ρ = rᵀz (all-reduced)
-    dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0,
+    const int flex = D.krylov == 1;
+    if (flex) vcycle(D, D.r, D.z, st, dev::DOT_ZQ, D.q);  // FCG: zᵀq_prev (all-reduced)
+    else vcycle(D, D.r, D.z, st, dev::DOT_RZ);            // CG: ρ = rᵀz (all-reduced)
+    dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0, flex,
                                                            push_of(D, L0.K, D.p), p2p_of(D, L0.K));
     dev::k_roll_rho<<<1, 1, 0, st>>>(D.S);
     D.launches_total += 2;
     {
         halo(D, L0.K, D.p, st);
-        dev::EpiSpmvDot e{D.p, D.q};
-        launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ);
-        allreduce_dot(D, dev::DOT_PQ, st);
+        if (flex) {  // FCG: pᵀq and pᵀr in one pass
+            dev::EpiSpmvDot2 e{D.p, D.r, D.q};
+            launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ | (dev::DOT_PR << 8));
+            allreduce_dot(D, dev::DOT_PQ | (dev::DOT_PR << 8), st);
+        } else {
+            dev::EpiSpmvDot e{D.p, D.q};
+            launch_csr(D, L0.K, D.p, e, st, dev::DOT_PQ);
+            allreduce_dot(D, dev::DOT_PQ, st);
+        }
     }
-    dev::k_pcg_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR));
+    dev::k_pcg_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR), flex);
     D.launches_total++;
     allreduce_dot(D, dev::DOT_RR, st);
     CUDA_OK(cudaGetLastError());
@@ -1220,7 +1266,7 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     for (int k = 1; k <= maxit; k++) {
         // iteration k: [z = V(r); ρ = rᵀz; p = z + βp] then q = Kp, α, u += αp, r −= αq, ‖r‖²
         run_segment(D, k == 1 ? 0 : 1, u, st);
-        if (!(D.hS->rz > 0.0) || !(D.hS->pq > 0.0)) {  // CG breakdown: rᵀz <= 0 or pᵀKp <= 0
+        if ((D.krylov == 0 && !(D.hS->rz > 0.0)) || !(D.hS->pq > 0.0)) {  // breakdown: rᵀz <= 0 (CG) or pᵀKp <= 0
             *iters = k;
             return AMG_ENOTSPD;
         }

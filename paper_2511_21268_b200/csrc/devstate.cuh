@@ -84,6 +84,7 @@ struct DLevel {
     bool replicated = false;
     DCsr K, P, R;
     double *invd = nullptr;
+    double *diag = nullptr;  // coarsest level: diag(K_L) (§5.1 coarse CG)
     double *b = nullptr, *x = nullptr, *r = nullptr, *d[2] = {nullptr, nullptr};
 };
 
@@ -121,6 +122,9 @@ struct DevState {
     dev::Scalars *hS = nullptr;  // pinned host mirror
     double *stage = nullptr;  // device copies of F and u for amg_pcg_solve_host (2·N_0)
     int max_grid = 1184;
+    // solver variants (amg_params): FCG outer iteration, §5.1 coarse CG
+    int krylov = 0, coarse_solver = 0, coarse_maxit = 30;
+    double coarse_tol = 1e-4;
     // profiling
     bool prof = false;
     std::vector<cudaEvent_t> ev;
@@ -164,8 +168,10 @@ inline dev::P2P p2p_of(const DevState &D, const DCsr &A) {
     return p;
 }
 // dot products of the PCG are global: with P2P every rank deposits into every rank's slots
-inline dev::DotCtx dotctx(DevState &D, int kind) {
-    return dev::DotCtx{D.partials, D.counter, D.S, kind, (kind != dev::DOT_NONE) ? p2p_of(D, true) : dev::P2P{}};
+// dotkind = kind | (kind2 << 8): up to two fused dot products of one kernel
+inline dev::DotCtx dotctx(DevState &D, int dotkind) {
+    return dev::DotCtx{D.partials, D.counter, D.S, dotkind & 255,
+                       (dotkind != dev::DOT_NONE) ? p2p_of(D, true) : dev::P2P{}, dotkind >> 8};
 }
 // push descriptor of `buf` (a vector in the own slab) along operator A's push plan
 inline dev::Push push_of(const DevState &D, const DCsr &A, const double *buf) {
@@ -178,7 +184,7 @@ template <class Epi>
 void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind = dev::DOT_NONE);
 
 #define AMGB_EPILOGUES(X) \
-    X(dev::EpiStore) X(dev::EpiSpmvDot) X(dev::EpiResidualFrom) X(dev::EpiCheb<false>) X(dev::EpiCheb<true>) \
+    X(dev::EpiStore) X(dev::EpiSpmvDot) X(dev::EpiSpmvDot2) X(dev::EpiResidualFrom) X(dev::EpiCheb<false>) X(dev::EpiCheb<true>) \
     X(dev::EpiPostFirst) X(dev::EpiRestrict) X(dev::EpiProlong)
 #define AMGB_EXTERN_LAUNCH(E) \
     extern template void launch_csr<E>(DevState &, const DCsr &, const double *, E, cudaStream_t, int);

@@ -180,6 +180,130 @@ std::vector<double> load_factor(int ax, int p, int n) {
     return out;
 }
 
+// 1-D moments ∫_0^1 g(t) N_a(t) dt of all m functions, (p+1)-point Gauss per element in binary128.
+template <class Fn>
+std::vector<double> moments(int p, int n, Fn g) {
+    const int m = n + p;
+    std::vector<q128> F(m, 0);
+    std::vector<q128> gx, gw;
+    gauss_legendre_q(p + 1, gx, gw);
+    q128 val[16], der[16];
+    for (int e = 0; e < n; e++)
+        for (int q = 0; q <= p; q++) {
+            basis_and_derivs(e + p, e + gx[q], p, n, val, der);
+            const q128 x = (e + gx[q]) / n;
+            const q128 f = g(x);
+            for (int i = 0; i <= p; i++) F[e + i] += gw[q] / n * f * val[i];
+        }
+    std::vector<double> out(m);
+    for (int a = 0; a < m; a++) out[a] = (double)F[a];
+    return out;
+}
+
+// The paper's cube data: f = −e^{x+z} sin y, g_D = e^{x+z} sin y
+// on sides 1-3, g_N = e^{x+z} cos y (side 4), −e^{x+z} sin y (5), e^{x+z} sin y (6).  Readings
+// (DESIGN.md §3): g_D by ONE L2 projection onto the trace space of the union of the Dirichlet faces
+// (face mass M⊗M, DOFs on shared edges get both faces' contributions), solved by Jacobi-preconditioned
+// CG to round-off; F_free = (source + Neumann load)_free − (K_full u_D)_free.  All integrals by
+// (p+1)-point Gauss per element and direction.
+void paper_cube_load(int p, int n, const Tables1D &T, const int *lo, const int *nf, Buf<double> &F) {
+    const int m = n + p, bw = 2 * p + 1;
+    const double *M1 = T.M.data(), *K1 = T.K.data();
+    const std::vector<double> E = moments(p, n, [](q128 x) { return expq(x); });
+    const std::vector<double> S = moments(p, n, [](q128 x) { return sinq(x); });
+    const int64_t m3 = (int64_t)m * m * m;
+    auto id = [m](int a, int b, int c) { return (int64_t)a + (int64_t)m * (b + (int64_t)m * c); };
+    auto band = [bw, p](const double *A, int i, int j) { return A[(size_t)i * bw + (j - i + p)]; };
+    // --- joint L2 projection of g_D on faces x=0 (a=0), x=1 (a=m−1), y=0 (b=0) -------------------
+    // y = M_bnd x on the Dirichlet DOFs (x, y full m³ arrays, zero elsewhere)
+    auto onD = [m](int a, int b) { return a == 0 || a == m - 1 || b == 0; };
+    auto apply_bnd = [&](const std::vector<double> &x, std::vector<double> &y) {
+        std::fill(y.begin(), y.end(), 0.0);
+        for (int face = 0; face < 3; face++) {
+            // face 0: a=0, 1: a=m−1 (in-face axes b, c); face 2: b=0 (in-face axes a, c)
+#pragma omp parallel for schedule(static)
+            for (int c = 0; c < m; c++)
+                for (int u = 0; u < m; u++) {
+                    double acc = 0.0;
+                    for (int c2 = std::max(0, c - p); c2 <= std::min(m - 1, c + p); c2++)
+                        for (int u2 = std::max(0, u - p); u2 <= std::min(m - 1, u + p); u2++) {
+                            const int64_t j = face == 2 ? id(u2, 0, c2) : id(face == 0 ? 0 : m - 1, u2, c2);
+                            acc += band(M1, u, u2) * band(M1, c, c2) * x[j];
+                        }
+                    const int64_t i = face == 2 ? id(u, 0, c) : id(face == 0 ? 0 : m - 1, u, c);
+                    y[i] += acc;  // rows of different faces are disjoint except on shared edges
+                }
+        }
+    };
+    std::vector<double> rhs(m3, 0.0), diag(m3, 0.0), x(m3, 0.0), r(m3), z(m3), pp(m3, 0.0), q(m3);
+    for (int c = 0; c < m; c++)
+        for (int u = 0; u < m; u++) {
+            rhs[id(0, u, c)] += S[u] * E[c];              // x = 0: e^z sin y
+            rhs[id(m - 1, u, c)] += M_E * S[u] * E[c];    // x = 1: e·e^z sin y
+            // y = 0: g_D = 0
+            const double mm = band(M1, u, u) * band(M1, c, c);
+            diag[id(0, u, c)] += mm;
+            diag[id(m - 1, u, c)] += mm;
+            diag[id(u, 0, c)] += mm;
+        }
+    double rr = 0.0, bb = 0.0;
+    for (int64_t i = 0; i < m3; i++) {
+        r[i] = rhs[i];
+        z[i] = diag[i] > 0.0 ? r[i] / diag[i] : 0.0;
+        pp[i] = z[i];
+        rr += r[i] * z[i];
+        bb += rhs[i] * rhs[i];
+    }
+    for (int it = 0; it < 100000 && bb > 0.0; it++) {
+        apply_bnd(pp, q);
+        double pq = 0.0;
+        for (int64_t i = 0; i < m3; i++) pq += pp[i] * q[i];
+        if (!(pq > 0.0)) break;
+        const double alpha = rr / pq;
+        double rn = 0.0, rz = 0.0;
+        for (int64_t i = 0; i < m3; i++) {
+            x[i] += alpha * pp[i];
+            r[i] -= alpha * q[i];
+            rn += r[i] * r[i];
+            z[i] = diag[i] > 0.0 ? r[i] / diag[i] : 0.0;
+            rz += r[i] * z[i];
+        }
+        if (rn <= 1e-30 * bb) break;
+        const double beta = rz / rr;
+        for (int64_t i = 0; i < m3; i++) pp[i] = z[i] + beta * pp[i];
+        rr = rz;
+    }
+    for (int a = 0; a < m; a++)
+        for (int b = 0; b < m; b++)
+            if (!onD(a, b))
+                for (int c = 0; c < m; c++) x[id(a, b, c)] = 0.0;
+    // --- lifting L = K_full u_D, K_full = K⊗M⊗M + M⊗K⊗M + M⊗M⊗K, evaluated on the free DOFs ----------
+    const int64_t N = (int64_t)nf[0] * nf[1] * nf[2];
+    F.alloc(N);
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < N; row++) {
+        const int a = lo[0] + (int)(row % nf[0]);
+        const int b = lo[1] + (int)((row / nf[0]) % nf[1]);
+        const int c = lo[2] + (int)(row / ((int64_t)nf[0] * nf[1]));
+        double lift = 0.0;
+        for (int c2 = std::max(0, c - p); c2 <= std::min(m - 1, c + p); c2++)
+            for (int b2 = std::max(0, b - p); b2 <= std::min(m - 1, b + p); b2++)
+                for (int a2 = std::max(0, a - p); a2 <= std::min(m - 1, a + p); a2++) {
+                    const double u = x[id(a2, b2, c2)];
+                    if (u == 0.0) continue;
+                    const double Ma = band(M1, a, a2), Ka = band(K1, a, a2);
+                    const double Mb = band(M1, b, b2), Kb = band(K1, b, b2);
+                    const double Mc = band(M1, c, c2), Kc = band(K1, c, c2);
+                    lift += (Ka * Mb * Mc + Ma * Kb * Mc + Ma * Mb * Kc) * u;
+                }
+        double f = -E[a] * S[b] * E[c];
+        if (b == m - 1) f += std::cos(1.0) * E[a] * E[c];
+        if (c == 0) f += -E[a] * S[b];
+        if (c == m - 1) f += M_E * E[a] * S[b];
+        F[row] = f - lift;
+    }
+}
+
 }  // namespace
 
 void iga_tables_hat(int p, int n, double *mhat, double *khat) { hat_tables(p, n, mhat, khat); }
@@ -260,7 +384,13 @@ void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
             }
         }
     }
-    // load vector (c.5)
+    // load vector (c.5), or the paper's own cube data (rhs = 2)
+    if (d.rhs == 2) {
+        if (dim != 3 || d.dirichlet_sides != 0b000111u)
+            throw Error{AMG_EINVAL, "rhs = 2 (the paper's cube data) needs dim = 3 and Dirichlet sides 1, 2, 3"};
+        paper_cube_load(p, n, T, lo, nf, F);
+        return;
+    }
     F.alloc(N);
     if (d.rhs == 1) {
         std::memset(F.data(), 0, sizeof(double) * N);

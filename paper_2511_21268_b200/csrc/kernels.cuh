@@ -29,10 +29,31 @@ struct Scalars {
     double pq;       // pᵀKp
     double rz;       // ρ = rᵀz of the current iteration
     double rz_prev;  // ρ of the previous iteration (set at the end of each iteration)
-    double pad[3];
+    double pr;       // FCG: pᵀr (α = pᵀr / pᵀq)
+    double zq;       // FCG: zᵀq_prev (β = −zᵀq_prev / pᵀq_prev)
+    double pad;
 };
 
-enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ };
+enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ, DOT_PR, DOT_ZQ, DOT_NKINDS };
+
+__device__ __forceinline__ double *scalar_slot(Scalars *S, int kind) {
+    switch (kind) {
+        case DOT_FF: return &S->ff;
+        case DOT_RR: return &S->rr;
+        case DOT_PQ: return &S->pq;
+        case DOT_RZ: return &S->rz;
+        case DOT_PR: return &S->pr;
+        case DOT_ZQ: return &S->zq;
+        default: return &S->pad;
+    }
+}
+
+// accumulation of one (double) or two (double2) fused dot products
+__device__ __forceinline__ void acc_add(double &a, double b) { a += b; }
+__device__ __forceinline__ void acc_add(double2 &a, double2 b) {
+    a.x += b.x;
+    a.y += b.y;
+}
 
 // ------------------------------------------------------------------------------------------------
 // P2P transport of the multi-GPU path (one process per GPU; every rank's "slab" of vectors, flags and
@@ -145,11 +166,12 @@ struct Push {
 };
 
 struct DotCtx {
-    double *partials;    // >= gridDim.x
+    double *partials;    // >= 2·gridDim.x
     unsigned *counter;   // zero between launches
     Scalars *S;
     int kind;
     P2P pp;              // nranks > 0: deposit the rank's sum in every rank's dslot[kind][rank] instead
+    int kind2;           // second fused dot (double2 accumulators), DOT_NONE if none
 };
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -159,20 +181,26 @@ __device__ __forceinline__ double warp_sum(double s) {
 }
 
 // Deterministic block reduction + "last block finalises" (fixed partial order ⇒ run-to-run
-// identical scalars; no atomics on values).
-template <int BS>
-__device__ __forceinline__ void block_dot_finalize_n(double v, const DotCtx &dc) {
-    __shared__ double red[BS / 32];
+// identical scalars; no atomics on values).  NV values (1 or 2 fused dots) per launch.
+template <int BS, int NV>
+__device__ __forceinline__ void block_dot_finalize_v(const double *v, const DotCtx &dc) {
+    __shared__ double red[NV][BS / 32];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    v = warp_sum(v);
-    if (lane == 0) red[wid] = v;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const double t = warp_sum(v[k]);
+        if (lane == 0) red[k][wid] = t;
+    }
     __syncthreads();
     if (wid == 0) {
-        double t = lane < BS / 32 ? red[lane] : 0.0;
-        t = warp_sum(t);
+#pragma unroll
+        for (int k = 0; k < NV; k++) {
+            double t = lane < BS / 32 ? red[k][lane] : 0.0;
+            t = warp_sum(t);
+            if (lane == 0) dc.partials[(size_t)k * gridDim.x + blockIdx.x] = t;
+        }
         if (lane == 0) {
-            dc.partials[blockIdx.x] = t;
             __threadfence();
             unsigned ticket = atomicAdd(dc.counter, 1u);
             last = (ticket == gridDim.x - 1);
@@ -181,34 +209,46 @@ __device__ __forceinline__ void block_dot_finalize_n(double v, const DotCtx &dc)
     __syncthreads();
     if (!last) return;
     __threadfence();
-    double t = 0.0;
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += BS) t += __ldcg(dc.partials + i);
-    t = warp_sum(t);
-    if (lane == 0) red[wid] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    double tot[NV];
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        double t = 0.0;
+        for (unsigned i = threadIdx.x; i < gridDim.x; i += BS) t += __ldcg(dc.partials + (size_t)k * gridDim.x + i);
+        t = warp_sum(t);
+        __syncthreads();
+        if (lane == 0) red[k][wid] = t;
+        __syncthreads();
         double s = 0.0;
-        for (int w = 0; w < BS / 32; w++) s += red[w];
-        if (dc.pp.nranks > 0) {  // P2P: every rank sums the slots in rank order (k_dot_collect)
-            for (int q = 0; q < dc.pp.nranks; q++)
-                *reinterpret_cast<double *>(dc.pp.base[q] + dc.pp.dslot_off +
-                                            8ll * (dc.kind * dc.pp.nranks + dc.pp.rank)) = s;
-            *dc.counter = 0u;
-            return;
-        }
-        Scalars *S = dc.S;
-        switch (dc.kind) {
-            case DOT_FF: S->ff = s; break;
-            case DOT_RR: S->rr = s; break;
-            case DOT_PQ: S->pq = s; break;
-            case DOT_RZ: S->rz = s; break;
-            default: break;
+        for (int w = 0; w < BS / 32; w++) s += red[k][w];
+        tot[k] = s;
+    }
+    if (threadIdx.x == 0) {
+        const int kinds[2] = {dc.kind, dc.kind2};
+        for (int k = 0; k < NV; k++) {
+            if (dc.pp.nranks > 0) {  // P2P: every rank sums the slots in rank order (k_dot_collect)
+                for (int q = 0; q < dc.pp.nranks; q++)
+                    *reinterpret_cast<double *>(dc.pp.base[q] + dc.pp.dslot_off +
+                                                8ll * (kinds[k] * dc.pp.nranks + dc.pp.rank)) = tot[k];
+            } else {
+                *scalar_slot(dc.S, kinds[k]) = tot[k];
+            }
         }
         *dc.counter = 0u;
     }
 }
 
-__device__ __forceinline__ void block_dot_finalize(double v, const DotCtx &dc) { block_dot_finalize_n<kBlock>(v, dc); }
+template <int BS>
+__device__ __forceinline__ void block_dot_finalize_n(double v, const DotCtx &dc) {
+    block_dot_finalize_v<BS, 1>(&v, dc);
+}
+template <int BS>
+__device__ __forceinline__ void block_dot_finalize_n(double2 v, const DotCtx &dc) {
+    const double a[2] = {v.x, v.y};
+    block_dot_finalize_v<BS, 2>(a, dc);
+}
+
+template <class T>
+__device__ __forceinline__ void block_dot_finalize(T v, const DotCtx &dc) { block_dot_finalize_n<kBlock>(v, dc); }
 
 // ------------------------------------------------------------------------------------------------
 // Epilogues.  load(row) fetches the row's vector inputs; the cores call it when a row group STARTS, so
@@ -220,6 +260,7 @@ struct NoPre {};
 
 struct EpiStore {  // y = A x
     static constexpr bool kDot = false;
+    using Acc = double;
     using Pre = NoPre;
     double *y;
     __device__ __forceinline__ Pre load(int64_t) const { return {}; }
@@ -228,6 +269,7 @@ struct EpiStore {  // y = A x
 
 struct EpiSpmvDot {  // a1: q = K p, pᵀq
     static constexpr bool kDot = true;
+    using Acc = double;
     struct Pre { double p; };
     const double *p;
     double *q;
@@ -238,8 +280,24 @@ struct EpiSpmvDot {  // a1: q = K p, pᵀq
     }
 };
 
+// a1 for the flexible CG: q = K p with both pᵀq and pᵀr (α = pᵀr / pᵀq)
+struct EpiSpmvDot2 {
+    static constexpr bool kDot = true;
+    using Acc = double2;
+    struct Pre { double p, r; };
+    const double *p;
+    const double *r;
+    double *q;
+    __device__ __forceinline__ Pre load(int64_t i) const { return {p[i], r[i]}; }
+    __device__ __forceinline__ double2 operator()(int64_t i, double s, const Pre &pr) const {
+        q[i] = s;
+        return make_double2(pr.p * s, pr.p * pr.r);
+    }
+};
+
 struct EpiResidualFrom {  // r = b − K x  (also: r −= K d with b == r);  optionally x = dpend
     static constexpr bool kDot = false;
+    using Acc = double;
     struct Pre { double b, dp; };
     const double *b;
     double *r;
@@ -261,6 +319,7 @@ struct EpiResidualFrom {  // r = b − K x  (also: r −= K d with b == r);  opt
 template <bool kDotRZ>
 struct EpiCheb {
     static constexpr bool kDot = kDotRZ;
+    using Acc = double;
     struct Pre { double rin, dold, invd, xin, dp, bd; };  // raw loads only: no arithmetic until the row sum
     const double *rin;
     double *rout;
@@ -300,6 +359,7 @@ struct EpiCheb {
 
 struct EpiPostFirst {  // a9: r = b − K x;  d0 = c0·(r·invd)  (x += d0 is folded into the next step)
     static constexpr bool kDot = false;
+    using Acc = double;
     struct Pre { double b, invd; };
     const double *b;
     double *r;
@@ -320,6 +380,7 @@ struct EpiPostFirst {  // a9: r = b − K x;  d0 = c0·(r·invd)  (x += d0 is fo
 
 struct EpiRestrict {  // a6 (+a3 of the coarse level): b_c = R r;  d0_c = c0·(b_c·invd_c)
     static constexpr bool kDot = false;
+    using Acc = double;
     struct Pre { double invd; };
     double *bc;
     const double *invd;  // nullable (coarsest level: no smoother)
@@ -341,6 +402,7 @@ struct EpiRestrict {  // a6 (+a3 of the coarse level): b_c = R r;  d0_c = c0·(b
 
 struct EpiProlong {  // a8: x += P̄ e
     static constexpr bool kDot = false;
+    using Acc = double;
     struct Pre { double x; };
     double *x;
     Push pushX;
@@ -465,7 +527,7 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t ngroups = (nrows + G - 1) / G;
     const uint64_t pol = stream_policy();
-    double dacc = 0.0;
+    typename Epi::Acc dacc{};
     bool waited = pp.gorder == nullptr;
     for (int64_t pos = warp; pos < ngroups; pos += nwarps) {
         if (!waited && pos >= pp.nint) {
@@ -530,7 +592,7 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
             const double s = warp_sum(s0 + s1);
             if (lane == t) mine = s;
         }
-        if (lane < nr) dacc += epi(r0 + lane, mine, pre);
+        if (lane < nr) acc_add(dacc, epi(r0 + lane, mine, pre));
     }
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
     peer_signal(pp);
@@ -659,7 +721,8 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         }
     };
 
-    double dacc = 0.0, acc = 0.0, acc1 = 0.0, mine = 0.0;
+    double acc = 0.0, acc1 = 0.0, mine = 0.0;
+    typename Epi::Acc dacc{};
     typename Epi::Pre pre{};
     uint32_t phase = 0;  // bit s = parity of stage s
     // cur = chunk being reduced; ahead = the last chunk issued (NS−1 chunks in flight ahead of cur)
@@ -719,7 +782,7 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
             acc1 = 0.0;
             if (lane == cur.t) mine = sum;
             if (cur.t == cur.nr - 1) {  // last row of the group: coalesced epilogue
-                if (lane < cur.nr) dacc += epi(cur.grp * G + lane, mine, pre);
+                if (lane < cur.nr) acc_add(dacc, epi(cur.grp * G + lane, mine, pre));
                 mine = 0.0;
             }
         }
@@ -748,7 +811,7 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t nslices = (nrows + 31) >> 5;
     const uint64_t pol = stream_policy();
-    double dacc = 0.0;
+    typename Epi::Acc dacc{};
     for (int64_t sl = warp; sl < nslices; sl += nwarps) {
         const int64_t off = __ldg(soff + sl);
         const int W = (int)((__ldg(soff + sl + 1) - off) >> 5);
@@ -781,7 +844,7 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
             acc[0] = fma(va.x, __ldg(g + ca.x), acc[0]);
             acc[0] = fma(va.y, __ldg(g + ca.y), acc[0]);
         }
-        if (row < nrows) dacc += epi(row, (acc[0] + acc[1]) + (acc[2] + acc[3]), pre);
+        if (row < nrows) acc_add(dacc, epi(row, (acc[0] + acc[1]) + (acc[2] + acc[3]), pre));
     }
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
     peer_signal(pp);
@@ -819,18 +882,16 @@ __global__ void __launch_bounds__(kBlock) k_copy_push(int64_t n, const double *_
 
 // P2P all-reduce of one dot product: every rank deposited its sum in dslot[kind][q] of every rank
 // (block_dot_finalize); each rank adds them in rank order (identical on every rank).
-__global__ void k_dot_collect(int kind, Scalars *S, P2P pp) {
+__global__ void k_dot_collect(int kind, int kind2, Scalars *S, P2P pp) {
     peer_wait(pp);
     if (threadIdx.x == 0) {
-        const double *slot = reinterpret_cast<const double *>(pp.base[pp.rank] + pp.dslot_off) + kind * pp.nranks;
-        double s = 0.0;
-        for (int q = 0; q < pp.nranks; q++) s += *(volatile const double *)(slot + q);
-        switch (kind) {
-            case DOT_FF: S->ff = s; break;
-            case DOT_RR: S->rr = s; break;
-            case DOT_PQ: S->pq = s; break;
-            case DOT_RZ: S->rz = s; break;
-            default: break;
+        const int kinds[2] = {kind, kind2};
+        for (int k = 0; k < 2; k++) {
+            if (kinds[k] == DOT_NONE) continue;
+            const double *slot = reinterpret_cast<const double *>(pp.base[pp.rank] + pp.dslot_off) + kinds[k] * pp.nranks;
+            double s = 0.0;
+            for (int q = 0; q < pp.nranks; q++) s += *(volatile const double *)(slot + q);
+            *scalar_slot(S, kinds[k]) = s;
         }
     }
     peer_signal(pp);
@@ -861,9 +922,9 @@ __global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const double *__restr
 // a2: u += α p; r −= α q; ‖r‖² with α = ρ/pᵀq from the (all-reduced) device scalars
 __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *__restrict__ p,
                                                         const double *__restrict__ q, double *__restrict__ u,
-                                                        double *__restrict__ r, DotCtx dc) {
+                                                        double *__restrict__ r, DotCtx dc, int flex) {
     peer_wait(dc.pp);
-    const double alpha = dc.S->rz / dc.S->pq;
+    const double alpha = (flex ? dc.S->pr : dc.S->rz) / dc.S->pq;  // FCG: pᵀr / pᵀq; CG: ρ / pᵀq
     double s = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         u[i] = u[i] + alpha * p[i];
@@ -875,11 +936,13 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *
     peer_signal(dc.pp);
 }
 
-// a11: p = z + β p with β = ρ/ρ_prev  (first iteration: p = z)
+// a11: p = z + β p  (first iteration: p = z)
 __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__restrict__ z, double *__restrict__ p,
-                                                      const Scalars *__restrict__ S, int first, Push push, P2P pp) {
+                                                      const Scalars *__restrict__ S, int first, int flex, Push push,
+                                                      P2P pp) {
     peer_wait(pp);
-    const double beta = first ? 0.0 : S->rz / S->rz_prev;
+    // CG: β = ρ/ρ_prev; FCG(1): β = −zᵀq_prev / pᵀq_prev (S->pq still holds the previous iteration's)
+    const double beta = first ? 0.0 : flex ? -S->zq / S->pq : S->rz / S->rz_prev;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double v = first ? z[i] : z[i] + beta * p[i];
         p[i] = v;
@@ -955,6 +1018,100 @@ __global__ void __launch_bounds__(1024) k_coarse_solve(int n, const int64_t *__r
         xb = tmp;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xa[i];
+    peer_signal(pp);
+}
+
+// Deterministic CTA-wide sum (fixed shuffle tree + fixed warp order); every thread gets the result.
+__device__ __forceinline__ double cta_sum(double v, double *red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();  // red is reused
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < nw; w++) s += red[w];
+    return s;
+}
+
+// a7, §5.1 variant: the coarsest level solved by CG preconditioned by one weighted-Jacobi
+// sweep (z = D⁻¹ r with D = diag(K_L); the weight does not change CG) from x = 0 until
+// ‖r‖₂ <= tol·‖b‖₂ or maxit iterations, in ONE CTA: the operator (when it fits), x, r, z, p, q and
+// D in shared memory, warp-per-row products, deterministic CTA reductions.
+__global__ void __launch_bounds__(1024) k_coarse_cg(int n, const int64_t *__restrict__ rp, const int *__restrict__ ci,
+                                                     const double *__restrict__ v, const double *__restrict__ diag,
+                                                     const double *__restrict__ b, double *__restrict__ x, double tol,
+                                                     int maxit, int staged, P2P pp) {
+    peer_wait(pp);
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    double *sx = sm, *sr = sm + n, *sz = sm + 2 * n, *sp = sm + 3 * n, *sq = sm + 4 * n, *sd = sm + 5 * n;
+    const int nnz = (int)rp[n];
+    double *sv = sm + 6 * n;
+    int *sc = reinterpret_cast<int *>(sv + (staged ? nnz : 0));
+    int *srp = sc + (staged ? nnz : 0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sx[i] = 0.0;
+        sr[i] = b[i];
+        sd[i] = diag[i];
+    }
+    if (staged) {
+        for (int k = threadIdx.x; k < nnz; k += blockDim.x) {
+            sv[k] = v[k];
+            sc[k] = ci[k];
+        }
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) srp[i] = (int)rp[i];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double loc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) loc += sr[i] * sr[i];
+    const double bn = sqrt(cta_sum(loc, red));
+    if (bn > 0.0) {
+        loc = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            sz[i] = sr[i] / sd[i];
+            sp[i] = sz[i];
+            loc += sr[i] * sz[i];
+        }
+        double rz = cta_sum(loc, red);
+        for (int it = 0; it < maxit; it++) {
+            for (int i = wid; i < n; i += nw) {  // q = K p
+                double t = 0.0;
+                if (staged) {
+                    for (int k = srp[i] + lane; k < srp[i + 1]; k += 32) t = fma(sv[k], sp[sc[k]], t);
+                } else {
+                    for (int64_t k = rp[i] + lane; k < rp[i + 1]; k += 32) t = fma(v[k], sp[ci[k]], t);
+                }
+                t = warp_sum(t);
+                if (lane == 0) sq[i] = t;
+            }
+            __syncthreads();
+            loc = 0.0;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) loc += sp[i] * sq[i];
+            const double pq = cta_sum(loc, red);
+            if (!(pq > 0.0)) break;
+            const double alpha = rz / pq;
+            loc = 0.0;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                sx[i] = sx[i] + alpha * sp[i];
+                sr[i] = sr[i] - alpha * sq[i];
+                loc += sr[i] * sr[i];
+            }
+            if (sqrt(cta_sum(loc, red)) <= tol * bn) break;
+            loc = 0.0;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                sz[i] = sr[i] / sd[i];
+                loc += sr[i] * sz[i];
+            }
+            const double rz_new = cta_sum(loc, red);
+            const double beta = rz_new / rz;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) sp[i] = sz[i] + beta * sp[i];
+            rz = rz_new;
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = sx[i];
     peer_signal(pp);
 }
 

@@ -226,3 +226,58 @@ def test_c3_full_size_properties(fmt):
     assert st == 0 and 5 <= it <= 40
     ud = u.cpu().numpy()
     assert np.linalg.norm(F - oracle.spmv(Ks, ud)) <= 1.05e-6 * np.linalg.norm(F)
+
+
+# --- NEXT-1: the paper's own cube experiment --------------------
+def test_coarse_cg_vcycle_matches_oracle():
+    """§5.1 coarsest solver (CG with one weighted-Jacobi sweep as preconditioner) inside the V-cycle:
+    with tolerance 0 and 30 iterations both sides reach the coarse solution to round-off."""
+    amg = _amg()
+    dim, p, n = CASES["cube12p3"]
+    K, F = amg.iga_poisson(dim, p, n)
+    H = amg.Hierarchy(K, amg.params(p, coarse_solver=1, coarse_tol=0.0, coarse_maxit=30))
+    Ho = oracle.setup(K.to_scipy(), oracle.OParams.for_degree(p, coarse_solver=1, coarse_tol=0.0, coarse_maxit=30))
+    for seed in (3, 4):
+        r = amg_inputs.uniform_pm1(K.shape[0], seed=seed)
+        z = H.vcycle(dev(r)).cpu().numpy()
+        zo = oracle.vcycle(Ho, r)
+        assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
+
+
+@pytest.mark.parametrize("case", ["cube12p3", "cube10p4"])
+def test_fcg_matches_oracle(case):
+    """Notay FCG(1) outer solver with the linear V-cycle: same iterate after the oracle's iteration
+    count (1e-10) and iteration counts within ±1."""
+    amg = _amg()
+    dim, p, n = CASES[case]
+    K, F = amg.iga_poisson(dim, p, n)
+    H = amg.Hierarchy(K, amg.params(p, krylov=1))
+    Ho = oracle.setup(K.to_scipy(), oracle.OParams.for_degree(p))
+    for rhs in (F, amg_inputs.uniform_pm1(K.shape[0])):
+        uo, ito, rro, histo, rco = oracle.fcg(Ho, rhs, rtol=1e-6, maxit=200)
+        u, it, rr, hist, st = H.solve(dev(rhs), rtol=1e-6, maxit=200)
+        assert rco == 0 and st == 0 and abs(it - ito) <= 1
+        u2 = H.solve(dev(rhs), rtol=0.0, maxit=ito)[0].cpu().numpy()
+        assert np.linalg.norm(u2 - uo) <= 1e-10 * np.linalg.norm(uo)
+
+
+@pytest.mark.parametrize("p,n", [(3, 12), (4, 8), (5, 6), (6, 6)])
+def test_paper_cube_experiment(p, n):
+    """The paper's configuration end to end: its data (rhs = 2), FCG outer, §5.1 coarse CG (1e-4 /
+    30 its), Chebyshev degree by p.  Iteration counts within ±1 of the oracle's, true
+    residual ≤ 1e-6, and the discrete solution within the discretisation error of u = e^{x+z} sin y."""
+    from oracle import cube_paper
+    amg = _amg()
+    K, F = amg.iga_poisson(3, p, n, rhs=2)
+    Fo, uD = cube_paper.paper_cube_rhs(p, n)
+    H = amg.Hierarchy(K, amg.params(p, krylov=1, coarse_solver=1))
+    Ho = oracle.setup(K.to_scipy(), oracle.OParams.for_degree(p, coarse_solver=1))
+    uo, ito, rro, histo, rco = oracle.fcg(Ho, F, rtol=1e-6, maxit=200)
+    u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6, maxit=200)
+    assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
+    ud = u.cpu().numpy()
+    Ks = K.to_scipy()
+    assert np.linalg.norm(F - oracle.spmv(Ks, ud)) <= 1.05e-6 * np.linalg.norm(F)
+    err = cube_paper.l2_error_full(p, n, ud, uD)
+    exact = cube_paper.l2_error_full(p, n, np.zeros_like(ud), np.zeros_like(uD))  # ‖u‖_L2
+    assert err <= 1e-3 * exact

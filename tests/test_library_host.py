@@ -124,3 +124,28 @@ def test_setup_independent_of_thread_count(threads):
     for l in range(ref.info()["levels"]):
         a, b = ref.export(l), H.export(l)
         assert _bitwise(a["K"].to_scipy(), b["K"].to_scipy())
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 4), (3, 12), (5, 6), (6, 6)])
+def test_paper_cube_load_matches_oracle(p, n):
+    """rhs = 2 (the paper's own cube data): library F (binary128 moments, CG boundary
+    projection) vs the oracle's separable route (fp64 moments, sparse direct projection)."""
+    from oracle import cube_paper
+    K, F = amg.iga_poisson(3, p, n, rhs=2)
+    Fo, _ = cube_paper.paper_cube_rhs(p, n)
+    assert np.abs(F - Fo).max() <= 1e-13 * np.abs(Fo).max()
+
+
+def test_paper_cube_load_rejects_other_geometries():
+    with pytest.raises(amg.AmgError):
+        amg.iga_poisson(2, 2, 8, rhs=2)
+
+
+def test_no_undefined_internal_symbols():
+    """Every kernel launcher the runtime uses is instantiated in the library (a missing explicit
+    instantiation would only fail at load time on the GPU box)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--undefined-only", _lib.LIB_PATH if hasattr(_lib, "LIB_PATH") else
+                          os.path.join(ROOT, "paper_2511_21268_b200", "libamg_b200.so")],
+                         capture_output=True, text=True).stdout
+    assert "amgb" not in out
