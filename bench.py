@@ -192,11 +192,12 @@ def run_gpu(args) -> None:
 
     wl = workload_desc(args.config, world)
     dim, p, n, m = wl["dim"], wl["p"], wl["n"], wl["m"]
+    paper = args.problem == "paper" and dim == 3
     t0 = time.perf_counter()
-    K, F = amg.iga_poisson(dim, p, n)
+    K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    prm = amg.params(p, format=args.format)
+    prm = amg.params(p, format=args.format, krylov=1 if paper else 0, coarse_solver=1 if paper else 0)
     if world > 1:
         # every rank builds the same global hierarchy; host threads are shared by the ranks
         prm.num_threads = max(1, (os.cpu_count() or world) // world)
@@ -307,12 +308,18 @@ def run_gpu(args) -> None:
             "scaling": wl["scaling"],
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (generated IgA Poisson system, manufactured-solution RHS)",
+            "data": ("synthetic: generated IgA system with the paper's own cube data (f = −e^{x+z} sin y, "
+                     "projected Dirichlet + Neumann loads)" if paper else
+                     "synthetic (generated IgA Poisson system, manufactured-solution RHS)"),
             "config": {
                 "workload": f"{args.config}: {dim}-D Poisson, B-spline p={p}, n={n} elements/dir, "
-                            f"{N} free DOFs, AMG-PCG rtol {args.rtol}",
+                            f"{N} free DOFs, " + ("the paper's cube experiment (its data, FCG, §5.1 coarse CG)"
+                                                  if paper else "manufactured sine RHS, PCG") + f", rtol {args.rtol}",
+                "problem": args.problem,
                 "dofs": N, "nnz_K0": info["nnz"][0], "levels": info["levels"], "level_N": info["N"],
-                "opc": round(info["opc"], 4), "cheb_degree": m, "coarse_sweeps": 30, "format": args.format,
+                "opc": round(info["opc"], 4), "cheb_degree": m,
+                "coarse_solver": "CG + one weighted-Jacobi sweep, 1e-4 / 30 its" if paper else "30 ℓ1-Jacobi sweeps",
+                "krylov": "FCG(1)" if paper else "PCG", "format": args.format,
                 "level_kernels": op_cfg,
                 "cuda_graphs": os.environ.get("AMG_GRAPHS", "1") != "0",
                 "parallelism": (f"row-block x{world}, replicated coarse levels, "
@@ -407,7 +414,8 @@ def run_reference(args) -> None:
     with open(path) as f:
         info = json.load(f)
     K = _oracle_sample(args.config)
-    iters = int(info.get("oracle_iters", args.ref_iters))
+    key = "oracle_iters_paper" if args.problem == "paper" and wl["dim"] == 3 else "oracle_iters"
+    iters = int(info.get(key, info.get("oracle_iters", args.ref_iters)))
     vals = []
     for i in range(args.warmup + args.steps):
         r = cpu_baseline(args.config, iters, info, wl["m"], reps=1, K=K)
@@ -438,6 +446,10 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=15, help="iteration count the reference arm scales to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--format", type=int, default=0, help="0 auto, 1 CSR2, 2 SELL2")
+    ap.add_argument("--problem", default="paper", choices=["paper", "manufactured"],
+                    help="paper: the paper's own cube experiment (P:L1061-1072: its data with the L2-projected "
+                         "Dirichlet and Neumann loads, FCG outer solver P:L1107, §5.1 coarse CG P:L1114); "
+                         "manufactured: homogeneous-data sine solution, PCG, 30 ℓ1-Jacobi coarse sweeps")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -26,7 +26,7 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, case, rep_nnz, transport, q):
+def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -37,8 +37,10 @@ def _worker(rank, world, port, case, rep_nnz, transport, q):
         import paper_2511_21268_b200 as amg
         import amg_inputs
         dim, p, n = case
-        K, F = amg.iga_poisson(dim, p, n)
-        H = amg.Hierarchy(K, amg.params(p), dist=amg.make_dist(rank, world, device=rank))
+        paper = solver == "fcg"  # the paper's own experiment: its data, FCG, §5.1 coarse CG
+        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
+        kw = dict(krylov=1, coarse_solver=1) if paper else {}
+        H = amg.Hierarchy(K, amg.params(p, **kw), dist=amg.make_dist(rank, world, device=rank))
         b, e = H.local_rows()
         out = {}
         # one V-cycle on a random residual: every rank's slice of the distributed output
@@ -56,7 +58,7 @@ def _worker(rank, world, port, case, rep_nnz, transport, q):
             out[name] = (it, st, hist, parts)
         if rank == 0:
             ref = {}
-            H1 = amg.Hierarchy(K, amg.params(p))
+            H1 = amg.Hierarchy(K, amg.params(p, **kw))
             ref["vcycle"] = H1.vcycle(torch.from_numpy(amg_inputs.uniform_pm1(K.shape[0], seed=17)).cuda()).cpu().numpy()
             for name, rhs in (("sine", F), ("random", amg_inputs.uniform_pm1(K.shape[0]))):
                 Fd = torch.from_numpy(rhs).cuda()
@@ -106,7 +108,34 @@ def test_distributed_solve_matches_single_gpu(world, case, rep_nnz, transport):
         for b, e, ul, ul8 in parts:
             u[b:e] = ul
             u8[b:e] = ul8
-        assert np.linalg.norm(u8 - u1_8) <= 1e-10 * np.linalg.norm(u1_8)
+        # the §5.1 coarse CG stops on a tolerance: round-off in the outer dots may move its stop by an
+        # iteration, so the FCG runs are compared at the level of that tolerance
+        tol = 1e-10 if solver == "pcg" else 1e-6
+        assert np.linalg.norm(u8 - u1_8) <= tol * np.linalg.norm(u1_8)
         if it == it1:
-            assert np.linalg.norm(u - u1) <= 1e-10 * np.linalg.norm(u1)
-        assert np.allclose(hist[: min(len(hist), len(hist1))], hist1[: min(len(hist), len(hist1))], rtol=1e-8)
+            assert np.linalg.norm(u - u1) <= tol * np.linalg.norm(u1)
+        assert np.allclose(hist[: min(len(hist), len(hist1))], hist1[: min(len(hist), len(hist1))],
+                           rtol=1e-8 if solver == "pcg" else 1e-4)
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_distributed_paper_experiment(transport):
+    """The paper's configuration (its cube data, FCG outer, §5.1 coarse CG on the replicated coarsest
+    level) at 2 GPUs vs 1 GPU."""
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (3, 3, 12), 100000, transport, q, "fcg"))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, out, ref, N = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert status == "ok", out
+    it, st, hist, parts = out["sine"]
+    it1 = ref["sine"][0]
+    assert st == 0 and abs(it - it1) <= 1
