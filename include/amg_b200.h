@@ -218,6 +218,12 @@ amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_confi
  * AMG_EINVAL for a bad level/op or an unavailable configuration. */
 amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);
 
+/* Per-level time breakdown of the V-cycles run since the last call (experiments): exclusive device
+ * milliseconds per V-cycle of every level — its smoothing, residual, transfers and halo / lock-step
+ * waits, without the coarser levels.  Recorded only for hierarchies created with the environment
+ * AMG_PROF_LEVELS=1 and AMG_GRAPHS=0 (else zeros).  Resets the accumulation.  nlevels: the level count. */
+amg_status amg_get_level_times(amg_hierarchy *H, double *ms_per_vcycle, int nmax, int *nlevels);
+
 /* Host view of this rank's share of operator op (0 K_l, 1 P̄_l, 2 R_l) on level l, for hierarchies
  * set up with an amg_dist of nranks > 1 (host_only or not).  Local column indices keep the global
  * order: ghost[0..n_ghost-1] holds the ghost columns' global ids ascending, the first n_ghost_lo of them

@@ -293,6 +293,13 @@ class Hierarchy:
     def set_op_config(self, level: int, op: int, kernel: int, G: int, U: int) -> None:
         check(lib().amg_operator_set_config(self._h, level, op, kernel, G, U))
 
+    def level_times(self) -> list:
+        """Exclusive ms per V-cycle of every level (AMG_PROF_LEVELS=1, AMG_GRAPHS=0); resets."""
+        buf = (C.c_double * 32)()
+        nl = C.c_int()
+        check(lib().amg_get_level_times(self._h, buf, 32, C.byref(nl)))
+        return list(buf[: nl.value])
+
     def kernel_stats(self) -> dict:
         s = _lib.amg_kernel_stats()
         check(lib().amg_get_kernel_stats(self._h, C.byref(s)))

@@ -21,7 +21,7 @@ STATUS = {0: "AMG_OK", 1: "AMG_NOT_CONVERGED", -1: "AMG_EINVAL", -2: "AMG_ENOMEM
 EXPORTED = ["amg_iga_poisson", "amg_iga_tables", "amg_csr_free", "amg_free", "amg_params_default",
             "amg_set_allocator", "amg_setup", "amg_pcg_solve", "amg_pcg_solve_host", "amg_vcycle",
             "amg_level_apply", "amg_hierarchy_info", "amg_hierarchy_export", "amg_set_profiling",
-            "amg_get_kernel_stats", "amg_operator_config", "amg_operator_set_config", "amg_nccl_unique_id", "amg_local_rows",
+            "amg_get_kernel_stats", "amg_operator_config", "amg_operator_set_config", "amg_get_level_times", "amg_nccl_unique_id", "amg_local_rows",
             "amg_dist_view_get", "amg_hierarchy_free", "amg_last_error"]
 
 
@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
         "amg_get_kernel_stats": ([vp, P(amg_kernel_stats)], C.c_int),
         "amg_operator_config": ([vp, C.c_int, C.c_int, P(amg_op_config)], C.c_int),
         "amg_operator_set_config": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
+        "amg_get_level_times": ([vp, P(C.c_double), C.c_int, P(C.c_int)], C.c_int),
         "amg_nccl_unique_id": ([P(C.c_ubyte)], C.c_int),
         "amg_local_rows": ([vp, P(C.c_int64), P(C.c_int64)], C.c_int),
         "amg_dist_view_get": ([vp, C.c_int, C.c_int, P(amg_dist_view)], C.c_int),

@@ -363,6 +363,43 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
     tune_store(key, A);
 }
 
+// Per-level breakdown mark (no-op unless D.lvl_prof).
+void level_mark(DevState &D, int l, int kind, cudaStream_t st) {
+    if (!D.lvl_prof) return;
+    if (D.lev_ev_used >= D.lev_ev.size()) {
+        for (int k = 0; k < 256; k++) {
+            cudaEvent_t e;
+            CUDA_OK(cudaEventCreate(&e));
+            D.lev_ev.push_back(e);
+        }
+    }
+    CUDA_OK(cudaEventRecord(D.lev_ev[D.lev_ev_used++], st));
+    D.lev_marks.push_back({l, kind});
+}
+
+// Fold the recorded marks into exclusive per-level times (after the stream has completed).
+void level_collect(DevState &D) {
+    if (!D.lvl_prof || D.lev_ev_used == 0) return;
+    // exclusive(l) = (exit − enter) − (child end − child start)
+    std::vector<size_t> enter(32), cstart(32);
+    for (size_t k = 0; k < D.lev_ev_used; k++) {
+        const int l = D.lev_marks[k].first, kind = D.lev_marks[k].second;
+        float ms = 0.f;
+        if (kind == 0) enter[l] = k;
+        else if (kind == 1) cstart[l] = k;
+        else if (kind == 2) {
+            CUDA_OK(cudaEventElapsedTime(&ms, D.lev_ev[cstart[l]], D.lev_ev[k]));
+            D.lvl_ms[l] -= ms;
+        } else {
+            CUDA_OK(cudaEventElapsedTime(&ms, D.lev_ev[enter[l]], D.lev_ev[k]));
+            D.lvl_ms[l] += ms;
+            if (l == 0) D.lvl_vcycles++;
+        }
+    }
+    D.lev_ev_used = 0;
+    D.lev_marks.clear();
+}
+
 // Profiling: events around the dominant kernel (level-0 fused Chebyshev step).
 struct ProfScope {
     DevState &D;
@@ -442,8 +479,16 @@ const double kC0 = 4.0 / 3.0;
 // (this rank's rows).  Ghost values reach the gathering kernels either by halo() (NCCL) right before
 // them, or (P2P) by the producing epilogues' pushes (push_of: d_new/d0 along K_l's plan, r along R_l's,
 // x after prolongation along K_l's, the final x of a coarse level along P̄_{l-1}'s).
+void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot,
+                       const double *final_bdot);
 void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot,
                   const double *final_bdot = nullptr) {
+    level_mark(D, l, 0, st);
+    vcycle_level_body(D, l, b, x, st, final_dot, final_bdot);
+    level_mark(D, l, 3, st);
+}
+void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStream_t st, int final_dot,
+                       const double *final_bdot) {
     DLevel &L = D.lev[l];
     const int m = D.m;
     // the first replicated level waits (P2P) for every rank's share of its right-hand side
@@ -565,7 +610,9 @@ void vcycle_level(DevState &D, int l, const double *b, double *x, cudaStream_t s
         e.pushD = push_of(D, C.K, C.d[0]);
         launch_csr(D, L.R, L.r, e, st);
     }
+    level_mark(D, l, 1, st);
     vcycle_level(D, l + 1, C.b, C.x, st, dev::DOT_NONE);
+    level_mark(D, l, 2, st);
     // prolongation x += P̄ x_c
     {
         halo(D, L.P, C.x, st);
@@ -919,6 +966,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         D->coarse_tol = H.prm.coarse_tol;
         D->coarse_maxit = H.prm.coarse_maxit;
         if (const char *e = std::getenv("AMG_GRAPHS")) D->graphs = std::atoi(e) != 0;
+        if (const char *e = std::getenv("AMG_PROF_LEVELS")) D->lvl_prof = std::atoi(e) != 0 && !D->graphs;
         const int nr = dist ? dist->nranks : 1;
         D->rank = dist ? dist->rank : 0;
         D->nranks = nr;
@@ -1177,6 +1225,7 @@ static void run_segment(DevState &D, int kind, double *u, cudaStream_t st) {
         enqueue_segment(D, kind, u, st);
         CUDA_OK(cudaStreamSynchronize(st));
         prof_collect(D);
+        level_collect(D);
         return;
     }
     DevState::Seg &S = D.seg[kind];
@@ -1425,6 +1474,21 @@ extern "C" amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *s
     st->total_ms = D->prof_ms;
     st->bytes_per_launch = D->bytes_dominant;
     st->kernels_launched = D->launches_total;
+    return AMG_OK;
+    API_END
+}
+
+extern "C" amg_status amg_get_level_times(amg_hierarchy *H, double *ms_per_vcycle, int nmax, int *nlevels) {
+    API_BEGIN
+    DevState *D = need_dev(H);
+    if (!ms_per_vcycle || !nlevels || nmax < 1) throw Error{AMG_EINVAL, "bad argument"};
+    CUDA_OK(cudaDeviceSynchronize());
+    level_collect(*D);
+    *nlevels = D->nlevels;
+    for (int l = 0; l < std::min(nmax, D->nlevels); l++)
+        ms_per_vcycle[l] = D->lvl_vcycles ? D->lvl_ms[l] / (double)D->lvl_vcycles : 0.0;
+    for (int l = 0; l < 32; l++) D->lvl_ms[l] = 0.0;
+    D->lvl_vcycles = 0;
     return AMG_OK;
     API_END
 }

@@ -133,6 +133,14 @@ struct DevState {
     double bytes_dominant = 0.0;
     double prof_ms = 0.0;
     int64_t prof_n = 0;
+    // per-level time breakdown (env AMG_PROF_LEVELS=1 with AMG_GRAPHS=0): events at the entry / exit of
+    // every level of the V-cycle and around its recursion; exclusive ms per level accumulated
+    bool lvl_prof = false;
+    std::vector<cudaEvent_t> lev_ev;
+    size_t lev_ev_used = 0;
+    std::vector<std::pair<int, int>> lev_marks;  // (level, kind) per event: 0 enter, 1 child start, 2 child end, 3 exit
+    double lvl_ms[32] = {0};
+    int64_t lvl_vcycles = 0;
     // CUDA graphs of the PCG iteration (kind 0: first iteration, 1: later iterations)
     bool graphs = true;
     cudaStream_t cap = nullptr;
