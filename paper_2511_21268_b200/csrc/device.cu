@@ -739,7 +739,8 @@ std::vector<int64_t> nccl_allgather_i64(DevState &D, const std::vector<int64_t> 
 }
 
 // Slab layout (identical on every rank): flags, epoch, ticket, dot slots, then the vectors.
-constexpr size_t kFlagsOff = 0, kEpochOff = 512, kTicketOff = 576, kDslotOff = 1024, kVecOff = 4096;
+constexpr size_t kFlagsOff = 0, kEpochOff = 512, kTicketOff = 576, kBTicketOff = 640, kDslotOff = 1024,
+                 kVecOff = 4096;
 
 // Push plan of operator A's gathered vector: for each owned index j, the (rank, slot) pairs of the
 // other ranks' ghost copies.  meta_of(q) = {lo_base, hi_base, nlo, recv_off[0..nranks)} of rank q's
@@ -774,21 +775,21 @@ void build_push(DevState &D, const LocalOp &op, DCsr &A, const std::vector<int64
     CUDA_OK(cudaMemcpy(A.push_dst, dst.data(), sizeof(int2) * dst.size(), cudaMemcpyHostToDevice));
 }
 
-// Row-group order of a CSR operator for its current G: interior groups (no boundary row) first.
+// Row-group order of a CSR operator for its current G: boundary groups (any row reading a ghost value
+// or pushed somewhere) first, then the interior ones.
 void build_gorder(DevState &D, DCsr &A) {
     if (A.bnd.empty() || A.fmt != 0) return;
     if (const char *e = std::getenv("AMG_P2P_INTERIOR"))  // 0: every kernel waits at its start (debug)
         if (std::atoi(e) == 0) return;
     const int64_t G = A.G, ng = (A.nrows + G - 1) / G;
-    std::vector<int> order;
+    std::vector<int> order, tail;
     order.reserve(ng);
-    std::vector<int> tail;
     for (int64_t g = 0; g < ng; g++) {
         bool b = false;
         for (int64_t i = g * G; i < std::min(A.nrows, (g + 1) * G) && !b; i++) b = A.bnd[i] != 0;
-        (b ? tail : order).push_back((int)g);
+        (b ? order : tail).push_back((int)g);
     }
-    A.nint = (int64_t)order.size();
+    A.nbnd = (int64_t)order.size();
     order.insert(order.end(), tail.begin(), tail.end());
     if (!A.gorder || A.gorder_cap < ng) {
         A.gorder = D.alloc_n<int>(ng);
@@ -928,6 +929,7 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
     D.pp.flags = reinterpret_cast<unsigned long long *>(D.slab + kFlagsOff);
     D.pp.epoch = reinterpret_cast<unsigned long long *>(D.slab + kEpochOff);
     D.pp.ticket = reinterpret_cast<unsigned *>(D.slab + kTicketOff);
+    D.pp.bticket = reinterpret_cast<unsigned *>(D.slab + kBTicketOff);
     D.pp.flags_off = (long long)kFlagsOff;
     D.pp.dslot_off = (long long)kDslotOff;
     D.pp.wait_mask = ~0u;

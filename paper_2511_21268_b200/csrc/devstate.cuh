@@ -70,8 +70,8 @@ struct DCsr {
     int2 *push_dst = nullptr;
     std::vector<char> pushed;   // host: owned index i has a push destination
     std::vector<char> bnd;      // host: row i touches a ghost value or is pushed (P2P boundary row)
-    int *gorder = nullptr;      // device: row groups (of the current G) interior-first
-    int64_t nint = 0, gorder_G = 0, gorder_cap = 0;
+    int *gorder = nullptr;      // device: row groups (of the current G) boundary-first
+    int64_t nbnd = 0, gorder_G = 0, gorder_cap = 0;
     int *sidx = nullptr;     // device: local owned indices to send, by destination rank
     double *sbuf = nullptr;  // device: packed send buffer
     std::vector<int> hs_count, hs_off, hr_count, hr_off;  // halo send/recv counts and offsets per rank
@@ -171,7 +171,7 @@ inline dev::P2P p2p_of(const DevState &D, const DCsr &A) {
     dev::P2P p = p2p_of(D, A.part, A.wmask);
     if (p.nranks > 0 && A.fmt == 0 && A.gorder && A.gorder_G == A.G) {
         p.gorder = A.gorder;
-        p.nint = A.nint;
+        p.nbnd = A.nbnd;
     }
     return p;
 }

@@ -76,11 +76,14 @@ struct P2P {
     long long flags_off;         // byte offset of flags[] in every slab
     long long dslot_off;         // byte offset of the dot slots dslot[kind][rank] in every slab
     unsigned wait_mask;          // ranks this kernel reads from or writes to (bit q): the ones it waits for
-    // CSR cores: row groups in the order interior-first.  Groups at positions < nint touch no ghost value
-    // and push nothing, so they run WITHOUT waiting; each warp waits once, before its first boundary
-    // group (gorder == nullptr: wait at the kernel start).
+    // CSR cores: row groups in the order BOUNDARY-FIRST.  Boundary groups (positions < nbnd) read ghost
+    // values or push theirs: each warp waits before its first one.  When every warp of the grid is past
+    // its boundary groups the kernel publishes its count (warp ticket `bticket`), EARLY: the interior
+    // groups that follow read only owned values and push nothing, so the neighbours' next kernel does
+    // not wait for them.  gorder == nullptr: wait at the kernel start, publish at its end.
     const int *gorder;
-    long long nint;
+    long long nbnd;
+    unsigned *bticket;           // own slab: warp ticket of the early publication (zero between launches)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -129,9 +132,30 @@ __device__ __forceinline__ void peer_wait_warp(const P2P &pp) {
     __syncwarp();
 }
 
+// Early publication of the boundary-first CSR cores: each warp calls it once, after its last boundary
+// group (all its pushes issued); the last warp of the grid publishes the new count.
+__device__ __forceinline__ void peer_signal_warp(const P2P &pp) {
+    if (pp.nranks == 0) return;
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence_system();
+        const unsigned total = gridDim.x * (blockDim.x >> 5);
+        const unsigned t = atomicAdd(pp.bticket, 1u);
+        if (t == total - 1) {
+            __threadfence_system();
+            const unsigned long long e = *(volatile unsigned long long *)pp.epoch + 1ull;
+            *(volatile unsigned long long *)pp.epoch = e;
+            *(volatile unsigned *)pp.bticket = 0u;
+            for (int q = 0; q < pp.nranks; q++)
+                st_release_sys(reinterpret_cast<unsigned long long *>(pp.base[q] + pp.flags_off) + pp.rank, e);
+        }
+    }
+    __syncwarp();
+}
+
 // Kernel epilogue (every CTA, after all its stores): the last CTA to finish publishes the new count.
 __device__ __forceinline__ void peer_signal(const P2P &pp) {
-    if (pp.nranks == 0) return;
+    if (pp.nranks == 0 || pp.gorder) return;  // boundary-first kernels published early
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
@@ -528,11 +552,12 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
     const int64_t ngroups = (nrows + G - 1) / G;
     const uint64_t pol = stream_policy();
     typename Epi::Acc dacc{};
-    bool waited = pp.gorder == nullptr;
+    bool signalled = pp.gorder == nullptr || pp.nranks == 0;
+    if (!signalled && warp < pp.nbnd) peer_wait_warp(pp);  // this warp has boundary groups
     for (int64_t pos = warp; pos < ngroups; pos += nwarps) {
-        if (!waited && pos >= pp.nint) {
-            peer_wait_warp(pp);
-            waited = true;
+        if (!signalled && pos >= pp.nbnd) {  // past this warp's boundary groups
+            peer_signal_warp(pp);
+            signalled = true;
         }
         const int64_t grp = pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos;
         const int64_t r0 = grp * G;
@@ -594,6 +619,7 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
         }
         if (lane < nr) acc_add(dacc, epi(r0 + lane, mine, pre));
     }
+    if (!signalled) peer_signal_warp(pp);  // only boundary groups (or none) for this warp
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
     peer_signal(pp);
 }
@@ -742,13 +768,14 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         issue(ahead, k);
     }
     int s = 0;
-    bool waited = pp.gorder == nullptr;
+    bool signalled = pp.gorder == nullptr || pp.nranks == 0;
+    if (!signalled && warp < pp.nbnd) peer_wait_warp(pp);  // this warp has boundary groups
     while (cur.valid) {
         advance(ahead);
         issue(ahead, (s + NS - 1) % NS);
-        if (!waited && cur.pos >= pp.nint) {  // first boundary group of this warp
-            peer_wait_warp(pp);
-            waited = true;
+        if (!signalled && cur.pos >= pp.nbnd) {  // past this warp's boundary groups
+            peer_signal_warp(pp);
+            signalled = true;
         }
         if (cur.gfirst && lane < cur.nr) pre = epi.load(cur.grp * G + lane);
         const int rs = cols.row(cur.grp * G + cur.t);
@@ -790,6 +817,7 @@ __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ r
         advance(cur);
         s = (s + 1) % NS;
     }
+    if (!signalled) peer_signal_warp(pp);
     if constexpr (Epi::kDot) block_dot_finalize_n<kBlockT>(dacc, dc);
     peer_signal(pp);
 }

@@ -81,6 +81,7 @@ def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg"):
 def test_distributed_solve_matches_single_gpu(world, case, rep_nnz, transport):
     """transport p2p: ghost values pushed from the producing kernels' epilogues into peer memory and a
     cross-GPU kernel lock-step (no NCCL in the solve); nccl: NCCL send/recv halos and all-reduces."""
+    solver = "pcg"
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     ctx = mp.get_context("spawn")
