@@ -16,6 +16,7 @@ C2     3    2    32    single-B200 full hierarchy, parity at full size
 C3     3    3    96    the paper's GPU cube case (Table 1b k=96: 941,094 DOFs)
 C4     3    4    128   high-degree bandwidth stress
 C5     3    2    250+  weak scaling, ~16M DOFs per GPU (n = 250/315/398/502)
+R3     3    3    96    thick quarter ring (NEXT-3, Table 3), random RHS
 =====  ===  ===  ====  =====================================================
 """
 from __future__ import annotations
@@ -31,6 +32,8 @@ CONFIGS = {
     "C3": dict(dim=3, p=3, n=96),
     "C4": dict(dim=3, p=4, n=128),
     "C5": dict(dim=3, p=2, n=250),
+    # NEXT-3: the thick quarter ring, Table 3 k=96 p=3 (941,094 DOFs); seeded random RHS
+    "R3": dict(dim=3, p=3, n=96, geometry=1),
 }
 C5_WEAK_N = {1: 250, 2: 315, 4: 398, 8: 502}
 

@@ -192,9 +192,14 @@ def run_gpu(args) -> None:
 
     wl = workload_desc(args.config, world)
     dim, p, n, m = wl["dim"], wl["p"], wl["n"], wl["m"]
-    paper = args.problem == "paper" and dim == 3
+    geom = wl.get("geometry", 0)
+    paper = args.problem == "paper" and dim == 3 and geom == 0
     t0 = time.perf_counter()
-    K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
+    if geom == 1:  # quarter ring: seeded random right-hand side (its paper data is not generated)
+        K, _ = amg.iga_poisson(dim, p, n, rhs=1, geometry=1)
+        F = amg_inputs.uniform_pm1(K.shape[0], seed=amg_inputs.SEED)
+    else:
+        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     prm = amg.params(p, format=args.format, krylov=1 if paper else 0, coarse_solver=1 if paper else 0)
@@ -310,11 +315,13 @@ def run_gpu(args) -> None:
             "dtype": "f64",
             "data": ("synthetic: generated IgA system with the paper's own cube data (f = −e^{x+z} sin y, "
                      "projected Dirichlet + Neumann loads)" if paper else
+                     "synthetic: generated quarter-ring IgA system, seeded uniform(−1,1) RHS" if geom == 1 else
                      "synthetic (generated IgA Poisson system, manufactured-solution RHS)"),
             "config": {
-                "workload": f"{args.config}: {dim}-D Poisson, B-spline p={p}, n={n} elements/dir, "
-                            f"{N} free DOFs, " + ("the paper's cube experiment (its data, FCG, §5.1 coarse CG)"
-                                                  if paper else "manufactured sine RHS, PCG") + f", rtol {args.rtol}",
+                "workload": f"{args.config}: {dim}-D Poisson on the " + ("thick quarter ring" if geom == 1 else "cube")
+                            + f", B-spline p={p}, n={n} elements/dir, {N} free DOFs, "
+                            + ("the paper's cube experiment (its data, FCG, §5.1 coarse CG)" if paper else
+                               "random RHS, PCG" if geom == 1 else "manufactured sine RHS, PCG") + f", rtol {args.rtol}",
                 "problem": args.problem,
                 "dofs": N, "nnz_K0": info["nnz"][0], "levels": info["levels"], "level_N": info["N"],
                 "opc": round(info["opc"], 4), "cheb_degree": m,
@@ -375,6 +382,9 @@ def _oracle_sample(cfg: str):
     """Assemble the workload's K with the oracle (exact tables + plain C Kronecker sum)."""
     import oracle
     wl = workload_desc(cfg)
+    if wl.get("geometry", 0) == 1:
+        from oracle import ring
+        return ring.assemble_ring(wl["p"], wl["n"])
     return oracle.assemble(wl["dim"], wl["p"], wl["n"])
 
 

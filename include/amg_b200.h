@@ -67,6 +67,13 @@ typedef struct {
  * Outputs: *K (free with amg_csr_free) and *F (length K->n_rows, free with amg_free).
  * Errors: AMG_EINVAL for dim ∉ {2,3}, degree ∉ [1,8], n_elem < 1, sides out of range, or more
  * than 2^31-1 free DOFs; AMG_ENOMEM.
+ *
+ * geometry = 1: the thick quarter ring of the paper (dim 3 only): inner radius 1, outer
+ *          radius 2, height 1, exact NURBS circle, B-spline solution space (non-isoparametric, §3.3
+ *          P:L592-605).  x = (1+u)c_x(v), y = (1+u)c_y(v), z = w; sides 1: u=0, 2: u=1, 3: v=0 (y=0),
+ *          4: v=1 (x=0), 5: w=0, 6: w=1.  Since JᵀJ = diag(1, r²|c'|², 1), K = A_u⊗B_v⊗M_w +
+ *          C_u⊗D_v⊗M_w + E_u⊗B_v⊗K_w with r- and |c'|-weighted 1-D tables (binary128 Gauss, rounded
+ *          once), entry ((A·B)·M + (C·D)·M) + (E·B)·K.  Only rhs = 1 (F = 0) is defined for the ring.
  */
 typedef struct {
     int dim;
@@ -74,6 +81,7 @@ typedef struct {
     int n_elem;
     uint32_t dirichlet_sides;
     int rhs;
+    int geometry; /* 0 unit square / cube, 1 thick quarter ring (dim 3) */
 } amg_iga_desc;
 
 amg_status amg_iga_poisson(const amg_iga_desc *desc, amg_csr **K, double **F);

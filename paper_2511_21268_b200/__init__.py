@@ -46,9 +46,9 @@ def _from_c(ptr) -> HostCsr:
     return HostCsr(rp, ci, v, shape)
 
 
-def iga_poisson(dim: int, p: int, n: int, dirichlet_sides: int = 0b000111, rhs: int = 0):
-    """amg_iga_poisson: (K as HostCsr, F as numpy fp64)."""
-    d = _lib.amg_iga_desc(dim, p, n, dirichlet_sides, rhs)
+def iga_poisson(dim: int, p: int, n: int, dirichlet_sides: int = 0b000111, rhs: int = 0, geometry: int = 0):
+    """amg_iga_poisson: (K as HostCsr, F as numpy fp64).  geometry 1 = the thick quarter ring (dim 3)."""
+    d = _lib.amg_iga_desc(dim, p, n, dirichlet_sides, rhs, geometry)
     Kp = C.POINTER(_lib.amg_csr)()
     Fp = C.POINTER(C.c_double)()
     check(lib().amg_iga_poisson(C.byref(d), C.byref(Kp), C.byref(Fp)))

@@ -38,7 +38,7 @@ class amg_csr(C.Structure):
 
 class amg_iga_desc(C.Structure):
     _fields_ = [("dim", C.c_int), ("degree", C.c_int), ("n_elem", C.c_int), ("dirichlet_sides", C.c_uint32),
-                ("rhs", C.c_int)]
+                ("rhs", C.c_int), ("geometry", C.c_int)]
 
 
 class amg_params(C.Structure):

@@ -180,6 +180,65 @@ std::vector<double> load_factor(int ax, int p, int n) {
     return out;
 }
 
+// Thick quarter ring (geometry 1): the seven weighted 1-D tables of K = A_u⊗B_v⊗M_w + C_u⊗D_v⊗M_w +
+// E_u⊗B_v⊗K_w (amg_b200.h), on [0,1] with n elements, (p+1)-point Gauss per element in binary128,
+// rounded once; band storage m × (2p+1).  r(u) = 1+u; |c'(v)| of the rational quadratic quarter circle
+// with weights (1, √2/2, 1).
+struct RingTables {
+    std::vector<double> A, C, E, B, Dv, M, K;
+};
+
+q128 circle_speed(q128 v) {
+    const q128 w1 = sqrtq(2.0Q) / 2;
+    const q128 X = (1 - v) * (1 - v) + 2 * v * (1 - v) * w1;
+    const q128 Y = 2 * v * (1 - v) * w1 + v * v;
+    const q128 W = (1 - v) * (1 - v) + 2 * v * (1 - v) * w1 + v * v;
+    const q128 Xp = -2 * (1 - v) + 2 * w1 * (1 - 2 * v);
+    const q128 Yp = 2 * w1 * (1 - 2 * v) + 2 * v;
+    const q128 Wp = -2 * (1 - v) + 2 * w1 * (1 - 2 * v) + 2 * v;
+    const q128 cx = (Xp * W - X * Wp) / (W * W);
+    const q128 cy = (Yp * W - Y * Wp) / (W * W);
+    return sqrtq(cx * cx + cy * cy);
+}
+
+RingTables ring_tables(int p, int n) {
+    const int m = n + p, bw = 2 * p + 1;
+    const size_t sz = (size_t)m * bw;
+    std::vector<q128> tA(sz, 0), tC(sz, 0), tE(sz, 0), tB(sz, 0), tD(sz, 0), tM(sz, 0), tK(sz, 0);
+    std::vector<q128> gx, gw;
+    gauss_legendre_q(p + 1, gx, gw);
+    q128 val[16], der[16];
+    for (int e = 0; e < n; e++)
+        for (int q = 0; q <= p; q++) {
+            basis_and_derivs(e + p, e + gx[q], p, n, val, der);  // integer-knot basis: d/dt
+            const q128 x = (e + gx[q]) / n, w = gw[q] / n;
+            const q128 r = 1 + x, sp = circle_speed(x);
+            for (int i = 0; i <= p; i++)
+                for (int j = 0; j <= p; j++) {
+                    const size_t k = (size_t)(e + i) * bw + (j - i + p);
+                    const q128 nn = val[i] * val[j] * w;
+                    const q128 dd = der[i] * der[j] * n * n * w;  // d/du = n·d/dt
+                    tA[k] += dd * r;
+                    tC[k] += nn / r;
+                    tE[k] += nn * r;
+                    tB[k] += nn * sp;
+                    tD[k] += dd / sp;
+                    tM[k] += nn;
+                    tK[k] += dd;
+                }
+        }
+    RingTables T;
+    auto rnd = [&](const std::vector<q128> &t) {
+        q128 sc = 0;
+        for (auto v : t) sc = fmaxq(sc, fabsq(v));
+        std::vector<double> o(t.size());
+        for (size_t i = 0; i < t.size(); i++) o[i] = round_q(t[i], sc);
+        return o;
+    };
+    T.A = rnd(tA); T.C = rnd(tC); T.E = rnd(tE); T.B = rnd(tB); T.Dv = rnd(tD); T.M = rnd(tM); T.K = rnd(tK);
+    return T;
+}
+
 // 1-D moments ∫_0^1 g(t) N_a(t) dt of all m functions, (p+1)-point Gauss per element in binary128.
 template <class Fn>
 std::vector<double> moments(int p, int n, Fn g) {
@@ -321,6 +380,8 @@ void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
     if (N > INT32_MAX) throw Error{AMG_EINVAL, "more than 2^31-1 free DOFs (int32 columns)"};
     const Tables1D T = physical_tables(p, n);
     const double *M1 = T.M.data(), *K1 = T.K.data();
+    const bool ring = d.geometry == 1;
+    const RingTables RT = ring ? ring_tables(p, n) : RingTables{};
 
     // per-axis column window [l, h] of function x
     auto win = [&](int ax, int x, int &l, int &h) {
@@ -367,7 +428,14 @@ void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
                     const double Ma = M1[(size_t)a * bw + (a2 - a + p)];
                     const double Ka = K1[(size_t)a * bw + (a2 - a + p)];
                     double val;
-                    if (dim == 3) {
+                    if (ring) {  // ((A·B)·M + (C·D)·M) + (E·B)·K
+                        const size_t ka = (size_t)a * bw + (a2 - a + p), kb = (size_t)b * bw + (b2 - b + p),
+                                     kc = (size_t)c * bw + (c2 - c + p);
+                        const double t1 = (RT.A[ka] * RT.B[kb]) * RT.M[kc];
+                        const double t2 = (RT.C[ka] * RT.Dv[kb]) * RT.M[kc];
+                        const double t3 = (RT.E[ka] * RT.B[kb]) * RT.K[kc];
+                        val = (t1 + t2) + t3;
+                    } else if (dim == 3) {
                         const double t1 = (Ka * Mb) * Mc;
                         const double t2 = (Ma * Kb) * Mc;
                         const double t3 = (Ma * Mb) * Kc;

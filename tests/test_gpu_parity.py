@@ -281,3 +281,22 @@ def test_paper_cube_experiment(p, n):
     err = cube_paper.l2_error_full(p, n, ud, uD)
     exact = cube_paper.l2_error_full(p, n, np.zeros_like(ud), np.zeros_like(uD))  # ‖u‖_L2
     assert err <= 1e-3 * exact
+
+
+@pytest.mark.parametrize("p,n", [(2, 8), (3, 8)])
+def test_ring_solve_matches_oracle(p, n):
+    """NEXT-3, the thick quarter ring (non-isoparametric) with a seeded random RHS:
+    V-cycle to 1e-12, the PCG iterate after the oracle's iteration count to 1e-10, counts ±1."""
+    from oracle import ring
+    amg = _amg()
+    K, _ = amg.iga_poisson(3, p, n, rhs=1, geometry=1)
+    H = amg.Hierarchy(K, amg.params(p))
+    Ho = oracle.setup(ring.assemble_ring(p, n), oracle.OParams.for_degree(p))
+    r = amg_inputs.uniform_pm1(K.shape[0], seed=31)
+    zo = oracle.vcycle(Ho, r)
+    assert np.abs(H.vcycle(dev(r)).cpu().numpy() - zo).max() <= 1e-12 * np.abs(zo).max()
+    uo, ito, rro, histo, rco = oracle.pcg(Ho, r, rtol=1e-6, maxit=200)
+    u, it, rr, hist, st = H.solve(dev(r), rtol=1e-6, maxit=200)
+    assert rco == 0 and st == 0 and abs(it - ito) <= 1
+    u2 = H.solve(dev(r), rtol=0.0, maxit=ito)[0].cpu().numpy()
+    assert np.linalg.norm(u2 - uo) <= 1e-10 * np.linalg.norm(uo)

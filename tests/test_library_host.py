@@ -149,3 +149,37 @@ def test_no_undefined_internal_symbols():
                           os.path.join(ROOT, "paper_2511_21268_b200", "libamg_b200.so")],
                          capture_output=True, text=True).stdout
     assert "amgb" not in out
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 6), (4, 5)])
+def test_ring_operator_bitwise_equal_to_oracle(p, n):
+    """geometry = 1 (thick quarter ring, NEXT-3): correctly rounded weighted 1-D tables on both sides
+    and the canonical evaluation order make K bitwise equal."""
+    from oracle import ring
+    K, F = amg.iga_poisson(3, p, n, rhs=1, geometry=1)
+    Ko = ring.assemble_ring(p, n)
+    assert np.array_equal(K.indptr, Ko.indptr) and np.array_equal(K.indices, Ko.indices)
+    assert np.array_equal(K.data.view(np.uint64), Ko.data.view(np.uint64))
+    assert not F.any()
+
+
+def test_ring_hierarchy_bitwise_equal_to_oracle():
+    from oracle import ring
+    p, n = 3, 8
+    K, _ = amg.iga_poisson(3, p, n, rhs=1, geometry=1)
+    H = amg.Hierarchy(K, amg.params(p, host_only=1))
+    Ho = oracle.setup(ring.assemble_ring(p, n), oracle.OParams.for_degree(p))
+    assert H.info()["levels"] == Ho.nlevels
+    for l, L in enumerate(Ho.levels):
+        e = H.export(l)
+        Kl = e["K"]
+        assert np.array_equal(Kl.indices, L.K.indices) and np.array_equal(Kl.data.view(np.uint64), L.K.data.view(np.uint64))
+        if L.P is not None:
+            assert np.array_equal(e["P"].data.view(np.uint64), L.P.data.view(np.uint64))
+
+
+def test_ring_rejects_bad_combinations():
+    with pytest.raises(amg.AmgError):
+        amg.iga_poisson(2, 2, 4, rhs=1, geometry=1)
+    with pytest.raises(amg.AmgError):
+        amg.iga_poisson(3, 2, 4, rhs=0, geometry=1)
