@@ -73,7 +73,9 @@ typedef struct {
  *          P:L592-605).  x = (1+u)c_x(v), y = (1+u)c_y(v), z = w; sides 1: u=0, 2: u=1, 3: v=0 (y=0),
  *          4: v=1 (x=0), 5: w=0, 6: w=1.  Since JᵀJ = diag(1, r²|c'|², 1), K = A_u⊗B_v⊗M_w +
  *          C_u⊗D_v⊗M_w + E_u⊗B_v⊗K_w with r- and |c'|-weighted 1-D tables (binary128 Gauss, rounded
- *          once), entry ((A·B)·M + (C·D)·M) + (E·B)·K.  Only rhs = 1 (F = 0) is defined for the ring.
+ *          once), entry ((A·B)·M + (C·D)·M) + (E·B)·K.  rhs = 1: F = 0; rhs = 2: the paper's ring data
+ *          (u = e^x sin(xy) cos z, f and g_N of eq:Lshapedcoeff; g_D by one L2 projection
+ *          onto sides 1-3; source by (p+1)³ Gauss points through the map).
  */
 typedef struct {
     int dim;

@@ -222,3 +222,122 @@ def element_loop_ring(p: int, n: int) -> np.ndarray:
             Kd[np.ix_(idx, idx)] += wq * (Gr @ G @ Gr.T)
     keep = free_index_list(3, m, 0b000111)
     return Kd[np.ix_(keep, keep)]
+
+
+# ------------------------------------------------------------------------------------------------
+# the paper's ring data (P:L1093-1102 with eq:Lshapedcoeff P:L1079-1089): plain quadrature, small n
+# ------------------------------------------------------------------------------------------------
+def exact_u(x, y, z):
+    return np.exp(x) * np.sin(x * y) * np.cos(z)
+
+
+def _f(x, y, z):
+    return np.exp(x) * np.cos(z) * (-2.0 * np.cos(x * y) * y + np.sin(x * y) * (y * y + x * x))
+
+
+_GN = {4: lambda x, y, z: -np.exp(x) * np.cos(z) * (np.sin(x * y) + y * np.cos(x * y)),
+       5: lambda x, y, z: np.exp(x) * np.sin(x * y) * np.sin(z),
+       6: lambda x, y, z: -np.exp(x) * np.sin(x * y) * np.sin(z)}
+
+
+def _speed(v):
+    _, _, _, (r, cx, cy, dcx, dcy) = geometry(np.zeros_like(v), v, np.zeros_like(v))
+    return np.sqrt(dcx * dcx + dcy * dcy)
+
+
+def paper_ring_rhs(p: int, n: int):
+    """(F_free, u_D_all) of the paper's ring problem: source ∫ f N det J, Neumann faces 4 (v=1, x=0 plane,
+    dS = du dw), 5/6 (w=0/1, dS = r|c'| du dv), Dirichlet data on sides 1-3 by one joint L2 projection
+    (face measures |c'| dv dw on u=0, 2|c'| dv dw on u=1, du dw on v=0; reading N1.a), lifting with the
+    full ring operator.  (p+1)-point Gauss per element and direction, fp64."""
+    m = n + p
+    xg, wg = gauss(p + 1)
+    t = np.concatenate([(e + xg) / n for e in range(n)])
+    w = np.concatenate([wg / n for _ in range(n)])
+    B = eval_basis(p, n, t)
+    sp_ = _speed(t)
+    # volume: points (u_i, v_j, w_k)
+    U, V, W = np.meshgrid(t, t, t, indexing="ij")
+    x, y, z, (r, cx, cy, dcx, dcy) = geometry(U, V, W)
+    detJ = r * np.sqrt(dcx * dcx + dcy * dcy)
+    fv = _f(x, y, z) * detJ * (w[:, None, None] * w[None, :, None] * w[None, None, :])
+    Fall = np.einsum("ijk,ia,jb,kc->cba", fv, B, B, B)
+    Uf, Wf = np.meshgrid(t, t, indexing="ij")
+    ww = w[:, None] * w[None, :]
+    # side 4: v = 1 (x = 0), in-face (u, w), dS = du dw; N_b(1) = δ_{b,m−1}
+    x4, y4, z4, _ = geometry(Uf, np.ones_like(Uf), Wf)
+    g4 = _GN[4](x4, y4, z4) * ww
+    Fall[:, m - 1, :] += np.einsum("ik,ia,kc->ca", g4, B, B)
+    # sides 5/6: w = 0 / 1, in-face (u, v), dS = r|c'| du dv
+    Uf2, Vf2 = np.meshgrid(t, t, indexing="ij")
+    for side, cz in ((5, 0), (6, m - 1)):
+        x5, y5, z5, (r5, _, _, d5x, d5y) = geometry(Uf2, Vf2, np.full_like(Uf2, 0.0 if side == 5 else 1.0))
+        g5 = _GN[side](x5, y5, z5) * r5 * np.sqrt(d5x * d5x + d5y * d5y) * ww
+        Fall[cz, :, :] += np.einsum("ij,ia,jb->ba", g5, B, B)
+    uD = _ring_projection(p, n, t, w, B, sp_)
+    T = weighted_tables(p, n)
+    Uc = uD.reshape(m, m, m)  # (c, b, a)
+
+    def apply(Az, Ay, Ax):
+        q = np.einsum("ad,cbd->cba", Ax, Uc)
+        q = np.einsum("bd,cda->cba", Ay, q)
+        return np.einsum("cd,dba->cba", Az, q)
+
+    KU = apply(T["M"], T["B"], T["A"]) + apply(T["M"], T["Dv"], T["C"]) + apply(T["K"], T["B"], T["E"])
+    free = free_index_list(3, m, 0b000111)
+    return (Fall.ravel() - KU.ravel())[free], uD
+
+
+def _ring_projection(p, n, t, w, B, sp_):
+    """Joint L2 projection of g_D = u on sides 1 (u=0), 2 (u=1), 3 (v=0) of the ring, dense solve."""
+    m = n + p
+    T = weighted_tables(p, n)
+    a, b, c = np.meshgrid(np.arange(m), np.arange(m), np.arange(m), indexing="ij")
+    on = (a == 0) | (a == m - 1) | (b == 0)
+    dofs = np.sort((a + m * (b + m * c))[on])
+    pos = {int(g): k for k, g in enumerate(dofs)}
+    Mb = np.zeros((len(dofs), len(dofs)))
+    rhs = np.zeros(len(dofs))
+    V1, W1 = np.meshgrid(t, t, indexing="ij")
+    ww = w[:, None] * w[None, :]
+    faces = []
+    for side, fixed, scale in ((1, 0, 1.0), (2, m - 1, 2.0)):  # u = 0 / 1: measure r|c'| dv dw, r = 1 / 2
+        xx, yy, zz, _ = geometry(np.full_like(V1, 0.0 if side == 1 else 1.0), V1, W1)
+        g = exact_u(xx, yy, zz) * scale * _speed(V1) * ww
+        Fface = np.einsum("jk,jb,kc->bc", g, B, B)
+        faces.append((lambda i0, i1, fx=fixed: fx + m * (i0 + m * i1), scale * T["B"], T["M"], Fface))
+    xx, yy, zz, _ = geometry(V1, np.zeros_like(V1), W1)  # v = 0: (u, w), measure du dw
+    g = exact_u(xx, yy, zz) * ww
+    Fface = np.einsum("ik,ia,kc->ac", g, B, B)
+    faces.append((lambda i0, i1: i0 + m * (0 + m * i1), T["M"], T["M"], Fface))
+    for gidx, M0, M1, Fface in faces:
+        for i0 in range(m):
+            for i1 in range(m):
+                gi = pos[gidx(i0, i1)]
+                rhs[gi] += Fface[i0, i1]
+                for j0 in range(max(0, i0 - p), min(m, i0 + p + 1)):
+                    for j1 in range(max(0, i1 - p), min(m, i1 + p + 1)):
+                        Mb[gi, pos[gidx(j0, j1)]] += M0[i0, j0] * M1[i1, j1]
+    uD = np.zeros(m ** 3)
+    uD[dofs] = np.linalg.solve(Mb, rhs)
+    return uD
+
+
+def l2_error_full(p: int, n: int, u_free: np.ndarray, uD: np.ndarray) -> float:
+    """‖u_h − u‖_{L2(Ω)} on the ring, (p+2)³ Gauss points per element with the map's det J."""
+    m = n + p
+    coef = uD.copy()
+    coef[free_index_list(3, m, 0b000111)] = u_free
+    coef = coef.reshape(m, m, m)
+    xg, wg = gauss(p + 2)
+    t = np.concatenate([(e + xg) / n for e in range(n)])
+    w = np.concatenate([wg / n for _ in range(n)])
+    Bq = eval_basis(p, n, t)
+    uh = np.einsum("ax,zyx->zya", Bq, coef)
+    uh = np.einsum("by,zya->zba", Bq, uh)
+    uh = np.einsum("cz,zba->cba", Bq, uh)  # (w, v, u)
+    Wq, Vq, Uq = np.meshgrid(t, t, t, indexing="ij")
+    x, y, z, (r, cx, cy, dcx, dcy) = geometry(Uq, Vq, Wq)
+    detJ = r * np.sqrt(dcx * dcx + dcy * dcy)
+    err = (uh - exact_u(x, y, z)) ** 2 * detJ
+    return float(np.sqrt(np.einsum("c,b,a,cba->", w, w, w, err)))

@@ -363,6 +363,195 @@ void paper_cube_load(int p, int n, const Tables1D &T, const int *lo, const int *
     }
 }
 
+// The paper's ring data (eq:Lshapedcoeff P:L1079-1089): u = e^x sin(xy) cos z.  Source by
+// (p+1)³-point Gauss per element through the map (f·det J), Neumann on side 4 (v = 1, the x = 0 plane,
+// dS = du dw) and sides 5/6 (w = 0/1, dS = r|c'| du dv), g_D = u on sides 1 (u = 0, dS = |c'| dv dw),
+// 2 (u = 1, 2|c'| dv dw), 3 (v = 0, du dw) by one joint L2 projection (reading N1.a; Jacobi-CG),
+// F_free = (source + Neumann)_free − (K_full u_D)_free with the full ring operator.  fp64 quadrature.
+void paper_ring_load(int p, int n, const RingTables &RT, const int *lo, const int *nf, Buf<double> &F) {
+    const int m = n + p, bw = 2 * p + 1;
+    auto id = [m](int a, int b, int c) { return (int64_t)a + (int64_t)m * (b + (int64_t)m * c); };
+    auto band = [bw, p](const std::vector<double> &A, int i, int j) { return A[(size_t)i * bw + (j - i + p)]; };
+    // quadrature points / weights and basis values per element (fp64)
+    std::vector<q128> gxq, gwq;
+    gauss_legendre_q(p + 1, gxq, gwq);
+    const int nq = p + 1;
+    std::vector<double> t((size_t)n * nq), wt((size_t)n * nq), Bv((size_t)n * nq * nq);  // B[e][q][i]
+    for (int e = 0; e < n; e++)
+        for (int q = 0; q < nq; q++) {
+            q128 val[16], der[16];
+            basis_and_derivs(e + p, e + gxq[q], p, n, val, der);
+            t[e * nq + q] = (double)((e + gxq[q]) / n);
+            wt[e * nq + q] = (double)(gwq[q] / n);
+            for (int i = 0; i <= p; i++) Bv[((size_t)e * nq + q) * nq + i] = (double)val[i];
+        }
+    auto geom = [](double u, double v, double &x, double &y, double &r, double &sp) {
+        const double w1 = std::sqrt(2.0) / 2.0;
+        const double X = (1 - v) * (1 - v) + 2 * v * (1 - v) * w1, Y = 2 * v * (1 - v) * w1 + v * v;
+        const double W = (1 - v) * (1 - v) + 2 * v * (1 - v) * w1 + v * v;
+        const double Xp = -2 * (1 - v) + 2 * w1 * (1 - 2 * v), Yp = 2 * w1 * (1 - 2 * v) + 2 * v;
+        const double Wp = -2 * (1 - v) + 2 * w1 * (1 - 2 * v) + 2 * v;
+        const double dcx = (Xp * W - X * Wp) / (W * W), dcy = (Yp * W - Y * Wp) / (W * W);
+        r = 1 + u;
+        x = r * X / W;
+        y = r * Y / W;
+        sp = std::sqrt(dcx * dcx + dcy * dcy);
+    };
+    auto uex = [](double x, double y, double z) { return std::exp(x) * std::sin(x * y) * std::cos(z); };
+    const int64_t m3 = (int64_t)m * m * m;
+    std::vector<double> Fall(m3, 0.0);
+    // --- source: element loop (parallel over z-elements: disjoint c ranges per element row are not
+    //     disjoint across neighbouring elements, so accumulate per element into a private buffer)
+#pragma omp parallel
+    {
+        std::vector<double> loc(m3, 0.0);
+#pragma omp for schedule(static)
+        for (int ez = 0; ez < n; ez++)
+            for (int ey = 0; ey < n; ey++)
+                for (int ex = 0; ex < n; ex++)
+                    for (int qz = 0; qz < nq; qz++)
+                        for (int qy = 0; qy < nq; qy++)
+                            for (int qx = 0; qx < nq; qx++) {
+                                const double u = t[ex * nq + qx], v = t[ey * nq + qy], z = t[ez * nq + qz];
+                                double x, y, r, sp;
+                                geom(u, v, x, y, r, sp);
+                                const double f = std::exp(x) * std::cos(z) *
+                                                 (-2.0 * std::cos(x * y) * y + std::sin(x * y) * (y * y + x * x));
+                                const double wq = f * r * sp * wt[ex * nq + qx] * wt[ey * nq + qy] * wt[ez * nq + qz];
+                                const double *Ba = &Bv[((size_t)ex * nq + qx) * nq];
+                                const double *Bb = &Bv[((size_t)ey * nq + qy) * nq];
+                                const double *Bc = &Bv[((size_t)ez * nq + qz) * nq];
+                                for (int k = 0; k <= p; k++)
+                                    for (int j = 0; j <= p; j++)
+                                        for (int i = 0; i <= p; i++)
+                                            loc[id(ex + i, ey + j, ez + k)] += wq * Ba[i] * Bb[j] * Bc[k];
+                            }
+#pragma omp critical
+        for (int64_t i = 0; i < m3; i++) Fall[i] += loc[i];
+    }
+    // --- Neumann faces
+    for (int e0 = 0; e0 < n; e0++)
+        for (int e1 = 0; e1 < n; e1++)
+            for (int q0 = 0; q0 < nq; q0++)
+                for (int q1 = 0; q1 < nq; q1++) {
+                    const double s0 = t[e0 * nq + q0], s1 = t[e1 * nq + q1];
+                    const double w01 = wt[e0 * nq + q0] * wt[e1 * nq + q1];
+                    const double *B0 = &Bv[((size_t)e0 * nq + q0) * nq], *B1 = &Bv[((size_t)e1 * nq + q1) * nq];
+                    double x, y, r, sp;
+                    // side 4: v = 1, in-face (u = s0, w = s1), dS = du dw
+                    geom(s0, 1.0, x, y, r, sp);
+                    const double g4 = -std::exp(x) * std::cos(s1) * (std::sin(x * y) + y * std::cos(x * y)) * w01;
+                    for (int i = 0; i <= p; i++)
+                        for (int k = 0; k <= p; k++) Fall[id(e0 + i, m - 1, e1 + k)] += g4 * B0[i] * B1[k];
+                    // sides 5 / 6: w = 0 / 1, in-face (u = s0, v = s1), dS = r|c'| du dv
+                    geom(s0, s1, x, y, r, sp);
+                    const double g5 = std::exp(x) * std::sin(x * y) * std::sin(0.0) * r * sp * w01;
+                    const double g6 = -std::exp(x) * std::sin(x * y) * std::sin(1.0) * r * sp * w01;
+                    for (int i = 0; i <= p; i++)
+                        for (int j = 0; j <= p; j++) {
+                            Fall[id(e0 + i, e1 + j, 0)] += g5 * B0[i] * B1[j];
+                            Fall[id(e0 + i, e1 + j, m - 1)] += g6 * B0[i] * B1[j];
+                        }
+                }
+    // --- Dirichlet projection: face 0 (u=0, in-face v,w, mass B_v⊗M_w), face 1 (u=1, 2·B_v⊗M_w),
+    //     face 2 (v=0, in-face u,w, mass M_u⊗M_w)
+    std::vector<double> rhs(m3, 0.0), diag(m3, 0.0), xs(m3, 0.0), r(m3), z(m3), pp(m3, 0.0), q(m3);
+    for (int e0 = 0; e0 < n; e0++)
+        for (int e1 = 0; e1 < n; e1++)
+            for (int q0 = 0; q0 < nq; q0++)
+                for (int q1 = 0; q1 < nq; q1++) {
+                    const double s0 = t[e0 * nq + q0], s1 = t[e1 * nq + q1];
+                    const double w01 = wt[e0 * nq + q0] * wt[e1 * nq + q1];
+                    const double *B0 = &Bv[((size_t)e0 * nq + q0) * nq], *B1 = &Bv[((size_t)e1 * nq + q1) * nq];
+                    double x, y, rr, sp;
+                    geom(0.0, s0, x, y, rr, sp);
+                    const double g0 = uex(x, y, s1) * sp * w01;  // u = 0: r = 1
+                    geom(1.0, s0, x, y, rr, sp);
+                    const double g1 = uex(x, y, s1) * 2.0 * sp * w01;  // u = 1: r = 2
+                    geom(s0, 0.0, x, y, rr, sp);
+                    const double g2 = uex(x, y, s1) * w01;  // v = 0: (u = s0, w = s1)
+                    for (int i = 0; i <= p; i++)
+                        for (int k = 0; k <= p; k++) {
+                            rhs[id(0, e0 + i, e1 + k)] += g0 * B0[i] * B1[k];
+                            rhs[id(m - 1, e0 + i, e1 + k)] += g1 * B0[i] * B1[k];
+                            rhs[id(e0 + i, 0, e1 + k)] += g2 * B0[i] * B1[k];
+                        }
+                }
+    auto apply_bnd = [&](const std::vector<double> &xv, std::vector<double> &yv) {
+        std::fill(yv.begin(), yv.end(), 0.0);
+        for (int face = 0; face < 3; face++) {
+            const double sc = face == 1 ? 2.0 : 1.0;
+            const std::vector<double> &M0 = face == 2 ? RT.M : RT.B;
+#pragma omp parallel for schedule(static)
+            for (int c = 0; c < m; c++)
+                for (int u = 0; u < m; u++) {
+                    double acc = 0.0;
+                    for (int c2 = std::max(0, c - p); c2 <= std::min(m - 1, c + p); c2++)
+                        for (int u2 = std::max(0, u - p); u2 <= std::min(m - 1, u + p); u2++) {
+                            const int64_t j = face == 2 ? id(u2, 0, c2) : id(face == 0 ? 0 : m - 1, u2, c2);
+                            acc += sc * band(M0, u, u2) * band(RT.M, c, c2) * xv[j];
+                        }
+                    const int64_t i = face == 2 ? id(u, 0, c) : id(face == 0 ? 0 : m - 1, u, c);
+                    yv[i] += acc;
+                }
+        }
+    };
+    for (int c = 0; c < m; c++)
+        for (int u = 0; u < m; u++) {
+            diag[id(0, u, c)] += band(RT.B, u, u) * band(RT.M, c, c);
+            diag[id(m - 1, u, c)] += 2.0 * band(RT.B, u, u) * band(RT.M, c, c);
+            diag[id(u, 0, c)] += band(RT.M, u, u) * band(RT.M, c, c);
+        }
+    double rz = 0.0, bb = 0.0;
+    for (int64_t i = 0; i < m3; i++) {
+        r[i] = rhs[i];
+        z[i] = diag[i] > 0.0 ? r[i] / diag[i] : 0.0;
+        pp[i] = z[i];
+        rz += r[i] * z[i];
+        bb += rhs[i] * rhs[i];
+    }
+    for (int it = 0; it < 100000 && bb > 0.0; it++) {
+        apply_bnd(pp, q);
+        double pq = 0.0;
+        for (int64_t i = 0; i < m3; i++) pq += pp[i] * q[i];
+        if (!(pq > 0.0)) break;
+        const double alpha = rz / pq;
+        double rn = 0.0, rzn = 0.0;
+        for (int64_t i = 0; i < m3; i++) {
+            xs[i] += alpha * pp[i];
+            r[i] -= alpha * q[i];
+            rn += r[i] * r[i];
+            z[i] = diag[i] > 0.0 ? r[i] / diag[i] : 0.0;
+            rzn += r[i] * z[i];
+        }
+        if (rn <= 1e-30 * bb) break;
+        const double beta = rzn / rz;
+        for (int64_t i = 0; i < m3; i++) pp[i] = z[i] + beta * pp[i];
+        rz = rzn;
+    }
+    // --- lifting with the full ring operator and the free-DOF load
+    const int64_t N = (int64_t)nf[0] * nf[1] * nf[2];
+    F.alloc(N);
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < N; row++) {
+        const int a = lo[0] + (int)(row % nf[0]);
+        const int b = lo[1] + (int)((row / nf[0]) % nf[1]);
+        const int c = lo[2] + (int)(row / ((int64_t)nf[0] * nf[1]));
+        double lift = 0.0;
+        for (int c2 = std::max(0, c - p); c2 <= std::min(m - 1, c + p); c2++)
+            for (int b2 = std::max(0, b - p); b2 <= std::min(m - 1, b + p); b2++)
+                for (int a2 = std::max(0, a - p); a2 <= std::min(m - 1, a + p); a2++) {
+                    const double u = xs[id(a2, b2, c2)];
+                    if (u == 0.0) continue;
+                    const double t1 = band(RT.A, a, a2) * band(RT.B, b, b2) * band(RT.M, c, c2);
+                    const double t2 = band(RT.C, a, a2) * band(RT.Dv, b, b2) * band(RT.M, c, c2);
+                    const double t3 = band(RT.E, a, a2) * band(RT.B, b, b2) * band(RT.K, c, c2);
+                    lift += (t1 + t2 + t3) * u;
+                }
+        F[row] = Fall[id(a, b, c)] - lift;
+    }
+}
+
 }  // namespace
 
 void iga_tables_hat(int p, int n, double *mhat, double *khat) { hat_tables(p, n, mhat, khat); }
@@ -452,7 +641,11 @@ void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
             }
         }
     }
-    // load vector (c.5), or the paper's own cube data (rhs = 2)
+    // load vector (c.5), or the paper's own data (rhs = 2): cube or quarter ring
+    if (d.rhs == 2 && ring) {
+        paper_ring_load(p, n, RT, lo, nf, F);
+        return;
+    }
     if (d.rhs == 2) {
         if (dim != 3 || d.dirichlet_sides != 0b000111u)
             throw Error{AMG_EINVAL, "rhs = 2 (the paper's cube data) needs dim = 3 and Dirichlet sides 1, 2, 3"};

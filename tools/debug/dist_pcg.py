@@ -22,6 +22,12 @@ for solver in ("pcg", "fcg"):
     if os.environ.get("DBG_VCYCLE_FIRST") == "1":
         zv = H.vcycle(Fl.clone())
         torch.cuda.synchronize()
+    if os.environ.get("DBG_GATHER") == "1":
+        zz = H.vcycle(Fl.clone()).cpu().numpy()
+        parts = [None] * world
+        dist.all_gather_object(parts, (b, e, zz))
+    u0 = torch.zeros_like(Fl)
+    print(f"rank {rank}: |F|={Fl.norm().item():.6e} |u0|={u0.norm().item():.3e} dev={torch.cuda.current_device()}", flush=True)
     u, it, rr, hist, st = H.solve(Fl, rtol=1e-6)
     if rank == 0:
         H1 = amg.Hierarchy(K, amg.params(3, **kw))
