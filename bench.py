@@ -193,13 +193,13 @@ def run_gpu(args) -> None:
     wl = workload_desc(args.config, world)
     dim, p, n, m = wl["dim"], wl["p"], wl["n"], wl["m"]
     geom = wl.get("geometry", 0)
-    paper = args.problem == "paper" and dim == 3 and geom == 0
+    paper = args.problem == "paper" and dim == 3
     t0 = time.perf_counter()
-    if geom == 1:  # quarter ring: seeded random right-hand side (its paper data is not generated)
+    if geom == 1 and not paper:  # quarter ring, manufactured-style run: seeded random right-hand side
         K, _ = amg.iga_poisson(dim, p, n, rhs=1, geometry=1)
         F = amg_inputs.uniform_pm1(K.shape[0], seed=amg_inputs.SEED)
     else:
-        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
+        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0, geometry=geom)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     prm = amg.params(p, format=args.format, krylov=1 if paper else 0, coarse_solver=1 if paper else 0)
@@ -313,14 +313,16 @@ def run_gpu(args) -> None:
             "scaling": wl["scaling"],
             "vs_baseline": None,
             "dtype": "f64",
-            "data": ("synthetic: generated IgA system with the paper's own cube data (f = −e^{x+z} sin y, "
+            "data": ("synthetic: generated quarter-ring IgA system with the paper's ring data (u = e^x sin(xy) cos z, "
+                     "projected Dirichlet + Neumann loads)" if paper and geom == 1 else
+                     "synthetic: generated IgA system with the paper's own cube data (f = −e^{x+z} sin y, "
                      "projected Dirichlet + Neumann loads)" if paper else
                      "synthetic: generated quarter-ring IgA system, seeded uniform(−1,1) RHS" if geom == 1 else
                      "synthetic (generated IgA Poisson system, manufactured-solution RHS)"),
             "config": {
                 "workload": f"{args.config}: {dim}-D Poisson on the " + ("thick quarter ring" if geom == 1 else "cube")
                             + f", B-spline p={p}, n={n} elements/dir, {N} free DOFs, "
-                            + ("the paper's cube experiment (its data, FCG, §5.1 coarse CG)" if paper else
+                            + ("the paper's experiment (its data, FCG, §5.1 coarse CG)" if paper else
                                "random RHS, PCG" if geom == 1 else "manufactured sine RHS, PCG") + f", rtol {args.rtol}",
                 "problem": args.problem,
                 "dofs": N, "nnz_K0": info["nnz"][0], "levels": info["levels"], "level_N": info["N"],

@@ -167,7 +167,11 @@ inline dev::P2P p2p_of(const DevState &D, bool part, unsigned mask = ~0u) {
     p.wait_mask = mask;
     return p;
 }
-inline dev::P2P p2p_of(const DevState &D, const DCsr &A) {
+// A kernel working for operator A that waits at its start and publishes at its end (plain kernels).
+inline dev::P2P p2p_of(const DevState &D, const DCsr &A) { return p2p_of(D, A.part, A.wmask); }
+// The CSR cores on A: with A's boundary-first group order (mid-kernel publication).  ONLY for kernels
+// that implement the group order — a plain kernel handed a group order would never publish.
+inline dev::P2P p2p_csr(const DevState &D, const DCsr &A) {
     dev::P2P p = p2p_of(D, A.part, A.wmask);
     if (p.nranks > 0 && A.fmt == 0 && A.gorder && A.gorder_G == A.G) {
         p.gorder = A.gorder;

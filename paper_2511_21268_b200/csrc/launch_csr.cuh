@@ -24,7 +24,7 @@ void launch_csr4t_gu(DevState &D, const DCsr &A, const Cols &cols, const double 
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
     dev::k_csr4t<G, U, Epi, Cols><<<grid, dev::kBlockT, smem, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
-                                                                      (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));
+                                                                      (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
 }
 
 template <int G, int U, class Epi, class Cols>
@@ -41,7 +41,7 @@ void launch_csr2_gu(DevState &D, const DCsr &A, const Cols &cols, const double *
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, (int64_t)per_sm * D.nsm));
     dev::k_csr2<G, U, Epi, Cols><<<grid, dev::kBlock, 0, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
-                                                               (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)),
+                                                               (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)),
                                                                A.mult >= 8 ? A.pf : 0);
 }
 

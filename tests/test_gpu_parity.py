@@ -300,3 +300,19 @@ def test_ring_solve_matches_oracle(p, n):
     assert rco == 0 and st == 0 and abs(it - ito) <= 1
     u2 = H.solve(dev(r), rtol=0.0, maxit=ito)[0].cpu().numpy()
     assert np.linalg.norm(u2 - uo) <= 1e-10 * np.linalg.norm(uo)
+
+
+@pytest.mark.parametrize("p,n", [(2, 8), (3, 8)])
+def test_ring_paper_experiment(p, n):
+    """The paper's ring configuration: its data (rhs = 2, geometry = 1), FCG, §5.1 coarse CG — counts
+    within ±1 of the oracle's and the converged true residual."""
+    from oracle import ring
+    amg = _amg()
+    K, F = amg.iga_poisson(3, p, n, rhs=2, geometry=1)
+    H = amg.Hierarchy(K, amg.params(p, krylov=1, coarse_solver=1))
+    Ho = oracle.setup(ring.assemble_ring(p, n), oracle.OParams.for_degree(p, coarse_solver=1))
+    uo, ito, rro, histo, rco = oracle.fcg(Ho, F, rtol=1e-6, maxit=200)
+    u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6, maxit=200)
+    assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
+    ud = u.cpu().numpy()
+    assert np.linalg.norm(F - oracle.spmv(K.to_scipy(), ud)) <= 1.05e-6 * np.linalg.norm(F)

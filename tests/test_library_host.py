@@ -182,4 +182,12 @@ def test_ring_rejects_bad_combinations():
     with pytest.raises(amg.AmgError):
         amg.iga_poisson(2, 2, 4, rhs=1, geometry=1)
     with pytest.raises(amg.AmgError):
-        amg.iga_poisson(3, 2, 4, rhs=0, geometry=1)
+        amg.iga_poisson(3, 2, 4, rhs=0, geometry=1)  # the manufactured sine is a cube solution
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 6), (4, 5)])
+def test_paper_ring_load_matches_oracle(p, n):
+    from oracle import ring
+    K, F = amg.iga_poisson(3, p, n, rhs=2, geometry=1)
+    Fo, _ = ring.paper_ring_rhs(p, n)
+    assert np.abs(F - Fo).max() <= 1e-13 * np.abs(Fo).max()

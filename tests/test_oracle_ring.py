@@ -50,3 +50,18 @@ def test_volume():
 def test_operator_complexity_table3c(k, p):
     H = oracle.setup(ring.assemble_ring(p, k), oracle.OParams.for_degree(p))
     assert abs(H.opc() - TABLE3C[(k, p)]) <= 0.02, H.opc()
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_paper_ring_data_converges_at_order(p):
+    """The paper's ring problem (u = e^x sin(xy) cos z) with its projected Dirichlet and
+    Neumann data: L2 error decays at rate ≥ p + 0.5 under refinement (n = 4, 8, 12)."""
+    import scipy.sparse.linalg as spla
+    ns = (4, 8, 12)
+    errs = []
+    for n in ns:
+        F, uD = ring.paper_ring_rhs(p, n)
+        uf = spla.spsolve(ring.assemble_ring(p, n).tocsc(), F)
+        errs.append(ring.l2_error_full(p, n, uf, uD))
+    rates = [np.log(errs[i] / errs[i + 1]) / np.log(ns[i + 1] / ns[i]) for i in range(2)]
+    assert min(rates) >= p + 0.5, (errs, rates)
