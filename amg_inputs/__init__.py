@@ -16,7 +16,9 @@ C2     3    2    32    single-B200 full hierarchy, parity at full size
 C3     3    3    96    the paper's GPU cube case (Table 1b k=96: 941,094 DOFs)
 C4     3    4    128   high-degree bandwidth stress
 C5     3    2    250+  weak scaling, ~16M DOFs per GPU (n = 250/315/398/502)
-R3     3    3    96    thick quarter ring (NEXT-3, Table 3), random RHS
+C5s    3    2    158+  weak scaling, ~4M DOFs per GPU (n = 158/200/252/317)
+R3     3    3    96    thick quarter ring (NEXT-3, Table 3)
+R4     3    4    96    thick quarter ring, the paper's GPU ring case
 =====  ===  ===  ====  =====================================================
 """
 from __future__ import annotations
@@ -32,10 +34,16 @@ CONFIGS = {
     "C3": dict(dim=3, p=3, n=96),
     "C4": dict(dim=3, p=4, n=128),
     "C5": dict(dim=3, p=2, n=250),
+    # C5 at a quarter of the per-GPU size (≈ 4M DOFs per GPU): the weak-scaling series that fits one
+    # global host setup in the GPU box's host RAM at 2 and 4 GPUs
+    "C5s": dict(dim=3, p=2, n=158),
     # NEXT-3: the thick quarter ring, Table 3 k=96 p=3 (941,094 DOFs); seeded random RHS
     "R3": dict(dim=3, p=3, n=96, geometry=1),
+    # the paper's GPU ring case (k=96 p=4, 970,200 DOFs; 6.234 s on one A30)
+    "R4": dict(dim=3, p=4, n=96, geometry=1),
 }
 C5_WEAK_N = {1: 250, 2: 315, 4: 398, 8: 502}
+C5S_WEAK_N = {1: 158, 2: 200, 4: 252, 8: 317}
 
 # Chebyshev degree by spline degree: P:L1117 (deg_3=8, deg_4=12, deg_5=14, deg_6=16);
 # p=2 is unstated in the paper -> 4 (SURVEY c.16); p=1 -> 2.

@@ -47,11 +47,12 @@ def load_peaks():
 
 def workload_desc(cfg: str, world: int = 1) -> dict:
     """The BASELINE.json config; C5 is the weak-scaling one (n grows with the GPU count so that every
-    GPU keeps ≈ 16M DOFs: n = 250/315/398/502 at 1/2/4/8 GPUs), every other config is strong scaling."""
+    GPU keeps ≈ 16M DOFs: n = 250/315/398/502 at 1/2/4/8 GPUs; C5s ≈ 4M DOFs per GPU: n =
+    158/200/252/317), every other config is strong scaling."""
     c = dict(amg_inputs.CONFIGS[cfg])
-    weak = cfg == "C5"
+    weak = cfg in ("C5", "C5s")
     if weak:
-        c["n"] = amg_inputs.C5_WEAK_N.get(world, c["n"])
+        c["n"] = (amg_inputs.C5_WEAK_N if cfg == "C5" else amg_inputs.C5S_WEAK_N).get(world, c["n"])
     return dict(c, name=cfg, m=amg_inputs.CHEB_DEGREE[c["p"]], scaling="weak" if weak else "strong")
 
 
@@ -194,31 +195,52 @@ def run_gpu(args) -> None:
     dim, p, n, m = wl["dim"], wl["p"], wl["n"], wl["m"]
     geom = wl.get("geometry", 0)
     paper = args.problem == "paper" and dim == 3
+    # the problem is generated once (rank 0 under torchrun)
     t0 = time.perf_counter()
-    if geom == 1 and not paper:  # quarter ring, manufactured-style run: seeded random right-hand side
-        K, _ = amg.iga_poisson(dim, p, n, rhs=1, geometry=1)
-        F = amg_inputs.uniform_pm1(K.shape[0], seed=amg_inputs.SEED)
-    else:
-        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0, geometry=geom)
+    K = F = None
+    if rank == 0:
+        if geom == 1 and not paper:  # quarter ring, manufactured-style run: seeded random right-hand side
+            K, _ = amg.iga_poisson(dim, p, n, rhs=1, geometry=1)
+            F = amg_inputs.uniform_pm1(K.shape[0], seed=amg_inputs.SEED)
+        else:
+            K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0, geometry=geom)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     prm = amg.params(p, format=args.format, krylov=1 if paper else 0, coarse_solver=1 if paper else 0)
     if world > 1:
-        # every rank builds the same global hierarchy; host threads are shared by the ranks
-        prm.num_threads = max(1, (os.cpu_count() or world) // world)
-    H = amg.Hierarchy(K, prm, dist=amg.make_dist(rank, world, device=local) if world > 1 else None)
+        # one host setup on rank 0 with all host cores; every rank receives its share (local operators,
+        # halo plans, replicated levels) over gloo and builds its device state from it
+        gl = dist.new_group(backend="gloo")
+        H = amg.setup_distributed(K, prm, rank, world, device=local, group=gl)
+    else:
+        H = amg.Hierarchy(K, prm)
+    del K
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     info = H.info()
-    N = K.shape[0]
+    N = info["N"][0]
     rb, re_ = H.local_rows()
-    F = np.ascontiguousarray(F[rb:re_])
-    del K
+    if world > 1:  # rank 0 sends every rank its rows of F
+        mine = torch.tensor([rb, re_], dtype=torch.int64)
+        allb = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allb, mine, group=gl)
+        if rank == 0:
+            for q in range(1, world):
+                b_, e_ = allb[q].tolist()
+                dist.send(torch.from_numpy(np.ascontiguousarray(F[b_:e_])), q, group=gl)
+            F = np.ascontiguousarray(F[rb:re_])
+        else:
+            Ft = torch.empty(re_ - rb, dtype=torch.float64)
+            dist.recv(Ft, 0, group=gl)
+            F = Ft.numpy()
+    else:
+        F = np.ascontiguousarray(F[rb:re_])
     ops = {(l, k): H.op_config(l, k) for l in range(info["levels"]) for k in range(3)
            if k == 0 or l + 1 < info["levels"]}
     op_cfg = [ops[(l, 0)] for l in range(info["levels"])]
     k0 = op_cfg[0]
-    cols = "ColsD16" if "_d16" in k0["kernel"] else "ColsI32"
+    kb = k0["kernel_bits"]
+    cols = ("ColsD16" if kb & 2 else "ColsI32") + (f"V{8 * k0['value_index_bytes']}" if kb & 8 else "")
     family = "k_csr4t" if k0["kernel"].startswith("csr_tma") else "k_csr2"
     pf = ", L2 prefetch of the next row" if k0["kernel"].endswith("_pf") else ""
     kname = f"{family}<G={k0['G']},U={k0['U']},EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0{pf})"
@@ -342,6 +364,7 @@ def run_gpu(args) -> None:
             "s_per_iter": round(solve_s / max(iters, 1), 7),
             "relres": relres,
             "setup_s": round(t_setup, 3),
+            "setup_phases": getattr(H, "setup_phases", None),
             "generator_s": round(t_gen, 3),
             "vcycle_GBps": round(vcyc_gbs, 1),
             "vcycle_frac_of_peak": round(vcyc_gbs / peak, 4),

@@ -109,10 +109,14 @@ typedef struct {
     int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30)                */
     int64_t coarse_size;    /* coarsest when N_l <= coarse_size (50)                 */
     int max_levels;         /* 20                                                                 */
-    int format;             /* device matrix format: 0 auto (rows padded to 8; autotuned kernel and column
-                               source per operator), 1 CSR warp-per-row, 2 SELL-32 (row per lane),
-                               3 TMA-staged CSR, 4 CSR with 16-bit column offsets (register core),
-                               5 CSR with 16-bit column offsets (TMA-staged values) */
+    int format;             /* device matrix format: 0 auto (K_l with >= 2e6 non-zeros, rows spanning
+                               < 65536 columns, <= 65536 distinct values and <= 25 % slice padding:
+                               SELL-VI, a fixed rule; every other operator: CSR rows padded to 8 with the
+                               kernel, column and value source autotuned), 1 CSR warp-per-row,
+                               2 SELL-32 (row per lane), 3 TMA-staged CSR, 4 CSR with 16-bit column
+                               offsets (register core), 5 CSR with 16-bit column offsets (TMA-staged
+                               values), 6 SELL-VI (row per lane, 16-bit column offset + 16-bit value
+                               index per entry) for every K_l, P̄_l, R_l that admits it, any size */
     int host_only;          /* 1: build the hierarchy on the host only (export/inspection; no CUDA call) */
     int num_threads;        /* host setup threads (OpenMP); 0 = runtime default                     */
     int krylov;             /* outer solver: 0 = PCG (c.19); 1 = flexible CG, Notay's FCG(1)
@@ -152,7 +156,8 @@ amg_status amg_nccl_unique_id(unsigned char id[128]);
  * nnz; levels with nnz <= 7e6 (env AMG_REPLICATE_NNZ) and the coarsest are replicated on all ranks.
  * With nranks > 1, the F and u passed to amg_pcg_solve are this rank's rows [row_begin, row_end) of
  * level 0 (global numbering); every rank builds the same global hierarchy on the host from the same
- * full K.  Returns [0, N_0) on one GPU. */
+ * full K (or receives its share of it: amg_share_export below).  Returns [0, N_0) on one GPU.  Host
+ * information: also valid for host_only setups. */
 amg_status amg_local_rows(amg_hierarchy *H, int64_t *row_begin, int64_t *row_end);
 
 /* Builds the hierarchy of K on the host (deterministic; bitwise reproducible; c.6-c.15) and, unless
@@ -205,25 +210,33 @@ amg_status amg_set_profiling(amg_hierarchy *H, int enable); /* enable resets the
 amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
 
 /* Device kernel chosen for operator op (0 K_l, 1 P̄_l, 2 R_l) of level l: layout (0 padded CSR,
- * 1 SELL-32), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
+ * 1 SELL-32, 2 SELL-VI: row per lane, 16-bit column offset + 16-bit value index per entry), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
  * source, 0 int32 columns, 1 16-bit column offsets from a per-row base; bit 2: register core with an L2
- * bulk prefetch of the next row), rows per warp group G, pairs per lane per round trip
- * U, stored entries (with padding), the autotuned y = A·x time in microseconds (0 if the heuristic
- * choice was kept), the bytes one application streams for the operator in that format (8 B per value
- * of the nnz entries + the column data actually stored + 8 B row pointers; vectors excluded) and nnz.
- * AMG_EINVAL for a bad level/op. */
+ * bulk prefetch of the next row; bit 3: value source, 0 streamed fp64 values, 1 value index into the
+ * operator's table of distinct values — CSR-VI, register core only), rows per warp group G, pairs per
+ * lane per round trip U, stored entries (with padding), the autotuned y = A·x time in microseconds (0
+ * if the heuristic choice was kept), the bytes one application streams for the operator in that format
+ * (8 B per value, or the value index bytes + 8 B per distinct value, for the nnz entries + the column
+ * data actually stored + 8 B row pointers; vectors excluded), nnz, the number of distinct values in
+ * the value table (0: no value index built) and the bytes of one value index (2: packed with the 16-bit
+ * column offset into one 32-bit word; 4; 0: none).  AMG_EINVAL for a bad level/op. */
 typedef struct {
     int layout, kernel, G, U;
     int64_t stored;
     double tuned_us;
     double alg_bytes;
     int64_t nnz;
+    int64_t n_values;
+    int value_index_bytes;
 } amg_op_config;
 amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
 /* Force the kernel configuration of one CSR-layout operator (experiments and the kernel-equivalence
  * tests): kernel as in the amg_op_config struct: bit 1 needs the 16-bit encoding (formats 0, 3, 4, 5, and
  * only where every row spans < 65536 columns); bit 0 = TMA needs rows padded to 8 and U <= 4; bit 2
- * (prefetch) needs the register core and rows padded to 8; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
+ * (prefetch) needs the register core and rows padded to 8; bit 3 (value index) needs the register core
+ * and a value table (built at setup for format 0 operators with >= 2e6 stored entries, >= 4 entries per
+ * distinct value and <= 2^21 distinct values, unless env AMG_VALUE_INDEX=0); a SELL-VI operator
+ * (layout 2) takes kernel 0, G 32 and U in {1, 2, 4} only; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
  * sums each row in the same order, so results are bitwise unchanged.  Drops captured PCG graphs.
  * AMG_EINVAL for a bad level/op or an unavailable configuration. */
 amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);
@@ -252,6 +265,24 @@ typedef struct {
     amg_csr local;
 } amg_dist_view;
 amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist_view *view);
+
+/* Shared setup for one process per GPU (the host hierarchy is built once, not once per
+ * rank).  One process calls amg_setup on the full K with prm->host_only = 1 and dist = NULL, then
+ * amg_share_export once per rank: *share receives a malloc'd blob (free with amg_free) of *bytes bytes
+ * holding everything rank `rank` of an nranks-GPU run needs — the row bounds of every level, its local
+ * operators and halo plans on the distributed levels (the same plan amg_setup with that amg_dist would
+ * build), the replicated levels whole, every level's size, nnz, ω and ℓ1 diagonal.  The caller moves
+ * the blob to that rank (e.g. torch.distributed).  AMG_EINVAL for a bad rank/nranks or a hierarchy
+ * itself built from a share; AMG_ENOMEM.
+ * Each rank then calls amg_setup_from_share with its blob and its amg_dist, whose rank/nranks must match the
+ * export (NULL dist = rank 0 of 1): the result behaves like amg_setup's for that rank — same device
+ * state, same kernels, bitwise the same solve — except that amg_hierarchy_export is unavailable
+ * (AMG_EINVAL: the global operators are not held).  host_only = 1 skips the device part (for
+ * amg_dist_view_get / amg_hierarchy_info).  The blob is borrowed (copied); AMG_EINVAL on a truncated or
+ * corrupt blob. */
+amg_status amg_share_export(const amg_hierarchy *H, int rank, int nranks, void **share, int64_t *bytes);
+amg_status amg_setup_from_share(const void *share, int64_t bytes, const amg_dist *dist, int host_only,
+                                amg_hierarchy **H);
 
 void amg_hierarchy_free(amg_hierarchy *H);
 

@@ -19,7 +19,8 @@ import numpy as np
 from . import _lib
 from ._lib import AmgError, check, lib
 
-__all__ = ["AmgError", "Hierarchy", "iga_poisson", "iga_tables", "params", "use_torch_allocator", "HostCsr"]
+__all__ = ["AmgError", "Hierarchy", "iga_poisson", "iga_tables", "params", "use_torch_allocator", "HostCsr",
+           "Share", "setup_distributed"]
 
 
 @dataclass
@@ -150,10 +151,34 @@ def _stream_ptr(stream) -> C.c_void_p:
     return C.c_void_p(getattr(stream, "cuda_stream", stream))
 
 
+class Share:
+    """amg_share_export's blob: a library-owned byte array (``array``: zero-copy uint8 view), freed
+    with amg_free by ``close()`` (or garbage collection)."""
+
+    def __init__(self, ptr: C.c_void_p, nbytes: int):
+        self._p, self.nbytes = ptr, nbytes
+        self.array = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(nbytes,))
+
+    def close(self) -> None:
+        if getattr(self, "_p", None) and self._p.value:
+            self.array = None
+            lib().amg_free(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class Hierarchy:
     """amg_setup / amg_pcg_solve / amg_vcycle / amg_level_apply / export / info on one handle."""
 
     def __init__(self, K, prm: _lib.amg_params | None = None, dist: _lib.amg_dist | None = None):
+        if K is None:  # from_share
+            self._h = C.c_void_p()
+            return
         c, keep = _borrow(K)
         self._h = C.c_void_p()
         if prm is None:
@@ -164,6 +189,25 @@ class Hierarchy:
                               C.byref(self._h)))
         self.prm = prm
         del keep
+
+    @classmethod
+    def from_share(cls, share, dist: _lib.amg_dist | None = None, host_only: bool = False) -> "Hierarchy":
+        """amg_setup_from_share: this rank's hierarchy from its blob (a Share, or any uint8 buffer)."""
+        arr = share.array if isinstance(share, Share) else np.ascontiguousarray(share, dtype=np.uint8)
+        if not host_only:
+            use_torch_allocator()
+        H = cls(None)
+        check(lib().amg_setup_from_share(arr.ctypes.data_as(C.c_void_p), arr.size,
+                                         C.byref(dist) if dist is not None else None, int(host_only),
+                                         C.byref(H._h)))
+        H.prm = None
+        return H
+
+    def export_share(self, rank: int, nranks: int) -> Share:
+        """amg_share_export: what rank `rank` of an nranks-GPU run needs from this (host) hierarchy."""
+        p, n = C.c_void_p(), C.c_int64()
+        check(lib().amg_share_export(self._h, rank, nranks, C.byref(p), C.byref(n)))
+        return Share(p, n.value)
 
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
@@ -286,9 +330,14 @@ class Hierarchy:
     def op_config(self, level: int, op: int = 0) -> dict:
         c = _lib.amg_op_config()
         check(lib().amg_operator_config(self._h, level, op, C.byref(c)))
-        return dict(layout=("csr", "sell32")[c.layout],
-                    kernel=("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")[c.kernel], G=c.G, U=c.U,
-                    stored=c.stored, nnz=c.nnz, alg_bytes=c.alg_bytes, tuned_us=round(c.tuned_us, 2))
+        k = c.kernel
+        name = ("csr_tma" if k & 1 else "csr_regs") + ("_d16" if k & 2 else "") + \
+            (f"_vi{8 * c.value_index_bytes}" if k & 8 else "") + ("_pf" if k & 4 else "")
+        if c.layout == 2:
+            name = "sellvi"
+        return dict(layout=("csr", "sell32", "sellvi")[c.layout], kernel=name, kernel_bits=k, G=c.G, U=c.U,
+                    stored=c.stored, nnz=c.nnz, alg_bytes=c.alg_bytes, tuned_us=round(c.tuned_us, 2),
+                    n_values=c.n_values, value_index_bytes=c.value_index_bytes)
 
     def set_op_config(self, level: int, op: int, kernel: int, G: int, U: int) -> None:
         check(lib().amg_operator_set_config(self._h, level, op, kernel, G, U))
@@ -305,3 +354,69 @@ class Hierarchy:
         check(lib().amg_get_kernel_stats(self._h, C.byref(s)))
         return dict(launches=s.launches, total_ms=s.total_ms, bytes_per_launch=s.bytes_per_launch,
                     kernels_launched=s.kernels_launched)
+
+
+def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: int = 0, group=None,
+                      nccl_id: bytes | None = None, host_only: bool = False,
+                      chunk_bytes: int = 1 << 28) -> Hierarchy:
+    """One host setup for the whole job: rank 0 builds the hierarchy of K once
+    (amg_setup, host_only), exports every rank's share (amg_share_export) and sends it over `group`
+    (a gloo group of torch.distributed; created when None); every rank then creates its device state
+    from its own share (amg_setup_from_share).  K is only read on rank 0 (others pass None).  Plumbing
+    only: the plans and the device state are the library's."""
+    import torch
+    import torch.distributed as dist
+
+    import time
+
+    ph = {}
+    t0 = time.perf_counter()
+
+    def lap(name):
+        nonlocal t0
+        t1 = time.perf_counter()
+        ph[name] = round(ph.get(name, 0.0) + t1 - t0, 3)
+        t0 = t1
+
+    if group is None:
+        group = dist.new_group(backend="gloo")
+    d = make_dist(rank, nranks, device=device, nccl_id=nccl_id)
+    size = torch.zeros(1, dtype=torch.int64)
+    lap("init")
+    if rank == 0:
+        hp = _lib.amg_params()
+        C.memmove(C.byref(hp), C.byref(prm), C.sizeof(hp))
+        hp.host_only = 1
+        G = Hierarchy(K, hp)
+        lap("host_setup")
+        mine = None
+        for q in range(nranks):
+            sh = G.export_share(q, nranks)
+            lap("export")
+            ph["share_bytes"] = ph.get("share_bytes", 0) + sh.nbytes
+            if q == 0:
+                mine = sh
+                continue
+            size[0] = sh.nbytes
+            dist.send(size, q, group=group)
+            t = torch.from_numpy(sh.array)
+            for o in range(0, sh.nbytes, chunk_bytes):
+                dist.send(t[o:o + chunk_bytes], q, group=group)
+            sh.close()
+            lap("send")
+        G.close()
+        H = Hierarchy.from_share(mine, d, host_only=host_only)
+        mine.close()
+    else:
+        dist.recv(size, 0, group=group)
+        lap("wait")
+        buf = torch.empty(int(size[0]), dtype=torch.uint8)
+        for o in range(0, buf.numel(), chunk_bytes):
+            dist.recv(buf[o:o + chunk_bytes], 0, group=group)
+        lap("recv")
+        H = Hierarchy.from_share(buf.numpy(), d, host_only=host_only)
+        del buf
+    lap("device_setup")
+    H.prm = prm
+    H.setup_phases = ph
+    return H

@@ -21,9 +21,10 @@ LIB = os.path.join(HERE, "libamg_b200.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
-HOST_SRCS = ["api.cpp", "iga_gen.cpp", "setup.cpp", "dist.cpp"]
-CUDA_SRCS = ["device.cu", "inst_cheb.cu", "inst_cheb_dot.cu", "inst_spmv.cu", "inst_transfer.cu"]
-HEADERS = ["common.hpp", "kernels.cuh", "devstate.cuh", "launch_csr.cuh"]
+HOST_SRCS = ["api.cpp", "iga_gen.cpp", "setup.cpp", "dist.cpp", "share.cpp"]
+CUDA_SRCS = ["device.cu", "inst_cheb.cu", "inst_cheb_dot.cu", "inst_spmv.cu", "inst_transfer.cu",
+             "inst_vi_cheb.cu", "inst_vi_cheb_dot.cu", "inst_vi_spmv.cu", "inst_vi_transfer.cu"]
+HEADERS = ["common.hpp", "kernels.cuh", "devstate.cuh", "launch_csr.cuh", "launch_csr_vi.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -33,6 +33,12 @@ using namespace amgb;
     }
 
 namespace {
+int64_t replicate_nnz() {  // replicate levels below ~7e6 non-zeros
+    int64_t rep = 7000000;
+    if (const char *e = std::getenv("AMG_REPLICATE_NNZ")) rep = std::atoll(e);
+    return rep;
+}
+
 amg_csr *export_csr(const HCsr &A) {
     amg_csr *c = static_cast<amg_csr *>(std::calloc(1, sizeof(amg_csr)));
     if (!c) throw Error{AMG_ENOMEM, "host allocation failed"};
@@ -136,7 +142,7 @@ amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist 
     if (prm.agg_steps < 1 || prm.cheb_degree < 1 || prm.coarse_sweeps < 0 || prm.max_levels < 1 ||
         prm.coarse_size < 1 || !(prm.filter_theta >= 0.0) || prm.krylov < 0 || prm.krylov > 1 ||
         prm.coarse_solver < 0 || prm.coarse_solver > 1 || !(prm.coarse_tol >= 0.0) || prm.coarse_maxit < 0 ||
-        prm.format < 0 || prm.format > 5)
+        prm.format < 0 || prm.format > 6)
         throw Error{AMG_EINVAL, "bad parameter"};
     if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
         throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
@@ -144,12 +150,42 @@ amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist 
     try {
         build_hierarchy(*K, prm, H->host);
         if (dist && dist->nranks > 1) {
-            int64_t rep = 7000000;  // replicate levels below ~7e6 non-zeros
-            if (const char *e = std::getenv("AMG_REPLICATE_NNZ")) rep = std::atoll(e);
-            build_dist_plan(H->host, dist->rank, dist->nranks, rep, H->plan);
+            build_dist_plan(H->host, dist->rank, dist->nranks, replicate_nnz(), H->plan);
             H->distributed = true;
         }
         if (!prm.host_only) H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
+    } catch (...) {
+        delete H;
+        throw;
+    }
+    *Hout = H;
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_share_export(const amg_hierarchy *H, int rank, int nranks, void **share, int64_t *bytes) {
+    API_BEGIN
+    if (!H || !share || !bytes) throw Error{AMG_EINVAL, "NULL argument"};
+    uint8_t *p = nullptr;
+    share_export(H->host, rank, nranks, replicate_nnz(), &p, bytes);
+    *share = p;
+    return AMG_OK;
+    API_END
+}
+
+amg_status amg_setup_from_share(const void *share, int64_t bytes, const amg_dist *dist, int host_only,
+                                amg_hierarchy **Hout) {
+    API_BEGIN
+    if (!share || !Hout) throw Error{AMG_EINVAL, "NULL argument"};
+    if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+        throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
+    const int rank = dist ? dist->rank : 0, nranks = dist ? dist->nranks : 1;
+    amg_hierarchy *H = new amg_hierarchy();
+    try {
+        share_import(share, bytes, rank, nranks, H->host, H->plan);
+        H->host.prm.host_only = host_only ? 1 : 0;
+        H->distributed = nranks > 1;
+        if (!host_only) H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
     } catch (...) {
         delete H;
         throw;
@@ -174,11 +210,11 @@ amg_status amg_hierarchy_info(const amg_hierarchy *H, int64_t *n_levels, int64_t
     double tot = 0.0;
     for (int l = 0; l < h.nlevels; l++) {
         if (N) N[l] = h.lev[l].N;
-        if (nnz) nnz[l] = h.lev[l].K.nnz();
-        if (nnz_P) nnz_P[l] = (l + 1 < h.nlevels) ? h.lev[l].P.nnz() : 0;
-        tot += (double)h.lev[l].K.nnz();
+        if (nnz) nnz[l] = level_nnz_K(h, l);
+        if (nnz_P) nnz_P[l] = level_nnz_P(h, l);
+        tot += (double)level_nnz_K(h, l);
     }
-    if (opc) *opc = tot / (double)h.lev[0].K.nnz();
+    if (opc) *opc = tot / (double)level_nnz_K(h, 0);
     return AMG_OK;
     API_END
 }
@@ -187,6 +223,7 @@ amg_status amg_hierarchy_export(const amg_hierarchy *H, int level, amg_csr **K_l
                                 int32_t **aggregate_of, double **dhat, double *omega) {
     API_BEGIN
     if (!H || level < 0 || level >= H->host.nlevels) throw Error{AMG_EINVAL, "bad level"};
+    if (H->host.thin) throw Error{AMG_EINVAL, "a hierarchy built from a share holds only this rank's operators"};
     const HLevel &L = H->host.lev[level];
     const bool last = level == H->host.nlevels - 1;
     if (K_l) *K_l = export_csr(L.K);

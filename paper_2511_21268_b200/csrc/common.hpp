@@ -73,13 +73,21 @@ struct HLevel {
     Buf<double> ptent;   // composite tentative P value per row
     Buf<double> dhat;    // ℓ1 diagonal
     double omega = 0.0;
+    int64_t nnz_K = 0, nnz_P = 0;  // thin hierarchies only (K, P of distributed levels not held)
 };
 
 struct HHierarchy {
     amg_params prm{};
     int nlevels = 0;
+    bool thin = false;  // built from one rank's share (share.cpp): distributed levels held as LocalOps
     HLevel lev[32];
 };
+
+inline int64_t level_nnz_K(const HHierarchy &H, int l) { return H.thin ? H.lev[l].nnz_K : H.lev[l].K.nnz(); }
+inline int64_t level_nnz_P(const HHierarchy &H, int l) {
+    if (l + 1 >= H.nlevels) return 0;
+    return H.thin ? H.lev[l].nnz_P : H.lev[l].P.nnz();
+}
 
 // ---- multi-GPU plumbing (dist.cpp) ------------------------------------------------------------
 // One rank's share of a distributed operator: its rows [row_begin, row_end), columns renumbered in
@@ -113,6 +121,10 @@ struct DistPlan {
 // Row partition of every level balanced by nnz, the replication cut, and this rank's local
 // operators + halo plans.  Deterministic; identical on every rank given the same hierarchy.
 void build_dist_plan(const HHierarchy &H, int rank, int nranks, int64_t replicate_nnz, DistPlan &P);
+
+// share.cpp: one rank's share of a global host hierarchy as a malloc'd blob, and back (thin H + plan)
+void share_export(const HHierarchy &H, int rank, int nranks, int64_t replicate_nnz, uint8_t **blob, int64_t *bytes);
+void share_import(const void *blob, int64_t bytes, int rank, int nranks, HHierarchy &H, DistPlan &plan);
 
 // iga_gen.cpp
 void iga_tables_hat(int p, int n, double *mhat, double *khat);

@@ -7,7 +7,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <omp.h>
+
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cmath>
 #include <string>
@@ -95,7 +98,8 @@ inline int32_t pad_col(const HCsr &A, int64_t i, bool square) {
     return A.rp[i + 1] > A.rp[i] ? A.ci[A.rp[i]] : 0;
 }
 
-bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out);
+bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out, Buf<uint16_t> *keep);
+void encode_values(DevState &D, const double *v, int64_t stored, const uint16_t *off, DCsr &out);
 
 // Upload a host CSR as CSR2 (rows padded to a multiple of `mult` entries with (pad column, 0.0);
 // mult = 2 for format 1, 8 for the autotuned layouts: the TMA-staged core's bulk copies need 16-byte
@@ -142,12 +146,208 @@ void upload_csr2(DevState &D, const HCsr &A, DCsr &out, bool square, int mult = 
     CUDA_OK(cudaMemcpy(out.rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.ci, ci.data(), sizeof(int32_t) * nnz2, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.v, v.data(), sizeof(double) * nnz2, cudaMemcpyHostToDevice));
-    if (mult >= 4) encode_d16(D, rp.data(), ci.data(), n, out);
+    if (mult >= 4) {
+        Buf<uint16_t> off;
+        const bool d16 = encode_d16(D, rp.data(), ci.data(), n, out, &off);
+        if (mult >= 8) encode_values(D, v.data(), nnz2, d16 ? off.data() : nullptr, out);
+    }
+}
+
+// Open-addressing map of fp64 bit patterns -> uint64 (value dictionary of encode_values).
+struct BitsTable {
+    static constexpr uint64_t kEmpty = ~0ull;  // a NaN pattern: never a stored value (checked)
+    std::vector<uint64_t> key, val;
+    uint64_t mask = 0;
+    int64_t count = 0;
+    explicit BitsTable(int64_t cap) {
+        uint64_t sz = 16;
+        while (sz < (uint64_t)cap * 2) sz <<= 1;
+        key.assign(sz, kEmpty);
+        val.assign(sz, 0);
+        mask = sz - 1;
+    }
+    static uint64_t hash(uint64_t x) {
+        x ^= x >> 31;
+        x *= 0x7fb5d329728ea185ull;
+        x ^= x >> 27;
+        x *= 0x81dadef4bc2dd44dull;
+        return x ^ (x >> 33);
+    }
+    // slot of x, inserted (value 0) if absent; the table must keep a free slot
+    uint64_t insert(uint64_t x) {
+        uint64_t h = hash(x) & mask;
+        while (key[h] != kEmpty && key[h] != x) h = (h + 1) & mask;
+        if (key[h] == kEmpty) {
+            key[h] = x;
+            count++;
+        }
+        return h;
+    }
+    uint64_t find(uint64_t x) const {
+        uint64_t h = hash(x) & mask;
+        while (key[h] != x) h = (h + 1) & mask;
+        return h;
+    }
+};
+
+// Distinct-value dictionary of n fp64 values (plus +0.0 when with_zero: the padding value): the
+// distinct bit patterns ordered by decreasing frequency (ties: ascending bit pattern) into `tab`, and
+// each value's index into idx[0..n).  Frequency order puts the values of the interior stencil — most
+// of the entries — at the head of the table, so one warp's lookups touch few L1 lines.  Returns false
+// (nothing built) if there are more than `cap` distinct values.  Parallel: per-thread count maps, merged.
+bool value_dictionary(const double *v, int64_t n, bool with_zero, int64_t cap, std::vector<double> &tab,
+                      Buf<uint32_t> &idx) {
+    const int nt = omp_get_max_threads();
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> loc(nt);
+    bool ok = true;
+#pragma omp parallel num_threads(nt) reduction(&& : ok)
+    {
+        const int t = omp_get_thread_num(), T = omp_get_num_threads();
+        const int64_t k0 = n * t / T, k1 = n * (t + 1) / T;
+        BitsTable m(std::min<int64_t>(cap, 1 << 12));
+        for (int64_t k = k0; k < k1; k++) {
+            uint64_t x;
+            std::memcpy(&x, v + k, 8);
+            if (x == BitsTable::kEmpty || m.count > cap) { ok = false; break; }
+            m.val[m.insert(x)]++;
+            if (m.count * 2 > (int64_t)m.key.size()) {  // grow: load factor <= 1/2
+                BitsTable big(m.count * 2);
+                for (size_t h = 0; h < m.key.size(); h++)
+                    if (m.key[h] != BitsTable::kEmpty) big.val[big.insert(m.key[h])] = m.val[h];
+                m = std::move(big);
+            }
+        }
+        if (ok)
+            for (size_t h = 0; h < m.key.size(); h++)
+                if (m.key[h] != BitsTable::kEmpty) loc[t].push_back({m.key[h], m.val[h]});
+    }
+    if (!ok) return false;
+    std::vector<std::pair<uint64_t, uint64_t>> all;  // (bits, count)
+    if (with_zero) all.push_back({0ull, 0ull});
+    for (auto &l : loc) all.insert(all.end(), l.begin(), l.end());
+    std::sort(all.begin(), all.end());
+    size_t w = 0;
+    for (size_t i = 0; i < all.size(); i++) {
+        if (w > 0 && all[w - 1].first == all[i].first) all[w - 1].second += all[i].second;
+        else all[w++] = all[i];
+    }
+    all.resize(w);
+    const int64_t nv = (int64_t)all.size();
+    if (nv > cap) return false;
+    std::stable_sort(all.begin(), all.end(), [](const auto &a, const auto &b) { return a.second > b.second; });
+    BitsTable map(nv);
+    for (int64_t i = 0; i < nv; i++) map.val[map.insert(all[i].first)] = (uint64_t)i;
+    idx.alloc(n);
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < n; k++) {
+        uint64_t x;
+        std::memcpy(&x, v + k, 8);
+        idx[k] = (uint32_t)map.val[map.find(x)];
+    }
+    tab.resize(nv);
+    for (int64_t i = 0; i < nv; i++) std::memcpy(&tab[i], &all[i].first, 8);
+    return true;
+}
+
+// Value index (CSR-VI, kernels.cuh ColsD16V16 / ColsD16V32 / ColsI32V32) of an autotuned CSR operator:
+// the value dictionary of its stored entries (padding 0.0 included) and every stored entry's index;
+// plus the packed (16-bit offset | 16-bit value index) words when the operator has the 16-bit column
+// encoding and at most 65536 distinct values.  Built only where it can pay — at least 4 entries per
+// distinct value and at most 2^21 distinct values (a 16 MB table, L2 resident) — so the autotuner can
+// choose it; env AMG_VALUE_INDEX=0 disables it.  Lossless: the kernels read bitwise the stored values.
+void encode_values(DevState &D, const double *v, int64_t stored, const uint16_t *off, DCsr &out) {
+    if (stored < 2000000) return;  // below the autotuning threshold: never chosen
+    if (const char *e = std::getenv("AMG_VALUE_INDEX"))
+        if (std::atoi(e) == 0) return;
+    std::vector<double> tab;
+    Buf<uint32_t> idx;
+    if (!value_dictionary(v, stored, false, std::min<int64_t>(1 << 21, stored / 4), tab, idx)) return;
+    const int64_t nv = (int64_t)tab.size();
+    out.nvals = nv;
+    out.vtab = D.alloc_n<double>(nv);
+    out.vidx = D.alloc_n<uint32_t>(stored);
+    CUDA_OK(cudaMemcpy(out.vtab, tab.data(), 8 * (size_t)nv, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.vidx, idx.data(), 4 * (size_t)stored, cudaMemcpyHostToDevice));
+    if (off && nv <= 65536) {
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < stored; k++) idx[k] = (uint32_t)off[k] | (idx[k] << 16);
+        out.vpk = D.alloc_n<uint32_t>(stored);
+        CUDA_OK(cudaMemcpy(out.vpk, idx.data(), 4 * (size_t)stored, cudaMemcpyHostToDevice));
+    }
+}
+
+// SELL-VI layout (fmt 2; kernels.cuh k_sellvi) of a host CSR: 32-row slices of one 32-bit word per
+// entry (16-bit offset from the row's smallest column | 16-bit value index), column-major within the
+// slice.  Returns false (caller keeps CSR) unless every row spans < 65536 columns and the operator has
+// at most 65536 distinct values (+0.0 for the padding); `rule` additionally requires >= 2e6 non-zeros
+// and at most 25 % padding (the automatic choice of format 0).
+bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
+    const int64_t n = A.nrows, nsl = (n + 31) / 32, nnz = A.nnz();
+    if (n == 0 || nnz == 0) return false;
+    if (rule && nnz < 2000000) return false;
+    if (const char *e = std::getenv("AMG_SELLVI"))
+        if (std::atoi(e) == 0) return false;
+    Buf<int32_t> base(n);
+    bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+    for (int64_t i = 0; i < n; i++) {
+        const bool has = A.rp[i + 1] > A.rp[i];
+        const int32_t lo = has ? A.ci[A.rp[i]] : 0, hi = has ? A.ci[A.rp[i + 1] - 1] : 0;  // ascending columns
+        base[i] = lo;
+        ok = ok && ((int64_t)hi - (int64_t)lo <= 65535);
+    }
+    if (!ok) return false;
+    Buf<int64_t> soff(nsl + 1);
+    soff[0] = 0;
+    for (int64_t s = 0; s < nsl; s++) {
+        int64_t W = 0;
+        for (int64_t i = s * 32; i < std::min(n, s * 32 + 32); i++) W = std::max(W, A.rp[i + 1] - A.rp[i]);
+        soff[s + 1] = soff[s] + W;
+    }
+    const int64_t stored = soff[nsl] * 32;
+    if (rule && (double)stored > 1.25 * (double)nnz) return false;
+    std::vector<double> tab;
+    Buf<uint32_t> idx;
+    if (!value_dictionary(A.v.data(), nnz, true, 65536, tab, idx)) return false;
+    uint32_t zero = 0;
+    for (size_t t = 0; t < tab.size(); t++) {
+        uint64_t b;
+        std::memcpy(&b, &tab[t], 8);
+        if (b == 0) zero = (uint32_t)t;
+    }
+    Buf<uint32_t> w(stored);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < nsl; s++) {
+        const int64_t W = soff[s + 1] - soff[s];
+        for (int t = 0; t < 32; t++) {
+            const int64_t i = s * 32 + t;
+            const int64_t b = i < n ? A.rp[i] : 0, len = i < n ? A.rp[i + 1] - A.rp[i] : 0;
+            for (int64_t k = 0; k < W; k++) {
+                const int64_t dst = (soff[s] + k) * 32 + t;
+                w[dst] = k < len ? (uint32_t)(A.ci[b + k] - base[i]) | (idx[b + k] << 16) : zero << 16;
+            }
+        }
+    }
+    out.fmt = 2;
+    out.stored = stored;
+    out.G = 32;
+    out.U = 2;
+    out.kern = 0;
+    out.nvals = (int64_t)tab.size();
+    out.soff = D.alloc_n<int64_t>(nsl + 1);
+    out.vpk = D.alloc_n<uint32_t>(stored);
+    out.rbase = D.alloc_n<int32_t>(n);
+    out.vtab = D.alloc_n<double>(out.nvals);
+    CUDA_OK(cudaMemcpy(out.soff, soff.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.vpk, w.data(), sizeof(uint32_t) * stored, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.rbase, base.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(out.vtab, tab.data(), sizeof(double) * out.nvals, cudaMemcpyHostToDevice));
+    return true;
 }
 
 // 16-bit column offsets (ColsD16, kernels.cuh): base = the row's smallest stored column, offsets
 // col − base.  Returns false (no encoding; int32 columns only) if a row spans more than 65535 columns.
-bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out) {
+bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows, DCsr &out, Buf<uint16_t> *keep) {
     Buf<int32_t> base(nrows);
     bool ok = true;
 #pragma omp parallel for schedule(static) reduction(&& : ok)
@@ -171,8 +371,10 @@ bool encode_d16(DevState &D, const int64_t *rp, const int32_t *ci, int64_t nrows
     out.rbase = D.alloc_n<int32_t>(nrows);
     CUDA_OK(cudaMemcpy(out.off16, off.data(), sizeof(uint16_t) * stored, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.rbase, base.data(), sizeof(int32_t) * nrows, cudaMemcpyHostToDevice));
+    if (keep) *keep = std::move(off);
     return true;
 }
+
 
 // Slice offsets (in pairs) of the SELL2 layout; returns the stored entry count.
 int64_t sell2_offsets(const HCsr &A, Buf<int64_t> &soff) {
@@ -222,15 +424,17 @@ void upload_sell2(DevState &D, const HCsr &A, DCsr &out, bool square) {
 // Format choice (amg_params.format): 1 = CSR2 everywhere; 2 = SELL2 wherever allowed; 0 = auto.
 // Auto = CSR2: measured on B200 at C3 level 0, CSR2 streams at 4.55 TB/s vs SELL2's 4.10 TB/s
 // (profiles/r01), and SELL2 starves the GPU on the short coarse levels.
-void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, bool force_csr) {
+void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, bool force_csr, int role) {
     out.nrows = A.nrows;
     out.ncols = A.ncols;
     out.nnz = A.nnz();
+    // SELL-VI: format 0 by the fixed rule on the K_l, format 6 wherever admissible (never the coarsest K)
+    if (!force_csr && ((format == 0 && role == 0) || format == 6) && upload_sellvi(D, A, out, format == 0)) return;
     if (format == 0 || format >= 3) {
         // rows padded to 8 entries (16-byte aligned value, int32 and 16-bit column ranges): runnable by
         // both the register-batched CSR2 core and the TMA-staged CSR4T core (format 0 autotunes)
         upload_csr2(D, A, out, square, 8);
-        out.kern = (format == 3) ? 1 : (format == 4 && out.off16) ? 2 : (format == 5 && out.off16) ? 3 : 0;
+        out.kern = (format == 3) ? 1 : (format == 4 && out.off16) ? 2 : (format == 5 && out.off16) ? 3 : 0;  // 6: CSR fallback
         return;
     }
     const bool sell = !force_csr && format == 2;
@@ -283,7 +487,9 @@ bool tune_lookup(const TuneKey &k, DCsr &A) {
     bool hit = false;
     while (std::fscanf(f, "%d %d %d %d %lld %lld %d %d %d %d %f", &r, &nr, &l, &ro, &n, &z, &kern, &G, &U, &pf, &us) == 11) {
         if (r == k.rank && nr == k.nranks && l == k.level && ro == k.role && n == k.nrows && z == k.nnz) {
-            if ((kern & 2) && !A.off16) continue;  // stale entry for this operator's encodings
+            // kern 16 marks a SELL-VI entry; skip entries of another layout or for encodings this operator lacks
+            if ((kern == 16) != (A.fmt == 2) || ((kern & 2) && !A.off16) || ((kern & 8) && !A.vtab)) continue;
+            if (kern == 16) kern = 0;
             A.kern = kern;
             A.G = G;
             A.U = U;
@@ -300,13 +506,28 @@ void tune_store(const TuneKey &k, const DCsr &A) {
     if (!path) return;
     if (FILE *f = std::fopen(path, "a")) {
         std::fprintf(f, "%d %d %d %d %lld %lld %d %d %d %d %.2f\n", k.rank, k.nranks, k.level, k.role,
-                     (long long)k.nrows, (long long)k.nnz, A.kern, A.G, A.U, A.pf, A.tuned_us);
+                     (long long)k.nrows, (long long)k.nnz, A.fmt == 2 ? 16 : A.kern, A.G, A.U, A.pf, A.tuned_us);
         std::fclose(f);
     }
 }
 
+float time_role(DevState &D, DCsr &A, int role, double *x, double *y1, double *y2, double *y3, cudaEvent_t e0,
+                cudaEvent_t e1) {
+    if (role == 0) {
+        dev::EpiCheb<false> e{};
+        e.rin = y1; e.rout = y1; e.dold = x; e.dnew = y2; e.invd = y3;
+        e.xin = y3; e.dpend = nullptr; e.xout = y3; e.bdot = nullptr; e.a = 0.5; e.bc = 0.5;
+        return time_op(D, A, x, e, e0, e1);
+    } else if (role == 1) {
+        dev::EpiProlong e{y1};
+        return time_op(D, A, x, e, e0, e1);
+    }
+    dev::EpiRestrict e{y1, y3, y2, 1.0};
+    return time_op(D, A, x, e, e0, e1);
+}
+
 void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y1, double *y2, double *y3) {
-    if (A.fmt != 0 || A.nnz < 2000000) return;
+    if ((A.fmt != 0 && A.fmt != 2) || A.nnz < 2000000) return;
     if (std::getenv("AMG_CSR_G") || std::getenv("AMG_CSR_U")) return;
     if (const char *e = std::getenv("AMG_AUTOTUNE"))
         if (std::atoi(e) == 0) return;
@@ -315,12 +536,37 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
     cudaEvent_t e0, e1;
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
+    if (A.fmt == 2) {  // SELL-VI: entries in flight per lane (bitwise-equal results for every U)
+        float best = 1e30f;
+        int bu = A.U;
+        for (int U : {1, 2, 4}) {
+            A.U = U;
+            const float ms = time_role(D, A, role, x, y1, y2, y3, e0, e1);
+            if (ms < best) {
+                best = ms;
+                bu = U;
+            }
+        }
+        A.U = bu;
+        A.tuned_us = best / 3.f * 1000.f;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        D.launches_total = 0;
+        tune_store(key, A);
+        return;
+    }
     const int Gs[] = {1, 4, 8, 32};
     const int Us[] = {2, 4, 6, 8};
     float best = 1e30f;
     int bk = A.kern, bg = A.G, bu = A.U, bp = A.pf;
-    const int nkern = A.off16 ? 4 : 2;  // kern bit 1 (16-bit column offsets) needs the encoding
-    for (int kern = 0; kern < nkern; kern++)
+    // kern bit 1 (16-bit column offsets) needs the encoding, bit 3 (value index) the value table
+    std::vector<int> kerns = {0, 1};
+    if (A.off16) kerns.insert(kerns.end(), {2, 3});
+    if (A.vtab) {
+        kerns.push_back(8);
+        if (A.off16) kerns.push_back(10);
+    }
+    for (int kern : kerns)
         for (int G : Gs)
             for (int U : Us)
                 for (int pf = 0; pf < 2; pf++) {
@@ -331,19 +577,7 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
                 A.G = G;
                 A.U = U;
                 A.pf = pf;
-                float ms;
-                if (role == 0) {
-                    dev::EpiCheb<false> e{};
-                    e.rin = y1; e.rout = y1; e.dold = x; e.dnew = y2; e.invd = y3;
-                    e.xin = y3; e.dpend = nullptr; e.xout = y3; e.bdot = nullptr; e.a = 0.5; e.bc = 0.5;
-                    ms = time_op(D, A, x, e, e0, e1);
-                } else if (role == 1) {
-                    dev::EpiProlong e{y1};
-                    ms = time_op(D, A, x, e, e0, e1);
-                } else {
-                    dev::EpiRestrict e{y1, y3, y2, 1.0};
-                    ms = time_op(D, A, x, e, e0, e1);
-                }
+                const float ms = time_role(D, A, role, x, y1, y2, y3, e0, e1);
                 if (ms < best) {
                     best = ms;
                     bk = kern;
@@ -685,7 +919,8 @@ namespace {
 // Upload one rank's share of a distributed operator (local columns + halo plan).  Local columns keep
 // the global order (lower ghosts negative, dist.cpp); lo_shift / hi_shift move the lower / upper ghost
 // columns further out, past another gatherer's ghosts of the same vector (P̄_l's beyond K_{l+1}'s).
-void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int64_t lo_shift = 0, int64_t hi_shift = 0) {
+void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int role, int64_t lo_shift = 0,
+                  int64_t hi_shift = 0) {
     const int64_t nown = op.col_end - op.col_begin;
     if ((lo_shift > 0 || hi_shift > 0) && !op.full_cols && !op.ghost.empty()) {
         HCsr A;
@@ -701,9 +936,9 @@ void upload_local(DevState &D, const LocalOp &op, DCsr &out, int format, int64_t
             const int32_t c = op.A.ci[k];
             A.ci[k] = c < 0 ? (int32_t)(c - lo_shift) : c >= nown ? (int32_t)(c + hi_shift) : c;
         }
-        upload_op(D, A, out, false, format, false);
+        upload_op(D, A, out, false, format, false, role);
     } else {
-        upload_op(D, op.A, out, false, format, false);
+        upload_op(D, op.A, out, false, format, false, role);
     }
     if (op.full_cols || D.nranks == 1) return;
     out.halo = true;
@@ -778,7 +1013,7 @@ void build_push(DevState &D, const LocalOp &op, DCsr &A, const std::vector<int64
 // Row-group order of a CSR operator for its current G: boundary groups (any row reading a ghost value
 // or pushed somewhere) first, then the interior ones.
 void build_gorder(DevState &D, DCsr &A) {
-    if (A.bnd.empty() || A.fmt != 0) return;
+    if (A.bnd.empty() || (A.fmt != 0 && A.fmt != 2)) return;
     if (const char *e = std::getenv("AMG_P2P_INTERIOR"))  // 0: every kernel waits at its start (debug)
         if (std::atoi(e) == 0) return;
     const int64_t G = A.G, ng = (A.nrows + G - 1) / G;
@@ -946,6 +1181,16 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
     if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
         throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
     auto D = new DevState();
+    // env AMG_VERBOSE=1: setup phase times on stderr
+    const bool verbose = std::getenv("AMG_VERBOSE") && std::atoi(std::getenv("AMG_VERBOSE")) != 0;
+    auto t_start = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (!verbose) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[amg rank %d] %s %.3f s\n", dist ? dist->rank : 0, what,
+                     std::chrono::duration<double>(t - t_start).count());
+        t_start = t;
+    };
     try {
         int dev_id = 0;
         if (dist) {
@@ -1006,7 +1251,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             const HLevel &h = H.lev[l];
             DLevel &L = D->lev[l];
             L.N = h.N;
-            L.nnz = h.K.nnz();
+            L.nnz = level_nnz_K(H, l);
             const bool coarsest = (l + 1 == H.nlevels);
             L.replicated = nr > 1 && l > D->last_dist;
             int64_t r0 = 0;
@@ -1014,21 +1259,21 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                 const DistLevel &P = plan.lev[l];
                 r0 = P.K.row_begin;
                 L.n = P.K.row_end - P.K.row_begin;
-                upload_local(*D, P.K, L.K, fmt);
+                upload_local(*D, P.K, L.K, fmt, 0);
                 if (!coarsest) {
                     // P̄_l's ghosts of the coarse x lie beyond K_{l+1}'s on both sides
                     const LocalOp &Kc = plan.lev[l + 1].K;
                     const bool next_dist = !plan.lev[l + 1].replicated;
                     const int64_t klo = next_dist ? Kc.nlo : 0, khi = next_dist ? (int64_t)Kc.ghost.size() - Kc.nlo : 0;
-                    upload_local(*D, P.P, L.P, fmt, klo, khi);
-                    upload_local(*D, P.R, L.R, fmt);
+                    upload_local(*D, P.P, L.P, fmt, 1, klo, khi);
+                    upload_local(*D, P.R, L.R, fmt, 2);
                 }
             } else {
                 L.n = h.N;
-                upload_op(*D, h.K, L.K, true, fmt, coarsest);
+                upload_op(*D, h.K, L.K, true, fmt, coarsest, 0);
                 if (!coarsest) {
-                    upload_op(*D, h.P, L.P, false, fmt, false);
-                    upload_op(*D, h.R, L.R, false, fmt, false);
+                    upload_op(*D, h.P, L.P, false, fmt, false, 1);
+                    upload_op(*D, h.R, L.R, false, fmt, false, 2);
                 }
             }
             if (coarsest) {  // diag(K_L) for the §5.1 coarse CG (the coarsest level is whole on every rank)
@@ -1137,6 +1382,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         CUDA_OK(cudaMemset(D->counter, 0, 4 * sizeof(unsigned)));
         CUDA_OK(cudaMemset(D->S, 0, sizeof(dev::Scalars)));
         CUDA_OK(cudaMallocHost(&D->hS, sizeof(dev::Scalars)));
+        lap("upload");
         if (fmt == 0) {  // autotune every large operator on scratch vectors
             int64_t big = 1, lomax = 0;
             for (int l = 0; l < D->nlevels; l++)
@@ -1168,7 +1414,9 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         // format + 56 B/row of vectors (d_old, r in/out, x in/out, invd, d_new)
         D->bytes_dominant = D->lev[0].K.alg_bytes() + 56.0 * (double)n0;
         CUDA_OK(cudaDeviceSynchronize());
+        lap("autotune");
         if (want_p2p) p2p_setup(*D, plan);
+        lap("p2p_setup");
     } catch (...) {
         delete D;
         throw;
@@ -1445,10 +1693,14 @@ extern "C" amg_status amg_nccl_unique_id(unsigned char id[128]) {
 
 extern "C" amg_status amg_local_rows(amg_hierarchy *H, int64_t *row_begin, int64_t *row_end) {
     API_BEGIN
-    DevState *D = need_dev(H);
-    if (!row_begin || !row_end) throw Error{AMG_EINVAL, "NULL argument"};
-    *row_begin = D->row_begin0;
-    *row_end = D->row_end0;
+    if (!H || !row_begin || !row_end) throw Error{AMG_EINVAL, "NULL argument"};
+    if (H->distributed) {  // host plan (also for host_only setups)
+        *row_begin = H->plan.lev[0].K.row_begin;
+        *row_end = H->plan.lev[0].K.row_end;
+    } else {
+        *row_begin = 0;
+        *row_end = H->host.lev[0].N;
+    }
     return AMG_OK;
     API_END
 }
@@ -1502,14 +1754,28 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
     if (op > 0 && level == D->nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
     DLevel &L = D->lev[level];
     DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
+    if (A.fmt == 2) {  // SELL-VI: only U (entries in flight per lane) is free
+        if (kernel != 0 || G != 32 || !(U == 1 || U == 2 || U == 4))
+            throw Error{AMG_EINVAL, "SELL-VI operator: kernel 0, G 32 and U 1, 2 or 4"};
+        CUDA_OK(cudaDeviceSynchronize());
+        A.U = U;
+        A.tuned_us = 0.f;
+        for (auto &sg : D->seg)
+            if (sg.exec) {
+                cudaGraphExecDestroy(sg.exec);
+                sg.exec = nullptr;
+            }
+        return AMG_OK;
+    }
     if (A.fmt != 0) throw Error{AMG_EINVAL, "operator is not in a CSR layout"};
-    if (kernel < 0 || kernel > 7 || ((kernel & 2) && !A.off16) || ((kernel & 4) && ((kernel & 1) || A.mult < 8)))
+    if (kernel < 0 || kernel > 15 || ((kernel & 2) && !A.off16) || ((kernel & 4) && ((kernel & 1) || A.mult < 8)) ||
+        ((kernel & 8) && ((kernel & 1) || !A.vtab)))
         throw Error{AMG_EINVAL, "kernel not available for this operator"};
     if ((kernel & 1) && (A.mult < 8 || U > 4)) throw Error{AMG_EINVAL, "TMA core needs rows padded to 8 and U <= 4"};
     if (!(G == 1 || G == 4 || G == 8 || G == 32) || !(U == 2 || U == 4 || U == 6 || U == 8))
         throw Error{AMG_EINVAL, "G must be 1, 4, 8 or 32 and U 2, 4, 6 or 8"};
     CUDA_OK(cudaDeviceSynchronize());
-    A.kern = kernel & 3;
+    A.kern = kernel & 11;
     A.pf = (kernel >> 2) & 1;
     A.G = G;
     A.U = U;
@@ -1540,6 +1806,8 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     cfg->tuned_us = A.tuned_us;
     cfg->alg_bytes = A.alg_bytes();
     cfg->nnz = A.nnz;
+    cfg->n_values = A.nvals;
+    cfg->value_index_bytes = A.vtab ? ((A.vpk && (A.kern & 2)) ? 2 : 4) : 0;
     return AMG_OK;
     API_END
 }

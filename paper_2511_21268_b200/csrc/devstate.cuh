@@ -27,9 +27,11 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
-// A device operator in one of two streaming formats (kernels.cuh):
+// A device operator in one of three streaming formats (kernels.cuh):
 //   CSR2 (fmt 0): rows padded to even length; warp per group of G rows.
 //   SELL2 (fmt 1): 32-row slices, one row per lane, pair-interleaved columns; soff = slice offsets.
+//   SELL-VI (fmt 2): 32-row slices, one row per lane, one 32-bit word per entry (16-bit column offset
+//     from rbase | 16-bit value index into vtab); soff = slice offsets in 32-word columns; G = 32.
 struct DCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
     int fmt = 0;
@@ -41,17 +43,34 @@ struct DCsr {
     double *v = nullptr;
     int G = 32;    // CSR cores: rows per warp group
     int U = 4;     // CSR cores: pairs per lane per round trip (CSR2) / chunk of 32·U pairs (CSR4T)
-    // CSR layouts: kernel (bit 0: 0 register-batched k_csr2, 1 TMA-staged k_csr4t, needs 4-padding)
-    // and column source (bit 1: 0 int32 columns, 1 16-bit offsets from a per-row base, ColsD16)
+    // CSR layouts: kernel (bit 0: 0 register-batched k_csr2, 1 TMA-staged k_csr4t, needs 4-padding),
+    // column source (bit 1: 0 int32 columns, 1 16-bit offsets from a per-row base, ColsD16) and value
+    // source (bit 3: 0 streamed fp64 values, 1 value index into the distinct-value table; k_csr2 only)
     int kern = 0;
     // 16-bit column offsets (kern & 2): col − rbase[row] per stored entry, rbase = first column of the row
     uint16_t *off16 = nullptr;
     int32_t *rbase = nullptr;
-    // bytes one application must stream from HBM for this operator (values of the nnz stored entries,
-    // the column data of the chosen source, row pointers); vectors are counted by the caller
+    // value index (kern & 8, register core only; CSR-VI, kernels.cuh): vtab = the operator's distinct
+    // values (by decreasing frequency, nvals of them), vidx = per stored entry its index in vtab; vpk =
+    // per stored entry (16-bit column offset | value index << 16) when both fit 16 bits
+    double *vtab = nullptr;
+    int64_t nvals = 0;
+    uint32_t *vidx = nullptr;
+    uint32_t *vpk = nullptr;
+    // bytes one application must stream from HBM for this operator (values of the nnz stored entries
+    // or their value indices + the value table, the column data of the chosen source, row pointers);
+    // vectors are counted by the caller
     double alg_bytes() const {
-        const double idx = (kern & 2) ? 2.0 * (double)nnz + 4.0 * (double)nrows : 4.0 * (double)nnz;
-        return 8.0 * (double)nnz + idx + 8.0 * (double)(nrows + 1);
+        const double z = (double)nnz, rows = (double)nrows;
+        if (fmt == 2)  // SELL-VI: 4 B word per entry, the value table, row bases, slice offsets
+            return 4.0 * z + 8.0 * (double)nvals + 4.0 * rows + 8.0 * (double)((nrows + 31) / 32 + 1);
+        if (kern & 8) {
+            if ((kern & 2) && vpk) return 4.0 * z + 4.0 * rows + 8.0 * (double)nvals + 8.0 * (rows + 1);
+            const double cols = (kern & 2) ? 2.0 * z + 4.0 * rows : 4.0 * z;
+            return cols + 4.0 * z + 8.0 * (double)nvals + 8.0 * (rows + 1);
+        }
+        const double idx = (kern & 2) ? 2.0 * z + 4.0 * rows : 4.0 * z;
+        return 8.0 * z + idx + 8.0 * (rows + 1);
     }
     float tuned_us = 0.f;  // autotuned apply time (0 if not tuned)
     // halo plan (multi-GPU): ghost g (ascending global id) sits at slot lo_base + g of the gathered
@@ -173,7 +192,7 @@ inline dev::P2P p2p_of(const DevState &D, const DCsr &A) { return p2p_of(D, A.pa
 // that implement the group order — a plain kernel handed a group order would never publish.
 inline dev::P2P p2p_csr(const DevState &D, const DCsr &A) {
     dev::P2P p = p2p_of(D, A.part, A.wmask);
-    if (p.nranks > 0 && A.fmt == 0 && A.gorder && A.gorder_G == A.G) {
+    if (p.nranks > 0 && (A.fmt == 0 || A.fmt == 2) && A.gorder && A.gorder_G == A.G) {
         p.gorder = A.gorder;
         p.nbnd = A.nbnd;
     }

@@ -498,17 +498,24 @@ __device__ __forceinline__ double ld_gather(const double *p) {
     return r;
 }
 
-// Column sources of the CSR cores.  row(i) returns the per-row state, col(k, st, pol) the column of
-// stored entry k.  Every source yields the same columns, so the choice changes bytes and speed, never
-// results.  kStaged: the TMA core copies the column stream into shared memory with the values (int32
-// only); otherwise columns are read from global memory.
+// Entry sources of the CSR cores (the column and the value of stored entry k).  row(i) returns the
+// per-row state; the register core loads word(k) — the entry's streamed index data — for a whole batch
+// of entries first, then val(v, k, w) for the batch, then gathers x[col(w, row state)].  Every source
+// yields the same columns and bitwise the same values, so the choice changes bytes and speed, never
+// results.  kVals: the values are streamed from v (else val() looks them up in a value table).  The TMA
+// core stages the column stream (stream(k), kIdxBytes per entry) with the values into shared memory.
 //
 // ColsI32: plain int32 columns (4 B per entry), streamed like the values.
 struct ColsI32 {
     static constexpr int kIdxBytes = 4;  // bytes per entry of the staged column stream
+    static constexpr bool kVals = true;
+    using W = int;
     const int *ci;
     __device__ __forceinline__ int row(int64_t) const { return 0; }
-    __device__ __forceinline__ int col(int64_t k, int, uint64_t pol) const { return ld_stream(ci + k, pol); }
+    __device__ __forceinline__ W word(int64_t k, uint64_t pol) const { return ld_stream(ci + k, pol); }
+    __device__ __forceinline__ int col(W w, int) const { return w; }
+    __device__ __forceinline__ double val(const double *v, int64_t k, W, uint64_t pol) const { return ld_stream(v + k, pol); }
+    __device__ __forceinline__ void prefetch(int64_t b, int64_t e) const { prefetch_l2(ci + b, (uint32_t)((e - b) * 4)); }
     __device__ __forceinline__ const void *stream(int64_t k) const { return ci + k; }
     __device__ __forceinline__ int staged(const unsigned char *sidx, int j, int) const {
         return reinterpret_cast<const int *>(sidx)[j];
@@ -521,13 +528,84 @@ struct ColsI32 {
 // stream shrinks from 4 to 2 B per entry (12 → 10 B per non-zero with the value).
 struct ColsD16 {
     static constexpr int kIdxBytes = 2;
+    static constexpr bool kVals = true;
+    using W = unsigned;
     const unsigned short *off;
     const int *base;  // per row
     __device__ __forceinline__ int row(int64_t i) const { return __ldg(base + i); }
-    __device__ __forceinline__ int col(int64_t k, int b, uint64_t pol) const { return b + (int)ld_stream(off + k, pol); }
+    __device__ __forceinline__ W word(int64_t k, uint64_t pol) const { return ld_stream(off + k, pol); }
+    __device__ __forceinline__ int col(W w, int b) const { return b + (int)w; }
+    __device__ __forceinline__ double val(const double *v, int64_t k, W, uint64_t pol) const { return ld_stream(v + k, pol); }
+    __device__ __forceinline__ void prefetch(int64_t b, int64_t e) const { prefetch_l2(off + b, (uint32_t)((e - b) * 2)); }
     __device__ __forceinline__ const void *stream(int64_t k) const { return off + k; }
     __device__ __forceinline__ int staged(const unsigned char *sidx, int j, int b) const {
         return b + (int)reinterpret_cast<const unsigned short *>(sidx)[j];
+    }
+};
+
+// Value-indexed sources ("CSR-VI": Kourtis, Goumas, Koziris, "Optimizing sparse matrix-vector
+// multiplication using index and value compression", CF 2008).  An operator with few distinct values
+// stores each entry's value as an index into a table of its distinct values (most frequent first,
+// built on the host); the value read is an L1-resident table lookup instead of 8 streamed bytes.  The
+// IgA operators are full of repeated values (C3: K_0 has 306 M entries but 1,053 distinct values, K_1
+// 190 K) because every interior row is the same stencil.  Values are bitwise the stored ones (a
+// lossless format), so row sums are bitwise those of the streamed-value sources.  Tail entries beyond a
+// row's end (k >= e) are never looked up.
+//
+// ColsD16V16: one 32-bit word per entry: low half the 16-bit column offset (as ColsD16), high half the
+// value index (< 65536 distinct values): 4 B per entry instead of 10.
+struct ColsD16V16 {
+    static constexpr int kIdxBytes = 4;
+    static constexpr bool kVals = false;
+    using W = unsigned;
+    const unsigned *w;
+    const int *base;      // per row
+    const double *table;  // distinct values
+    __device__ __forceinline__ int row(int64_t i) const { return __ldg(base + i); }
+    __device__ __forceinline__ W word(int64_t k, uint64_t pol) const { return ld_stream(w + k, pol); }
+    __device__ __forceinline__ int col(W x, int b) const { return b + (int)(x & 0xffffu); }
+    __device__ __forceinline__ double val(const double *, int64_t, W x, uint64_t) const { return ld_gather(table + (x >> 16)); }
+    __device__ __forceinline__ void prefetch(int64_t b, int64_t e) const { prefetch_l2(w + b, (uint32_t)((e - b) * 4)); }
+};
+
+// ColsD16V32: 16-bit column offsets + a 32-bit value index per entry (6 B per entry instead of 10).
+struct ColsD16V32 {
+    static constexpr int kIdxBytes = 6;
+    static constexpr bool kVals = false;
+    using W = uint2;
+    const unsigned short *off;
+    const unsigned *vi;
+    const int *base;
+    const double *table;
+    __device__ __forceinline__ int row(int64_t i) const { return __ldg(base + i); }
+    __device__ __forceinline__ W word(int64_t k, uint64_t pol) const {
+        return make_uint2(ld_stream(off + k, pol), ld_stream(vi + k, pol));
+    }
+    __device__ __forceinline__ int col(W x, int b) const { return b + (int)x.x; }
+    __device__ __forceinline__ double val(const double *, int64_t, W x, uint64_t) const { return ld_gather(table + x.y); }
+    __device__ __forceinline__ void prefetch(int64_t b, int64_t e) const {
+        prefetch_l2(off + b, (uint32_t)((e - b) * 2));
+        prefetch_l2(vi + b, (uint32_t)((e - b) * 4));
+    }
+};
+
+// ColsI32V32: int32 columns + a 32-bit value index (8 B per entry instead of 12).
+struct ColsI32V32 {
+    static constexpr int kIdxBytes = 8;
+    static constexpr bool kVals = false;
+    using W = uint2;
+    const int *ci;
+    const unsigned *vi;
+    const double *table;
+    __device__ __forceinline__ int row(int64_t) const { return 0; }
+    __device__ __forceinline__ W word(int64_t k, uint64_t pol) const {
+        return make_uint2((unsigned)ld_stream(ci + k, pol), ld_stream(vi + k, pol));
+    }
+    __device__ __forceinline__ int col(W x, int) const { return (int)x.x; }
+    __device__ __forceinline__ double val(const double *, int64_t, W x, uint64_t) const { return ld_gather(table + x.y); }
+    __device__ __forceinline__ void prefetch(int64_t b, int64_t e) const {
+        prefetch_l2(ci + b, (uint32_t)((e - b) * 4));
+        prefetch_l2(vi + b, (uint32_t)((e - b) * 4));
     }
 };
 
@@ -579,34 +657,36 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
             const int rs = __shfl_sync(0xffffffffu, grs, t);
             if (pf && t + 1 < nr) {
                 const int64_t nb = __shfl_sync(0xffffffffu, gb, t + 1), ne = __shfl_sync(0xffffffffu, ge, t + 1);
-                if (lane == 0 && ne > nb && ((nb * Cols::kIdxBytes) & 15) == 0 && (((ne - nb) * Cols::kIdxBytes) & 15) == 0) {
-                    prefetch_l2(v + nb, (uint32_t)((ne - nb) * 8));
-                    prefetch_l2(cols.stream(nb), (uint32_t)((ne - nb) * Cols::kIdxBytes));
+                // rows are padded to 8 entries: every stream's range is 16-byte aligned
+                if (lane == 0 && ne > nb && (nb & 7) == 0 && ((ne - nb) & 7) == 0) {
+                    if constexpr (Cols::kVals) prefetch_l2(v + nb, (uint32_t)((ne - nb) * 8));
+                    cols.prefetch(nb, ne);
                 }
             }
             double s0 = 0.0, s1 = 0.0;
             for (int64_t k0 = b + lane; k0 < e; k0 += 64 * U) {
                 double va[U], vb[U];
-                int ca[U], cb[U];
+                typename Cols::W wa[U], wb[U];
                 // past the row end: column 0 (always a valid index) with value 0.0 — no sentinel, since
                 // distributed operators have negative (lower-ghost) columns
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int64_t ka = k0 + 64 * u, kb = ka + 32;
-                    ca[u] = ka < e ? cols.col(ka, rs, pol) : 0;
-                    cb[u] = kb < e ? cols.col(kb, rs, pol) : 0;
+                    if (ka < e) wa[u] = cols.word(ka, pol);
+                    if (kb < e) wb[u] = cols.word(kb, pol);
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int64_t ka = k0 + 64 * u, kb = ka + 32;
-                    va[u] = ka < e ? ld_stream(v + ka, pol) : 0.0;
-                    vb[u] = kb < e ? ld_stream(v + kb, pol) : 0.0;
+                    va[u] = ka < e ? cols.val(v, ka, wa[u], pol) : 0.0;
+                    vb[u] = kb < e ? cols.val(v, kb, wb[u], pol) : 0.0;
                 }
                 double xa[U], xb[U];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    xa[u] = ld_gather(g + ca[u]);
-                    xb[u] = ld_gather(g + cb[u]);
+                    const int64_t ka = k0 + 64 * u, kb = ka + 32;
+                    xa[u] = ld_gather(g + (ka < e ? cols.col(wa[u], rs) : 0));
+                    xb[u] = ld_gather(g + (kb < e ? cols.col(wb[u], rs) : 0));
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
@@ -874,6 +954,85 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
         }
         if (row < nrows) acc_add(dacc, epi(row, (acc[0] + acc[1]) + (acc[2] + acc[3]), pre));
     }
+    if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+    peer_signal(pp);
+}
+
+// ------------------------------------------------------------------------------------------------
+// SELL-VI core (layout 2): 32-row slices, ONE ROW PER LANE, one 32-bit word per stored entry = 16-bit
+// column offset from the row's smallest column | 16-bit index into the operator's distinct-value table
+// (CSR-VI above).  Slice s stores W_s = (its longest row) columns of 32 words; word k of lane t is
+// entry k of row 32s+t (padding: offset 0, the index of 0.0).
+//
+// Why row per lane on the IgA operators: lane t and lane t+1 hold rows i and i+1, x-neighbours, so
+// entry k of the 32 rows is one stencil position at 32 consecutive columns — the x-gather of one warp
+// instruction is 256 contiguous bytes (2–3 L1 wavefronts instead of ≈ 6 for a row per warp), and the
+// 32 rows of an interior slice have the SAME value at entry k — the table lookup is one broadcast.
+// Together with the 4 B streamed per entry this moves the fine-level operator from 10 B/entry at ≈ 9
+// L1 wavefronts per 32 entries (CSR-D16) to 4 B at ≈ 5.
+//
+// Summation order: entry k of a row goes to chain k & 1, each chain accumulates in increasing k, the
+// row sum is chain0 + chain1 — independent of U (entries in flight per lane), so every U gives
+// bitwise-equal results.  (Not the CSR cores' order: the layout is chosen per operator by a fixed rule at
+// setup, never by timing, so results do not depend on the autotuner.)  Slices are visited in
+// the boundary-first order of 32-row groups on P2P runs, with the same early publication as k_csr2.
+// ------------------------------------------------------------------------------------------------
+template <int U, class Epi>
+__global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ soff, const unsigned *__restrict__ w,
+                                                   const int *__restrict__ rbase, const double *__restrict__ table,
+                                                   const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc,
+                                                   P2P pp) {
+    if (!pp.gorder) peer_wait(pp);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t nslices = (nrows + 31) >> 5;
+    const uint64_t pol = stream_policy();
+    typename Epi::Acc dacc{};
+    bool signalled = pp.gorder == nullptr || pp.nranks == 0;
+    if (!signalled && warp < pp.nbnd) peer_wait_warp(pp);
+    for (int64_t pos = warp; pos < nslices; pos += nwarps) {
+        if (!signalled && pos >= pp.nbnd) {
+            peer_signal_warp(pp);
+            signalled = true;
+        }
+        const int64_t sl = pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos;
+        const int64_t off = __ldg(soff + sl);
+        const int W = (int)(__ldg(soff + sl + 1) - off);
+        const int64_t row = (sl << 5) + lane;
+        typename Epi::Pre pre{};
+        int b = 0;
+        if (row < nrows) {
+            b = __ldg(rbase + row);
+            pre = epi.load(row);
+        }
+        const unsigned *wp = w + (off << 5) + lane;
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 2 * U <= W; k += 2 * U) {
+            unsigned wa[2 * U];
+#pragma unroll
+            for (int u = 0; u < 2 * U; u++) wa[u] = ld_stream(wp + (int64_t)(k + u) * 32, pol);
+            double va[2 * U], xa[2 * U];
+#pragma unroll
+            for (int u = 0; u < 2 * U; u++) va[u] = ld_gather(table + (wa[u] >> 16));
+#pragma unroll
+            for (int u = 0; u < 2 * U; u++) xa[u] = ld_gather(g + (b + (int)(wa[u] & 0xffffu)));
+#pragma unroll
+            for (int u = 0; u < 2 * U; u += 2) {
+                s0 = fma(va[u], xa[u], s0);
+                s1 = fma(va[u + 1], xa[u + 1], s1);
+            }
+        }
+        for (; k < W; k++) {
+            const unsigned x = ld_stream(wp + (int64_t)k * 32, pol);
+            const double p = ld_gather(table + (x >> 16)), xv = ld_gather(g + (b + (int)(x & 0xffffu)));
+            if (k & 1) s1 = fma(p, xv, s1);
+            else s0 = fma(p, xv, s0);
+        }
+        if (row < nrows) acc_add(dacc, epi(row, s0 + s1, pre));
+    }
+    if (!signalled) peer_signal_warp(pp);
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
     peer_signal(pp);
 }

@@ -49,11 +49,18 @@ template <class Epi, class Cols>
 void launch_csr_cols(DevState &D, const DCsr &A, const Cols &cols, const double *g, Epi epi, cudaStream_t st,
                      int dotkind) {
     const bool tma = (A.kern & 1) != 0;
+    if constexpr (!Cols::kVals) {  // value-indexed sources: register core only
+        if (tma) throw Error{AMG_EINVAL, "the TMA core has no value-indexed source"};
+    }
     switch (A.G * 16 + A.U) {
-#define CASE(GG, UU)                                                                  \
-    case GG * 16 + UU:                                                                \
-        if (tma) launch_csr4t_gu<GG, UU, Epi, Cols>(D, A, cols, g, epi, st, dotkind); \
-        else launch_csr2_gu<GG, UU, Epi, Cols>(D, A, cols, g, epi, st, dotkind);      \
+#define CASE(GG, UU)                                                                            \
+    case GG * 16 + UU:                                                                          \
+        if constexpr (Cols::kVals) {                                                            \
+            if (tma) launch_csr4t_gu<GG, UU, Epi, Cols>(D, A, cols, g, epi, st, dotkind);       \
+            else launch_csr2_gu<GG, UU, Epi, Cols>(D, A, cols, g, epi, st, dotkind);            \
+        } else {                                                                                \
+            launch_csr2_gu<GG, UU, Epi, Cols>(D, A, cols, g, epi, st, dotkind);                 \
+        }                                                                                       \
         break;
 #define CASES_G(GG) CASE(GG, 2) CASE(GG, 4) CASE(GG, 6) CASE(GG, 8)
         CASES_G(1) CASES_G(4) CASES_G(8) CASES_G(32)
@@ -63,9 +70,18 @@ void launch_csr_cols(DevState &D, const DCsr &A, const Cols &cols, const double 
     }
 }
 
+// Value-indexed sources (kern bit 3): defined in launch_csr_vi.cuh, compiled in their own translation
+// units (inst_vi_*.cu) in parallel with the streamed-value ones.
+template <class Epi>
+void launch_csr_vi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind);
+template <class Epi>
+void launch_sellvi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind);
+
 template <class Epi>
 void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
-    if (A.fmt == 1) {
+    if (A.fmt == 2) {
+        launch_sellvi(D, A, g, epi, st, dotkind);  // instantiated in inst_vi_*.cu
+    } else if (A.fmt == 1) {
         const int2 *ci2 = reinterpret_cast<const int2 *>(A.ci);
         const double2 *v2 = reinterpret_cast<const double2 *>(A.v);
         const int64_t nsl = (A.nrows + 31) / 32;
@@ -78,6 +94,8 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
         dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind),
                                                          (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));
+    } else if (A.kern & 8) {
+        launch_csr_vi(D, A, g, epi, st, dotkind);  // instantiated in inst_vi_*.cu
     } else if (A.kern & 2) {
         launch_csr_cols(D, A, dev::ColsD16{reinterpret_cast<const unsigned short *>(A.off16), A.rbase}, g, epi, st, dotkind);
     } else {

@@ -1,0 +1,42 @@
+// launch_csr_vi.cuh — the value-indexed CSR launchers (kern bit 3; CSR-VI sources of kernels.cuh),
+// included only by the inst_vi_*.cu files.
+#pragma once
+#include "launch_csr.cuh"
+
+namespace amgb {
+
+template <class Epi>
+void launch_csr_vi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    if (!A.vtab || !A.vidx) throw Error{AMG_EINVAL, "operator has no value index"};
+    const unsigned short *off = reinterpret_cast<const unsigned short *>(A.off16);
+    if ((A.kern & 2) && A.vpk) launch_csr_cols(D, A, dev::ColsD16V16{A.vpk, A.rbase, A.vtab}, g, epi, st, dotkind);
+    else if (A.kern & 2) launch_csr_cols(D, A, dev::ColsD16V32{off, A.vidx, A.rbase, A.vtab}, g, epi, st, dotkind);
+    else launch_csr_cols(D, A, dev::ColsI32V32{A.ci, A.vidx, A.vtab}, g, epi, st, dotkind);
+}
+
+template <int U, class Epi>
+void launch_sellvi_u(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    const int64_t nsl = (A.nrows + 31) / 32;
+    const int64_t wpb = dev::kBlock / 32;
+    static int per_sm = 0;  // resident CTAs per SM of this instantiation
+    if (!per_sm) {
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sellvi<U, Epi>, dev::kBlock, 0));
+        per_sm = std::max(per_sm, 1);
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
+    dev::k_sellvi<U, Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, A.vpk, A.rbase, A.vtab, g, A.nrows, epi,
+                                                        dotctx(D, dotkind),
+                                                        (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
+}
+
+template <class Epi>
+void launch_sellvi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    switch (A.U) {
+        case 1: launch_sellvi_u<1, Epi>(D, A, g, epi, st, dotkind); break;
+        case 2: launch_sellvi_u<2, Epi>(D, A, g, epi, st, dotkind); break;
+        case 4: launch_sellvi_u<4, Epi>(D, A, g, epi, st, dotkind); break;
+        default: throw Error{AMG_EINVAL, "bad SELL-VI configuration (U must be 1, 2 or 4)"};
+    }
+}
+
+}  // namespace amgb

@@ -129,3 +129,126 @@ def test_partition_and_halo_plans_world2(case, rep_nnz):
     for rank, status, detail in res:
         assert status == "ok", detail
         assert detail >= 3  # at least K_0, P̄_0, R_0 were distributed and checked
+
+
+# ---- shared setup: one host hierarchy, one share per rank (amg_share_export / amg_setup_from_share) ----
+
+def _views(H, levels):
+    out = {}
+    for l in range(levels):
+        for op in range(3 if l + 1 < levels else 1):
+            v = H.dist_view(l, op)
+            if v["replicated"]:
+                out[(l, op)] = "replicated"
+                continue
+            loc = v.pop("local")
+            v = {k: (np.asarray(x).copy() if isinstance(x, np.ndarray) else x) for k, x in v.items()}
+            v["local"] = (loc.indptr.copy(), loc.indices.copy(), loc.data.view(np.uint64).copy())
+            out[(l, op)] = v
+    return out
+
+
+def _same(a, b):
+    assert a.keys() == b.keys()
+    for key in a:
+        va, vb = a[key], b[key]
+        if isinstance(va, str) or isinstance(vb, str):
+            assert va == vb, key
+            continue
+        assert va.keys() == vb.keys(), key
+        for f in va:
+            if f == "local":
+                assert all(np.array_equal(x, y) for x, y in zip(va[f], vb[f])), (key, f)
+            else:
+                assert np.array_equal(np.asarray(va[f]), np.asarray(vb[f])), (key, f)
+
+
+@pytest.mark.parametrize("case,world,rep_nnz", [((3, 2, 12), 2, 1000), ((3, 3, 10), 3, 20000),
+                                                ((2, 2, 16), 4, 100)])
+def test_share_equals_per_rank_setup(case, world, rep_nnz, monkeypatch):
+    """A rank's hierarchy rebuilt from its share has exactly the plan, local operators (bitwise values)
+    and sizes that amg_setup with that rank's amg_dist builds from the full K."""
+    monkeypatch.setenv("AMG_REPLICATE_NNZ", str(rep_nnz))
+    import paper_2511_21268_b200 as amg
+    dim, p, n = case
+    K, _ = amg.iga_poisson(dim, p, n)
+    G = amg.Hierarchy(K, amg.params(p, host_only=1))
+    for r in range(world):
+        d = amg.make_dist(r, world, nccl_id=bytes(128))
+        ref = amg.Hierarchy(K, amg.params(p, host_only=1), dist=d)
+        sh = G.export_share(r, world)
+        H = amg.Hierarchy.from_share(sh, d, host_only=True)
+        sh.close()
+        assert H.info() == ref.info() == G.info()
+        assert H.local_rows() == ref.local_rows()
+        L = ref.info()["levels"]
+        _same(_views(H, L), _views(ref, L))
+        with pytest.raises(amg.AmgError):
+            H.export(0)  # the global operators are not held
+        with pytest.raises(amg.AmgError):
+            H.export_share(0, world)
+
+
+def test_share_rejects_wrong_rank_and_corruption():
+    import paper_2511_21268_b200 as amg
+    K, _ = amg.iga_poisson(2, 2, 8)
+    G = amg.Hierarchy(K, amg.params(2, host_only=1))
+    sh = G.export_share(1, 2)
+    blob = sh.array.copy()
+    sh.close()
+    with pytest.raises(amg.AmgError):
+        amg.Hierarchy.from_share(blob, amg.make_dist(0, 2, nccl_id=bytes(128)), host_only=True)
+    with pytest.raises(amg.AmgError):
+        amg.Hierarchy.from_share(blob[:-9], amg.make_dist(1, 2, nccl_id=bytes(128)), host_only=True)
+    bad = blob.copy()
+    bad[0] ^= 1
+    with pytest.raises(amg.AmgError):
+        amg.Hierarchy.from_share(bad, amg.make_dist(1, 2, nccl_id=bytes(128)), host_only=True)
+    with pytest.raises(amg.AmgError):
+        G.export_share(2, 2)
+    # one rank: the whole hierarchy, every level "replicated"
+    sh1 = G.export_share(0, 1)
+    H1 = amg.Hierarchy.from_share(sh1, None, host_only=True)
+    assert H1.info() == G.info()
+
+
+def _share_worker(rank, world, port, case, rep_nnz, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        os.environ["AMG_REPLICATE_NNZ"] = str(rep_nnz)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2511_21268_b200 as amg
+        dim, p, n = case
+        K, _ = amg.iga_poisson(dim, p, n)
+        prm = amg.params(p, host_only=1)
+        # small chunks: the blob crosses several sends
+        H = amg.setup_distributed(K if rank == 0 else None, prm, rank, world, nccl_id=bytes(128),
+                                  host_only=True, group=dist.group.WORLD, chunk_bytes=4096)
+        ref = amg.Hierarchy(K, prm, dist=amg.make_dist(rank, world, nccl_id=bytes(128)))
+        assert H.info() == ref.info()
+        L = ref.info()["levels"]
+        _same(_views(H, L), _views(ref, L))
+        dist.barrier()
+        q.put((rank, "ok", L))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_setup_distributed_world2():
+    """setup_distributed over gloo: rank 0 builds once and ships rank 1 its share in chunks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_worker, args=(r, 2, port, (3, 2, 12), 1000, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, status, detail in res:
+        assert status == "ok", detail

@@ -26,7 +26,7 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg"):
+def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg", fmt=0):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -40,6 +40,8 @@ def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg"):
         paper = solver == "fcg"  # the paper's own experiment: its data, FCG, §5.1 coarse CG
         K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
         kw = dict(krylov=1, coarse_solver=1) if paper else {}
+        if fmt:
+            kw["format"] = fmt
         H = amg.Hierarchy(K, amg.params(p, **kw), dist=amg.make_dist(rank, world, device=rank))
         b, e = H.local_rows()
         out = {}
@@ -120,6 +122,38 @@ def test_distributed_solve_matches_single_gpu(world, case, rep_nnz, transport):
 
 
 @pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_distributed_sellvi(transport):
+    """Format 6 (SELL-VI operators on every level that admits them, row per lane): the distributed
+    solve (boundary-first slice order and early publication with P2P) matches the single-GPU one."""
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (3, 2, 32), 200000, transport, q, "pcg", 6))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, out, ref, N = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert status == "ok", out
+    zv = np.zeros(N)
+    for b, e, zl in out["vcycle"]:
+        zv[b:e] = zl
+    assert np.abs(zv - ref["vcycle"]).max() <= 1e-12 * np.abs(ref["vcycle"]).max()
+    for name in ("sine", "random"):
+        it, st, hist, parts = out[name]
+        it1, u1, u1_8, hist1 = ref[name]
+        assert st == 0 and abs(it - it1) <= 1, (name, it, it1)
+        u8 = np.zeros(N)
+        for b, e, ul, ul8 in parts:
+            u8[b:e] = ul8
+        assert np.linalg.norm(u8 - u1_8) <= 1e-10 * np.linalg.norm(u1_8)
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
 def test_distributed_paper_experiment(transport):
     """The paper's configuration (its cube data, FCG outer, §5.1 coarse CG on the replicated coarsest
     level) at 2 GPUs vs 1 GPU."""
@@ -140,3 +174,58 @@ def test_distributed_paper_experiment(transport):
     it, st, hist, parts = out["sine"]
     it1 = ref["sine"][0]
     assert st == 0 and abs(it - it1) <= 1
+
+
+def _share_worker(rank, world, port, case, rep_nnz, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        os.environ["AMG_REPLICATE_NNZ"] = str(rep_nnz)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+        import paper_2511_21268_b200 as amg
+        import amg_inputs
+        dim, p, n = case
+        K, F = amg.iga_poisson(dim, p, n)
+        prm = amg.params(p)
+        Hs = amg.setup_distributed(K if rank == 0 else None, prm, rank, world, device=rank)
+        Hr = amg.Hierarchy(K, prm, dist=amg.make_dist(rank, world, device=rank))
+        assert Hs.local_rows() == Hr.local_rows() and Hs.info() == Hr.info()
+        b, e = Hs.local_rows()
+        Fl = torch.from_numpy(np.ascontiguousarray(F[b:e])).cuda()
+        us, its, _, hs, sts = Hs.solve(Fl, rtol=1e-6)
+        ur, itr, _, hr, str_ = Hr.solve(Fl, rtol=1e-6)
+        rv = torch.from_numpy(np.ascontiguousarray(amg_inputs.uniform_pm1(K.shape[0], seed=5)[b:e])).cuda()
+        zs, zr = Hs.vcycle(rv), Hr.vcycle(rv)
+        ok = (sts == str_ == 0 and its == itr and torch.equal(us, ur) and torch.equal(zs, zr)
+              and list(hs) == list(hr))
+        flags = [None] * world
+        dist.all_gather_object(flags, (rank, ok, its, itr))
+        if rank == 0:
+            q.put(("ok", flags))
+        dist.barrier()
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_shared_setup_solve_bitwise():
+    """setup_distributed (one host setup on rank 0, shares shipped over gloo) gives every rank the
+    device state of the per-rank global setup: the solve and the V-cycle are bitwise identical."""
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_worker, args=(r, world, port, (3, 2, 32), 200000, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, flags = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert status == "ok", flags
+    assert all(f[1] for f in flags), flags

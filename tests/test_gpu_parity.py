@@ -39,8 +39,8 @@ _cache = {}
 
 
 # 1 CSR2 (warp per row group), 2 SELL2 (row per lane), 3 CSR4T (TMA-staged rows),
-# 4 CSR2 with 16-bit column offsets, 5 CSR4T with 16-bit column offsets
-FORMATS = [1, 2, 3, 4, 5]
+# 4 CSR2 with 16-bit column offsets, 5 CSR4T with 16-bit column offsets, 6 SELL-VI wherever admissible
+FORMATS = [1, 2, 3, 4, 5, 6]
 
 
 def build(case, fmt=0, **kw):
@@ -89,7 +89,22 @@ def test_kernel_configs_bitwise_equal(case):
             keep = H.op_config(l, op)
             x = dev(rng.uniform(-1, 1, A.shape[1]))
             ref = None
-            for kern in (0, 1, 2, 3, 4, 6):  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch
+            if keep["layout"] == "sellvi":  # SELL-VI: every U sums in the same order
+                ys = []
+                for U in (1, 2, 4):
+                    H.set_op_config(l, op, 0, 32, U)
+                    y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+                    H.apply(l, op, x, y)
+                    ys.append(y.cpu().numpy())
+                xo = x.cpu().numpy()
+                assert np.all(np.abs(ys[0] - oracle.spmv(A, xo)) <= 1e-13 * (abs(A) @ np.abs(xo)) + 1e-300)
+                assert all(np.array_equal(y, ys[0]) for y in ys)
+                H.set_op_config(l, op, 0, 32, keep["U"])
+                continue
+            kerns = [0, 1, 2, 3, 4, 6]  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch
+            if keep["n_values"]:  # bit 3: value index (CSR-VI), register core
+                kerns += [8, 10, 12, 14]
+            for kern in kerns:
                 for G in (1, 4, 8, 32):
                     for U in (2, 4, 6, 8):
                         if (kern & 1) and U > 4:
@@ -105,8 +120,7 @@ def test_kernel_configs_bitwise_equal(case):
                             assert np.all(np.abs(y - oracle.spmv(A, xo)) <= 1e-13 * bound + 1e-300)
                         else:
                             assert np.array_equal(y, ref), (l, op, kern, G, U)
-            kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")
-            H.set_op_config(l, op, kinds.index(keep["kernel"]), keep["G"], keep["U"])
+            H.set_op_config(l, op, keep["kernel_bits"], keep["G"], keep["U"])
 
 
 def test_d16_encoding_bytes():
@@ -118,11 +132,72 @@ def test_d16_encoding_bytes():
     d16 = H.op_config(0, 0)
     H.set_op_config(0, 0, 0, c["G"], c["U"])
     i32 = H.op_config(0, 0)["alg_bytes"]
-    kinds = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")
-    H.set_op_config(0, 0, kinds.index(c["kernel"]), c["G"], c["U"])
+    H.set_op_config(0, 0, c["kernel_bits"], c["G"], c["U"])
     nnz, N = c["nnz"], K.shape[0]
     assert i32 == 12 * nnz + 8 * (N + 1)
     assert d16["alg_bytes"] == 10 * nnz + 4 * N + 8 * (N + 1)
+
+
+def test_sellvi_layout():
+    """SELL-VI (format 6; format 0 picks it for the large K_l): row per lane, one 32-bit word per entry
+    (16-bit column offset | 16-bit value index).  The table holds exactly the distinct values (+0.0 of
+    the padding), the reported bytes are 4 B per non-zero + the table + row bases + slice offsets, every U
+    gives bitwise the same y, and y matches the oracle's SpMV on every level's K_l, P̄_l and R_l."""
+    K, F, H, Ho = build("C2", 6)
+    rng = np.random.default_rng(11)
+    seen = 0
+    for l, L in enumerate(Ho.levels):
+        ops = [(0, L.K)] + ([] if L.P is None else [(1, L.P), (2, L.R)])
+        for op, A in ops:
+            c = H.op_config(l, op)
+            if c["layout"] != "sellvi":
+                continue
+            seen += 1
+            A = A.tocsr()
+            bits = np.unique(np.concatenate([A.data.view(np.uint64), np.zeros(1, np.uint64)]))
+            assert c["n_values"] == bits.size
+            nr = A.shape[0]
+            assert c["alg_bytes"] == 4 * A.nnz + 8 * bits.size + 4 * nr + 8 * ((nr + 31) // 32 + 1)
+            x = dev(rng.uniform(-1, 1, A.shape[1]))
+            ys = []
+            for U in (1, 2, 4):
+                H.set_op_config(l, op, 0, 32, U)
+                y = torch.empty(nr, dtype=torch.float64, device="cuda")
+                H.apply(l, op, x, y)
+                ys.append(y.cpu().numpy())
+            H.set_op_config(l, op, 0, 32, c["U"])
+            xo = x.cpu().numpy()
+            assert all(np.array_equal(y, ys[0]) for y in ys)
+            assert np.all(np.abs(ys[0] - oracle.spmv(A, xo)) <= 1e-13 * (abs(A) @ np.abs(xo)) + 1e-300)
+    assert seen >= 1  # at least C2's K_0 (159 distinct values) qualifies
+
+
+def test_value_index_table():
+    """CSR-VI (kernel bit 3): the value table of C2's K_0 holds exactly the distinct stored values
+    (the operator's values and the 0.0 of the row padding, counted here by numpy on the host K), the
+    reported bytes follow the packed 4 B/entry format, and y = K_0 x through the value-indexed cores
+    is bitwise the streamed-value result and within 1e-13 of the oracle."""
+    K, F, H, Ho = build("C2", 4)  # CSR layout everywhere (format 0 would store C2's K_0 as SELL-VI)
+    c = H.op_config(0, 0)
+    bits = np.unique(np.concatenate([K.data.view(np.uint64), np.zeros(1, np.uint64)]))
+    assert c["n_values"] == bits.size and c["value_index_bytes"] == 2
+    N, nnz = K.shape[0], K.nnz
+    x = dev(np.random.default_rng(9).uniform(-1, 1, N))
+    ys = {}
+    for kern in (2, 10, 14, 8, 12):
+        H.set_op_config(0, 0, kern, c["G"], c["U"])
+        y = torch.empty(N, dtype=torch.float64, device="cuda")
+        H.apply(0, 0, x, y)
+        ys[kern] = y.cpu().numpy()
+        if kern == 10:
+            assert H.op_config(0, 0)["alg_bytes"] == 4 * nnz + 4 * N + 8 * bits.size + 8 * (N + 1)
+        if kern == 8:  # int32 columns + 32-bit value index
+            assert H.op_config(0, 0)["alg_bytes"] == 8 * nnz + 8 * bits.size + 8 * (N + 1)
+    H.set_op_config(0, 0, c["kernel_bits"], c["G"], c["U"])
+    for kern, y in ys.items():
+        assert np.array_equal(y, ys[2]), kern
+    xo = x.cpu().numpy()
+    assert np.all(np.abs(ys[10] - oracle.spmv(Ho.levels[0].K, xo)) <= 1e-13 * (abs(Ho.levels[0].K) @ np.abs(xo)))
 
 
 @pytest.mark.parametrize("fmt", FORMATS)

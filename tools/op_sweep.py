@@ -14,7 +14,10 @@ sys.path.insert(0, ROOT)
 
 import amg_inputs  # noqa: E402
 
-KINDS = ("csr_regs", "csr_tma", "csr_regs_d16", "csr_tma_d16", "csr_regs_pf", "csr_tma_pf", "csr_regs_d16_pf", "csr_tma_d16_pf")
+
+def kind_name(k: int) -> str:
+    return ("csr_tma" if k & 1 else "csr_regs") + ("_d16" if k & 2 else "") + ("_vi" if k & 8 else "") + \
+        ("_pf" if k & 4 else "")
 
 
 def main():
@@ -42,9 +45,13 @@ def main():
             ncol = info["N"][l] if op != 1 else info["N"][l + 1]
             x = torch.rand(ncol, dtype=torch.float64, device="cuda")
             y = torch.empty(nr, dtype=torch.float64, device="cuda")
-            for kern in (0, 1, 2, 3, 4, 6):  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch
-                for G in (1, 4, 8, 32):
-                    for U in (2, 4, 6, 8):
+            kerns = [0, 1, 2, 3, 4, 6]  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch, bit 3 value index
+            if chosen["n_values"]:
+                kerns += [8, 10, 12, 14]
+            sellvi = chosen["layout"] == "sellvi"
+            for kern in ([0] if sellvi else kerns):
+                for G in ((32,) if sellvi else (1, 4, 8, 32)):
+                    for U in ((1, 2, 4) if sellvi else (2, 4, 6, 8)):
                         if (kern & 1) and U > 4:
                             continue
                         try:
@@ -61,9 +68,9 @@ def main():
                         us = e0.elapsed_time(e1) * 1e3 / args.reps
                         cfg = H.op_config(l, op)
                         gbs = (cfg["alg_bytes"] + 16.0 * nr) / (us * 1e-6) / 1e9
-                        print(json.dumps(dict(level=l, op=op, kernel=KINDS[kern], G=G, U=U, us=round(us, 1),
+                        print(json.dumps(dict(level=l, op=op, kernel="sellvi" if sellvi else kind_name(kern), G=G, U=U, us=round(us, 1),
                                               GBps=round(gbs, 1), alg_bytes=cfg["alg_bytes"])), flush=True)
-            H.set_op_config(l, op, KINDS.index(chosen["kernel"]), chosen["G"], chosen["U"])
+            H.set_op_config(l, op, chosen["kernel_bits"], chosen["G"], chosen["U"])
             print(json.dumps(dict(level=l, op=op, autotuned=chosen)), flush=True)
     if args.sell:  # the SELL-32 layout (one row per lane) of the same operators
         H = None
