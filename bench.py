@@ -245,6 +245,10 @@ def run_gpu(args) -> None:
     pf = ", L2 prefetch of the next row" if k0["kernel"].endswith("_pf") else ""
     kname = f"{family}<G={k0['G']},U={k0['U']},EpiCheb,{cols}> (fused Chebyshev-ℓ1-Jacobi step on level 0{pf})"
     kkey = f"{family}<{k0['G']},{k0['U']},{cols}>"
+    if k0["layout"] == "sellvi":
+        kname = (f"k_sellvi<U={k0['U']},EpiCheb> (fused Chebyshev-ℓ1-Jacobi step on level 0; SELL-VI: row per "
+                 f"lane, 16-bit column offset + 16-bit index into {k0['n_values']} distinct values per entry)")
+        kkey = f"k_sellvi<{k0['U']}>"
     stream = torch.cuda.current_stream()
     Fd = torch.from_numpy(F).cuda()
     u = torch.zeros_like(Fd)

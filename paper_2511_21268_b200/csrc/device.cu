@@ -277,8 +277,8 @@ void encode_values(DevState &D, const double *v, int64_t stored, const uint16_t 
 }
 
 // SELL-VI layout (fmt 2; kernels.cuh k_sellvi) of a host CSR: 32-row slices of one 32-bit word per
-// entry (16-bit offset from the row's smallest column | 16-bit value index), column-major within the
-// slice.  Returns false (caller keeps CSR) unless every row spans < 65536 columns and the operator has
+// entry (16-bit offset from the row's smallest column | 16-bit value index), quads of 4 consecutive
+// entries of a row per lane, lane-interleaved within the slice; soff counts quads per lane.  Returns false (caller keeps CSR) unless every row spans < 65536 columns and the operator has
 // at most 65536 distinct values (+0.0 for the padding); `rule` additionally requires >= 2e6 non-zeros
 // and at most 25 % padding (the automatic choice of format 0).
 bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
@@ -297,14 +297,14 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
         ok = ok && ((int64_t)hi - (int64_t)lo <= 65535);
     }
     if (!ok) return false;
-    Buf<int64_t> soff(nsl + 1);
+    Buf<int64_t> soff(nsl + 1);  // in quads (4 entries) per lane
     soff[0] = 0;
     for (int64_t s = 0; s < nsl; s++) {
         int64_t W = 0;
         for (int64_t i = s * 32; i < std::min(n, s * 32 + 32); i++) W = std::max(W, A.rp[i + 1] - A.rp[i]);
-        soff[s + 1] = soff[s] + W;
+        soff[s + 1] = soff[s] + (W + 3) / 4;
     }
-    const int64_t stored = soff[nsl] * 32;
+    const int64_t stored = soff[nsl] * 128;
     if (rule && (double)stored > 1.25 * (double)nnz) return false;
     std::vector<double> tab;
     Buf<uint32_t> idx;
@@ -318,12 +318,12 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     Buf<uint32_t> w(stored);
 #pragma omp parallel for schedule(static)
     for (int64_t s = 0; s < nsl; s++) {
-        const int64_t W = soff[s + 1] - soff[s];
+        const int64_t W = (soff[s + 1] - soff[s]) * 4;
         for (int t = 0; t < 32; t++) {
             const int64_t i = s * 32 + t;
             const int64_t b = i < n ? A.rp[i] : 0, len = i < n ? A.rp[i + 1] - A.rp[i] : 0;
-            for (int64_t k = 0; k < W; k++) {
-                const int64_t dst = (soff[s] + k) * 32 + t;
+            for (int64_t k = 0; k < W; k++) {  // entry k of lane t: quad k/4, component k%4
+                const int64_t dst = ((soff[s] + k / 4) * 32 + t) * 4 + k % 4;
                 w[dst] = k < len ? (uint32_t)(A.ci[b + k] - base[i]) | (idx[b + k] << 16) : zero << 16;
             }
         }
@@ -1807,7 +1807,7 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     cfg->alg_bytes = A.alg_bytes();
     cfg->nnz = A.nnz;
     cfg->n_values = A.nvals;
-    cfg->value_index_bytes = A.vtab ? ((A.vpk && (A.kern & 2)) ? 2 : 4) : 0;
+    cfg->value_index_bytes = !A.vtab ? 0 : (A.fmt == 2 || (A.vpk && (A.kern & 2))) ? 2 : 4;
     return AMG_OK;
     API_END
 }

@@ -31,7 +31,8 @@ struct DevBuf {
 //   CSR2 (fmt 0): rows padded to even length; warp per group of G rows.
 //   SELL2 (fmt 1): 32-row slices, one row per lane, pair-interleaved columns; soff = slice offsets.
 //   SELL-VI (fmt 2): 32-row slices, one row per lane, one 32-bit word per entry (16-bit column offset
-//     from rbase | 16-bit value index into vtab); soff = slice offsets in 32-word columns; G = 32.
+//     from rbase | 16-bit value index into vtab) in lane-interleaved quads; soff = slice offsets in
+//     quads per lane; G = 32.
 struct DCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
     int fmt = 0;
@@ -63,7 +64,7 @@ struct DCsr {
     double alg_bytes() const {
         const double z = (double)nnz, rows = (double)nrows;
         if (fmt == 2)  // SELL-VI: 4 B word per entry, the value table, row bases, slice offsets
-            return 4.0 * z + 8.0 * (double)nvals + 4.0 * rows + 8.0 * (double)((nrows + 31) / 32 + 1);
+            return 4.0 * z + 8.0 * (double)nvals + 4.0 * rows + 8.0 * (double)((nrows + 31) / 32 + 1);  // padding excluded
         if (kern & 8) {
             if ((kern & 2) && vpk) return 4.0 * z + 4.0 * rows + 8.0 * (double)nvals + 8.0 * (rows + 1);
             const double cols = (kern & 2) ? 2.0 * z + 4.0 * rows : 4.0 * z;

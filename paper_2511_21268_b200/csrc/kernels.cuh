@@ -961,24 +961,34 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
 // ------------------------------------------------------------------------------------------------
 // SELL-VI core (layout 2): 32-row slices, ONE ROW PER LANE, one 32-bit word per stored entry = 16-bit
 // column offset from the row's smallest column | 16-bit index into the operator's distinct-value table
-// (CSR-VI above).  Slice s stores W_s = (its longest row) columns of 32 words; word k of lane t is
-// entry k of row 32s+t (padding: offset 0, the index of 0.0).
+// (CSR-VI above).  Slice s stores W4_s = ⌈(its longest row)/4⌉ columns of 32 quads: quad q of lane t
+// holds entries 4q..4q+3 of row 32s+t (padding: offset 0, the index of 0.0), so one 128-bit load per
+// lane fetches 4 entries and a warp load is 512 contiguous bytes.
 //
 // Why row per lane on the IgA operators: lane t and lane t+1 hold rows i and i+1, x-neighbours, so
 // entry k of the 32 rows is one stencil position at 32 consecutive columns — the x-gather of one warp
 // instruction is 256 contiguous bytes (2–3 L1 wavefronts instead of ≈ 6 for a row per warp), and the
 // 32 rows of an interior slice have the SAME value at entry k — the table lookup is one broadcast.
 // Together with the 4 B streamed per entry this moves the fine-level operator from 10 B/entry at ≈ 9
-// L1 wavefronts per 32 entries (CSR-D16) to 4 B at ≈ 5.
+// L1 wavefronts per 32 entries (CSR-D16) to 4 B at ≈ 4–5.
 //
 // Summation order: entry k of a row goes to chain k & 1, each chain accumulates in increasing k, the
-// row sum is chain0 + chain1 — independent of U (entries in flight per lane), so every U gives
+// row sum is chain0 + chain1 — independent of U (quads in flight per lane), so every U gives
 // bitwise-equal results.  (Not the CSR cores' order: the layout is chosen per operator by a fixed rule at
-// setup, never by timing, so results do not depend on the autotuner.)  Slices are visited in
-// the boundary-first order of 32-row groups on P2P runs, with the same early publication as k_csr2.
+// setup, never by timing, so results do not depend on the autotuner.)  Slices are visited in the
+// boundary-first order of 32-row groups on P2P runs, with the same early publication as k_csr2.
 // ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ unsigned quad_at(const uint4 &q, int j) { return j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w; }
+
 template <int U, class Epi>
-__global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ soff, const unsigned *__restrict__ w,
+__global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
                                                    const int *__restrict__ rbase, const double *__restrict__ table,
                                                    const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc,
                                                    P2P pp) {
@@ -998,7 +1008,7 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
         }
         const int64_t sl = pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos;
         const int64_t off = __ldg(soff + sl);
-        const int W = (int)(__ldg(soff + sl + 1) - off);
+        const int W4 = (int)(__ldg(soff + sl + 1) - off);
         const int64_t row = (sl << 5) + lane;
         typename Epi::Pre pre{};
         int b = 0;
@@ -1006,29 +1016,52 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
             b = __ldg(rbase + row);
             pre = epi.load(row);
         }
-        const unsigned *wp = w + (off << 5) + lane;
+        const uint4 *wp = w + (off << 5) + lane;
         double s0 = 0.0, s1 = 0.0;
-        int k = 0;
-        for (; k + 2 * U <= W; k += 2 * U) {
-            unsigned wa[2 * U];
+        int q = 0;
+        // software pipeline: the next batch's words are requested before this batch's gathers, so the
+        // HBM stream never waits behind the (L1/L2) gathers
+        uint4 wa[U], wn[U];
+        if (U <= W4) {
 #pragma unroll
-            for (int u = 0; u < 2 * U; u++) wa[u] = ld_stream(wp + (int64_t)(k + u) * 32, pol);
-            double va[2 * U], xa[2 * U];
+            for (int u = 0; u < U; u++) wa[u] = ld_stream(wp + (int64_t)u * 32, pol);
+        }
+        for (; q + U <= W4; q += U) {
+            const bool more = q + 2 * U <= W4;
+            if (more) {
 #pragma unroll
-            for (int u = 0; u < 2 * U; u++) va[u] = ld_gather(table + (wa[u] >> 16));
+                for (int u = 0; u < U; u++) wn[u] = ld_stream(wp + (int64_t)(q + U + u) * 32, pol);
+            }
+            double va[4 * U], xa[4 * U];
 #pragma unroll
-            for (int u = 0; u < 2 * U; u++) xa[u] = ld_gather(g + (b + (int)(wa[u] & 0xffffu)));
+            for (int u = 0; u < U; u++)
 #pragma unroll
-            for (int u = 0; u < 2 * U; u += 2) {
+                for (int j = 0; j < 4; j++) va[4 * u + j] = ld_gather(table + (quad_at(wa[u], j) >> 16));
+#pragma unroll
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) xa[4 * u + j] = ld_gather(g + (b + (int)(quad_at(wa[u], j) & 0xffffu)));
+#pragma unroll
+            for (int u = 0; u < 4 * U; u += 2) {
                 s0 = fma(va[u], xa[u], s0);
                 s1 = fma(va[u + 1], xa[u + 1], s1);
             }
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < U; u++) wa[u] = wn[u];
+            }
         }
-        for (; k < W; k++) {
-            const unsigned x = ld_stream(wp + (int64_t)k * 32, pol);
-            const double p = ld_gather(table + (x >> 16)), xv = ld_gather(g + (b + (int)(x & 0xffffu)));
-            if (k & 1) s1 = fma(p, xv, s1);
-            else s0 = fma(p, xv, s0);
+        for (; q < W4; q++) {
+            const uint4 wq = ld_stream(wp + (int64_t)q * 32, pol);
+            double va[4], xa[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) va[j] = ld_gather(table + (quad_at(wq, j) >> 16));
+#pragma unroll
+            for (int j = 0; j < 4; j++) xa[j] = ld_gather(g + (b + (int)(quad_at(wq, j) & 0xffffu)));
+            s0 = fma(va[0], xa[0], s0);
+            s1 = fma(va[1], xa[1], s1);
+            s0 = fma(va[2], xa[2], s0);
+            s1 = fma(va[3], xa[3], s1);
         }
         if (row < nrows) acc_add(dacc, epi(row, s0 + s1, pre));
     }

@@ -24,7 +24,8 @@ void launch_sellvi_u(DevState &D, const DCsr &A, const double *g, Epi epi, cudaS
         per_sm = std::max(per_sm, 1);
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-    dev::k_sellvi<U, Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, A.vpk, A.rbase, A.vtab, g, A.nrows, epi,
+    dev::k_sellvi<U, Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase,
+                                                        A.vtab, g, A.nrows, epi,
                                                         dotctx(D, dotkind),
                                                         (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
 }

@@ -31,7 +31,10 @@ UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 def kernel_key(name: str) -> str:
     """'void k_csr2<8, 6, EpiCheb<0>, ColsD16V16>(...)' -> 'k_csr2<8,6,ColsD16V16>'."""
     m = re.search(r"(k_csr2|k_csr4t)<(\d+), (\d+), [^,]+?(?:<[^>]*>)?, (Cols\w+)>", name)
-    return f"{m.group(1)}<{m.group(2)},{m.group(3)},{m.group(4)}>" if m else name
+    if m:
+        return f"{m.group(1)}<{m.group(2)},{m.group(3)},{m.group(4)}>"
+    m = re.search(r"k_sellvi<(\d+), ", name)  # 'void k_sellvi<2, EpiCheb<0>>(...)' -> 'k_sellvi<2>'
+    return f"k_sellvi<{m.group(1)}>" if m else name
 
 
 def main():

@@ -27,12 +27,13 @@ def main():
     ap.add_argument("--ops", default="0")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--sell", action="store_true", help="also time the SELL-32 layout")
+    ap.add_argument("--format", type=int, default=0, help="amg_params.format of the swept hierarchy")
     args = ap.parse_args()
     import torch
     import paper_2511_21268_b200 as amg
     c = amg_inputs.CONFIGS[args.config]
     K, F = amg.iga_poisson(c["dim"], c["p"], c["n"])
-    H = amg.Hierarchy(K, amg.params(c["p"]))
+    H = amg.Hierarchy(K, amg.params(c["p"], format=args.format))
     del K
     info = H.info()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
