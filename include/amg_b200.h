@@ -109,9 +109,9 @@ typedef struct {
     int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30)                */
     int64_t coarse_size;    /* coarsest when N_l <= coarse_size (50)                 */
     int max_levels;         /* 20                                                                 */
-    int format;             /* device matrix format: 0 auto (K_l with >= 2e6 non-zeros, rows spanning
-                               < 65536 columns, <= 65536 distinct values and <= 25 % slice padding:
-                               SELL-VI, a fixed rule; every other operator: CSR rows padded to 8 with the
+    int format;             /* device matrix format: 0 auto (K_l and P̄_l with >= 2e6 non-zeros, rows
+                               spanning < 65536 columns, <= 65536 distinct values and <= 50 % slice
+                               padding: SELL-VI, a fixed rule; every other operator: CSR rows padded to 8 with the
                                kernel, column and value source autotuned), 1 CSR warp-per-row,
                                2 SELL-32 (row per lane), 3 TMA-staged CSR, 4 CSR with 16-bit column
                                offsets (register core), 5 CSR with 16-bit column offsets (TMA-staged

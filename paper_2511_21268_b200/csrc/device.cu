@@ -278,9 +278,10 @@ void encode_values(DevState &D, const double *v, int64_t stored, const uint16_t 
 
 // SELL-VI layout (fmt 2; kernels.cuh k_sellvi) of a host CSR: 32-row slices of one 32-bit word per
 // entry (16-bit offset from the row's smallest column | 16-bit value index), quads of 4 consecutive
-// entries of a row per lane, lane-interleaved within the slice; soff counts quads per lane.  Returns false (caller keeps CSR) unless every row spans < 65536 columns and the operator has
-// at most 65536 distinct values (+0.0 for the padding); `rule` additionally requires >= 2e6 non-zeros
-// and at most 25 % padding (the automatic choice of format 0).
+// entries of a row per lane, lane-interleaved within the slice; soff counts quads per lane.  Returns
+// false (caller keeps CSR) unless every row spans < 65536 columns and the operator has at most 65536
+// distinct values (+0.0 for the padding); `rule` additionally requires >= 2e6 non-zeros and at most
+// 50 % padding (the automatic choice of format 0, for K_l and P̄_l).
 bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     const int64_t n = A.nrows, nsl = (n + 31) / 32, nnz = A.nnz();
     if (n == 0 || nnz == 0) return false;
@@ -305,7 +306,7 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
         soff[s + 1] = soff[s] + (W + 3) / 4;
     }
     const int64_t stored = soff[nsl] * 128;
-    if (rule && (double)stored > 1.25 * (double)nnz) return false;
+    if (rule && (double)stored > 1.5 * (double)nnz) return false;
     std::vector<double> tab;
     Buf<uint32_t> idx;
     if (!value_dictionary(A.v.data(), nnz, true, 65536, tab, idx)) return false;
@@ -428,8 +429,10 @@ void upload_op(DevState &D, const HCsr &A, DCsr &out, bool square, int format, b
     out.nrows = A.nrows;
     out.ncols = A.ncols;
     out.nnz = A.nnz();
-    // SELL-VI: format 0 by the fixed rule on the K_l, format 6 wherever admissible (never the coarsest K)
-    if (!force_csr && ((format == 0 && role == 0) || format == 6) && upload_sellvi(D, A, out, format == 0)) return;
+    // SELL-VI: format 0 by the fixed rule on the K_l and P̄_l, format 6 wherever admissible (never the
+    // coarsest K)
+    if (!force_csr && ((format == 0 && (role == 0 || role == 1)) || format == 6) && upload_sellvi(D, A, out, format == 0))
+        return;
     if (format == 0 || format >= 3) {
         // rows padded to 8 entries (16-byte aligned value, int32 and 16-bit column ranges): runnable by
         // both the register-batched CSR2 core and the TMA-staged CSR4T core (format 0 autotunes)

@@ -986,12 +986,25 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p, uint64_t pol) {
     return r;
 }
 __device__ __forceinline__ unsigned quad_at(const uint4 &q, int j) { return j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w; }
+extern __shared__ double sellvi_table[];  // dynamic shared memory of k_sellvi<.., kSmem = true>
+template <bool kSmem>
+__device__ __forceinline__ double tab_at(const double *t, unsigned i) {
+    if constexpr (kSmem) return sellvi_table[i];
+    else return ld_gather(t + i);
+}
 
-template <int U, class Epi>
+// kSmem: the value table (nvals entries) is first copied into shared memory, where the lookups of one
+// warp instruction — a few distinct values, mostly one — take one wavefront instead of ≈ 3 L1 lines.
+template <int U, class Epi, bool kSmem>
 __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
-                                                   const int *__restrict__ rbase, const double *__restrict__ table,
-                                                   const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc,
-                                                   P2P pp) {
+                                                   const int *__restrict__ rbase, const double *__restrict__ gtable,
+                                                   int nvals, const double *__restrict__ g, int64_t nrows, Epi epi,
+                                                   DotCtx dc, P2P pp) {
+    const double *table = gtable;
+    if constexpr (kSmem) {
+        for (int i = threadIdx.x; i < nvals; i += blockDim.x) sellvi_table[i] = __ldg(gtable + i);
+        __syncthreads();
+    }
     if (!pp.gorder) peer_wait(pp);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -1036,7 +1049,7 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) va[4 * u + j] = ld_gather(table + (quad_at(wa[u], j) >> 16));
+                for (int j = 0; j < 4; j++) va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> 16);
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
@@ -1055,7 +1068,7 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
             const uint4 wq = ld_stream(wp + (int64_t)q * 32, pol);
             double va[4], xa[4];
 #pragma unroll
-            for (int j = 0; j < 4; j++) va[j] = ld_gather(table + (quad_at(wq, j) >> 16));
+            for (int j = 0; j < 4; j++) va[j] = tab_at<kSmem>(table, quad_at(wq, j) >> 16);
 #pragma unroll
             for (int j = 0; j < 4; j++) xa[j] = ld_gather(g + (b + (int)(quad_at(wq, j) & 0xffffu)));
             s0 = fma(va[0], xa[0], s0);

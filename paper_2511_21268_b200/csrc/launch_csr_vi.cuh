@@ -14,20 +14,31 @@ void launch_csr_vi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStr
     else launch_csr_cols(D, A, dev::ColsI32V32{A.ci, A.vidx, A.vtab}, g, epi, st, dotkind);
 }
 
-template <int U, class Epi>
-void launch_sellvi_u(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+// Value tables of up to kSellviSmemVals entries (32 KB) are staged in shared memory per CTA.
+constexpr int64_t kSellviSmemVals = 4096;
+
+template <int U, class Epi, bool kSmem>
+void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
     const int64_t nsl = (A.nrows + 31) / 32;
     const int64_t wpb = dev::kBlock / 32;
-    static int per_sm = 0;  // resident CTAs per SM of this instantiation
-    if (!per_sm) {
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sellvi<U, Epi>, dev::kBlock, 0));
+    const int smem = kSmem ? (int)(A.nvals * 8) : 0;
+    // resident CTAs per SM of this instantiation at this table size (cached for the last size seen)
+    static int per_sm = 0, per_sm_smem = -1;
+    if (per_sm_smem != smem) {
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sellvi<U, Epi, kSmem>, dev::kBlock, smem));
         per_sm = std::max(per_sm, 1);
+        per_sm_smem = smem;
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-    dev::k_sellvi<U, Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase,
-                                                        A.vtab, g, A.nrows, epi,
-                                                        dotctx(D, dotkind),
-                                                        (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
+    dev::k_sellvi<U, Epi, kSmem><<<grid, dev::kBlock, smem, st>>>(
+        A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase, A.vtab, (int)A.nvals, g, A.nrows, epi,
+        dotctx(D, dotkind), (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
+}
+
+template <int U, class Epi>
+void launch_sellvi_u(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    if (A.nvals <= kSellviSmemVals) launch_sellvi_us<U, Epi, true>(D, A, g, epi, st, dotkind);
+    else launch_sellvi_us<U, Epi, false>(D, A, g, epi, st, dotkind);
 }
 
 template <class Epi>
