@@ -138,6 +138,12 @@ typedef void *(*amg_alloc_fn)(size_t bytes, int device, void *cuda_stream);
 typedef void (*amg_free_fn)(void *ptr, size_t bytes, int device, void *cuda_stream);
 amg_status amg_set_allocator(amg_alloc_fn alloc, amg_free_fn free_fn);
 
+/* Host threads (OpenMP) of this process's later library calls: generator, setup, share export/import,
+ * device uploads (amg_params.num_threads overrides it inside amg_setup).  Launchers such as torchrun
+ * set OMP_NUM_THREADS=1 per process; the shared setup gives rank 0 every core for the host setup and
+ * each rank its share of the cores for its device setup.  AMG_EINVAL if n < 1. */
+amg_status amg_set_num_threads(int n);
+
 /* Multi-GPU descriptor: one process per GPU.  NULL or nranks == 1 -> single GPU `device`
  * (NULL -> the current device). */
 typedef struct {

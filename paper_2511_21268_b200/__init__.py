@@ -20,7 +20,7 @@ from . import _lib
 from ._lib import AmgError, check, lib
 
 __all__ = ["AmgError", "Hierarchy", "iga_poisson", "iga_tables", "params", "use_torch_allocator", "HostCsr",
-           "Share", "setup_distributed"]
+           "Share", "setup_distributed", "set_num_threads"]
 
 
 @dataclass
@@ -104,6 +104,11 @@ def use_torch_allocator() -> None:
     refs = (ALLOC(_alloc), FREE(_free))
     check(lib().amg_set_allocator(C.cast(refs[0], C.c_void_p), C.cast(refs[1], C.c_void_p)))
     _ALLOC_REFS = refs
+
+
+def set_num_threads(n: int) -> None:
+    """amg_set_num_threads: host (OpenMP) threads of this process's later library calls."""
+    check(lib().amg_set_num_threads(int(n)))
 
 
 def nccl_unique_id() -> bytes:
@@ -381,6 +386,9 @@ def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: i
     if group is None:
         group = dist.new_group(backend="gloo")
     d = make_dist(rank, nranks, device=device, nccl_id=nccl_id)
+    import os
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    set_num_threads(cores)  # the host setup runs alone on rank 0: every core
     size = torch.zeros(1, dtype=torch.int64)
     lap("init")
     if rank == 0:
@@ -405,6 +413,7 @@ def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: i
             sh.close()
             lap("send")
         G.close()
+        set_num_threads(max(1, cores // nranks))  # the device setups run side by side
         H = Hierarchy.from_share(mine, d, host_only=host_only)
         mine.close()
     else:
@@ -414,6 +423,7 @@ def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: i
         for o in range(0, buf.numel(), chunk_bytes):
             dist.recv(buf[o:o + chunk_bytes], 0, group=group)
         lap("recv")
+        set_num_threads(max(1, cores // nranks))
         H = Hierarchy.from_share(buf.numpy(), d, host_only=host_only)
         del buf
     lap("device_setup")

@@ -74,6 +74,14 @@ void amg_csr_free(amg_csr *K) {
     std::free(K);
 }
 
+amg_status amg_set_num_threads(int n) {
+    API_BEGIN
+    if (n < 1) throw Error{AMG_EINVAL, "thread count must be >= 1"};
+    omp_set_num_threads(n);
+    return AMG_OK;
+    API_END
+}
+
 amg_status amg_iga_tables(int degree, int n_elem, double *mhat, double *khat) {
     API_BEGIN
     if (degree < 1 || degree > 8 || n_elem < 1 || !mhat || !khat) throw Error{AMG_EINVAL, "bad argument"};
