@@ -249,7 +249,7 @@ def run_gpu(args) -> None:
     kkey = f"{family}<{k0['G']},{k0['U']},{cols}>"
     if k0["layout"] == "sellvi":
         kname = (f"k_sellvi<U={k0['U']},EpiCheb> (fused Chebyshev-ℓ1-Jacobi step on level 0; SELL-VI: row per "
-                 f"lane, 16-bit column offset + 16-bit index into {k0['n_values']} distinct values per entry)")
+                 f"lane, one 32-bit word per entry = column offset | index into {k0['n_values']} distinct values)")
         kkey = f"k_sellvi<{k0['U']}>"
     stream = torch.cuda.current_stream()
     Fd = torch.from_numpy(F).cuda()

@@ -109,14 +109,15 @@ typedef struct {
     int coarse_sweeps;      /* ℓ1-Jacobi sweeps on the coarsest level (30)                */
     int64_t coarse_size;    /* coarsest when N_l <= coarse_size (50)                 */
     int max_levels;         /* 20                                                                 */
-    int format;             /* device matrix format: 0 auto (K_l and P̄_l with >= 2e6 non-zeros, rows
-                               spanning < 65536 columns, <= 65536 distinct values and <= 50 % slice
-                               padding: SELL-VI, a fixed rule; every other operator: CSR rows padded to 8 with the
+    int format;             /* device matrix format: 0 auto (K_l and P̄_l with >= 2e6 non-zeros whose
+                               column offsets (>= 16 bits, <= 24) and distinct-value indices fit one
+                               32-bit word, and <= 50 % slice padding: SELL-VI, a fixed rule; every
+                               other operator: CSR rows padded to 8 with the
                                kernel, column and value source autotuned), 1 CSR warp-per-row,
                                2 SELL-32 (row per lane), 3 TMA-staged CSR, 4 CSR with 16-bit column
                                offsets (register core), 5 CSR with 16-bit column offsets (TMA-staged
-                               values), 6 SELL-VI (row per lane, 16-bit column offset + 16-bit value
-                               index per entry) for every K_l, P̄_l, R_l that admits it, any size */
+                               values), 6 SELL-VI (row per lane, column offset + value index in one
+                               32-bit word per entry) for every K_l, P̄_l, R_l that admits it, any size */
     int host_only;          /* 1: build the hierarchy on the host only (export/inspection; no CUDA call) */
     int num_threads;        /* host setup threads (OpenMP); 0 = runtime default                     */
     int krylov;             /* outer solver: 0 = PCG (c.19); 1 = flexible CG, Notay's FCG(1)
@@ -216,7 +217,7 @@ amg_status amg_set_profiling(amg_hierarchy *H, int enable); /* enable resets the
 amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
 
 /* Device kernel chosen for operator op (0 K_l, 1 P̄_l, 2 R_l) of level l: layout (0 padded CSR,
- * 1 SELL-32, 2 SELL-VI: row per lane, 16-bit column offset + 16-bit value index per entry), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
+ * 1 SELL-32, 2 SELL-VI: row per lane, column offset + value index in one 32-bit word per entry), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
  * source, 0 int32 columns, 1 16-bit column offsets from a per-row base; bit 2: register core with an L2
  * bulk prefetch of the next row; bit 3: value source, 0 streamed fp64 values, 1 value index into the
  * operator's table of distinct values — CSR-VI, register core only), rows per warp group G, pairs per

@@ -278,10 +278,11 @@ void encode_values(DevState &D, const double *v, int64_t stored, const uint16_t 
 
 // SELL-VI layout (fmt 2; kernels.cuh k_sellvi) of a host CSR: 32-row slices of one 32-bit word per
 // entry (16-bit offset from the row's smallest column | 16-bit value index), quads of 4 consecutive
-// entries of a row per lane, lane-interleaved within the slice; soff counts quads per lane.  Returns
-// false (caller keeps CSR) unless every row spans < 65536 columns and the operator has at most 65536
-// distinct values (+0.0 for the padding); `rule` additionally requires >= 2e6 non-zeros and at most
-// 50 % padding (the automatic choice of format 0, for K_l and P̄_l).
+// entries of a row per lane, lane-interleaved within the slice; soff counts quads per lane.  The
+// offset takes obits = max(16, bits of the widest row's span) bits, the value index the other 32 −
+// obits.  Returns false (caller keeps CSR) if obits > 24 or the operator has more than 2^(32 − obits)
+// distinct values (+0.0 for the padding); `rule` additionally requires >= 2e6 non-zeros, at most 50 %
+// padding and row-to-row locality (below) — the automatic choice of format 0, for K_l and P̄_l.
 bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     const int64_t n = A.nrows, nsl = (n + 31) / 32, nnz = A.nnz();
     if (n == 0 || nnz == 0) return false;
@@ -289,15 +290,17 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     if (const char *e = std::getenv("AMG_SELLVI"))
         if (std::atoi(e) == 0) return false;
     Buf<int32_t> base(n);
-    bool ok = true;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
+    int64_t span = 0;
+#pragma omp parallel for schedule(static) reduction(max : span)
     for (int64_t i = 0; i < n; i++) {
         const bool has = A.rp[i + 1] > A.rp[i];
         const int32_t lo = has ? A.ci[A.rp[i]] : 0, hi = has ? A.ci[A.rp[i + 1] - 1] : 0;  // ascending columns
         base[i] = lo;
-        ok = ok && ((int64_t)hi - (int64_t)lo <= 65535);
+        span = std::max<int64_t>(span, (int64_t)hi - (int64_t)lo);
     }
-    if (!ok) return false;
+    int obits = 16;  // offset bits: at least 16, enough for the widest row; the value index gets the rest
+    while ((span >> obits) != 0) obits++;
+    if (obits > 24) return false;
     Buf<int64_t> soff(nsl + 1);  // in quads (4 entries) per lane
     soff[0] = 0;
     for (int64_t s = 0; s < nsl; s++) {
@@ -309,7 +312,39 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     if (rule && (double)stored > 1.5 * (double)nnz) return false;
     std::vector<double> tab;
     Buf<uint32_t> idx;
-    if (!value_dictionary(A.v.data(), nnz, true, 65536, tab, idx)) return false;
+    if (!value_dictionary(A.v.data(), nnz, true, (int64_t)1 << (32 - obits), tab, idx)) return false;
+    if (rule) {
+        // Locality test (sampled, deterministic): for an entry column k of a slice, the 32 rows' x-gather
+        // lines (128 B) and distinct table values are what one warp instruction costs in L1.  The
+        // row-per-lane layout pays only when rows i and i+1 are shifted copies of each other (the fine
+        // stencil: ≈ 4.7 lines, ≈ 4 values at C3-like sizes; P̄₀: 5.1, 9.0); the coarse Galerkin
+        // operators are not (K₁: 9.7 lines, 17 values), and stay CSR.
+        double lines = 0.0, vals = 0.0;
+        int64_t samples = 0;
+        const int64_t sstep = std::max<int64_t>(1, nsl / 512);
+        for (int64_t s = 0; s < nsl; s += sstep) {
+            const int64_t W = (soff[s + 1] - soff[s]) * 4;
+            for (int64_t k = 0; k < W; k += 4) {
+                int64_t ln[32], vv[32];
+                int nl = 0, nv2 = 0;
+                for (int64_t i = s * 32; i < std::min(n, s * 32 + 32); i++) {
+                    if (A.rp[i] + k >= A.rp[i + 1]) continue;
+                    const int64_t c = A.ci[A.rp[i] + k] >> 4, v = idx[A.rp[i] + k];
+                    bool seen = false;
+                    for (int t = 0; t < nl && !seen; t++) seen = ln[t] == c;
+                    if (!seen) ln[nl++] = c;
+                    seen = false;
+                    for (int t = 0; t < nv2 && !seen; t++) seen = vv[t] == v;
+                    if (!seen) vv[nv2++] = v;
+                }
+                if (!nl) continue;
+                lines += nl;
+                vals += nv2;
+                samples++;
+            }
+        }
+        if (samples == 0 || (lines + 0.5 * vals) / (double)samples > 12.0) return false;
+    }
     uint32_t zero = 0;
     for (size_t t = 0; t < tab.size(); t++) {
         uint64_t b;
@@ -325,11 +360,12 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
             const int64_t b = i < n ? A.rp[i] : 0, len = i < n ? A.rp[i + 1] - A.rp[i] : 0;
             for (int64_t k = 0; k < W; k++) {  // entry k of lane t: quad k/4, component k%4
                 const int64_t dst = ((soff[s] + k / 4) * 32 + t) * 4 + k % 4;
-                w[dst] = k < len ? (uint32_t)(A.ci[b + k] - base[i]) | (idx[b + k] << 16) : zero << 16;
+                w[dst] = k < len ? (uint32_t)(A.ci[b + k] - base[i]) | (idx[b + k] << obits) : zero << obits;
             }
         }
     }
     out.fmt = 2;
+    out.obits = obits;
     out.stored = stored;
     out.G = 32;
     out.U = 2;
@@ -1385,6 +1421,15 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         CUDA_OK(cudaMemset(D->counter, 0, 4 * sizeof(unsigned)));
         CUDA_OK(cudaMemset(D->S, 0, sizeof(dev::Scalars)));
         CUDA_OK(cudaMallocHost(&D->hS, sizeof(dev::Scalars)));
+        // operators whose streams fit in L2 may keep the normal L2 priority (env AMG_L2_KEEP_MB MB,
+        // default 0 = off), so that their 2m+1 applications per V-cycle read from L2
+        {
+            double keep_mb = 0.0;  // off: measured no gain at C3 level 2 (110 MB, run 41)
+            if (const char *e = std::getenv("AMG_L2_KEEP_MB")) keep_mb = std::atof(e);
+            for (int l = 0; l < D->nlevels; l++)
+                for (DCsr *A : {&D->lev[l].K, &D->lev[l].P, &D->lev[l].R})
+                    A->l2keep = A->fmt == 0 && A->nnz > 0 && 10.0 * (double)A->nnz <= keep_mb * 1e6;
+        }
         lap("upload");
         if (fmt == 0) {  // autotune every large operator on scratch vectors
             int64_t big = 1, lomax = 0;

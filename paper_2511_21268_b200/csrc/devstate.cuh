@@ -38,6 +38,7 @@ struct DCsr {
     int fmt = 0;
     int mult = 2;  // CSR layouts: every row padded to a multiple of `mult` entries
     int pf = 0;    // register CSR core: L2 bulk prefetch of the next row (autotuned)
+    bool l2keep = false;  // register CSR core: normal L2 priority for the streams (fits in L2)
     int64_t *rp = nullptr;    // CSR2 row pointers (entries)
     int64_t *soff = nullptr;  // SELL2 slice offsets (pairs)
     int32_t *ci = nullptr;
@@ -58,6 +59,7 @@ struct DCsr {
     int64_t nvals = 0;
     uint32_t *vidx = nullptr;
     uint32_t *vpk = nullptr;
+    int obits = 16;  // SELL-VI: column-offset bits of a word (the value index takes the other 32 − obits)
     // bytes one application must stream from HBM for this operator (values of the nnz stored entries
     // or their value indices + the value table, the column data of the chosen source, row pointers);
     // vectors are counted by the caller

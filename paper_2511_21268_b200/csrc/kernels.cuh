@@ -452,6 +452,14 @@ __device__ __forceinline__ uint64_t stream_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// Normal L2 priority for operators small enough to stay L2-resident across their repeated
+// applications in a V-cycle (DCsr::l2keep): their lines survive the evict-first streams of the large
+// levels.
+__device__ __forceinline__ uint64_t keep_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ double2 ld_stream(const double2 *p, uint64_t pol) {
     double2 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
@@ -616,9 +624,10 @@ struct ColsI32V32 {
 // (2l, 2l+1) pairing, measured on the C3 levels), accumulating them in two separate chains.  U windows
 // are loaded back to back before any is consumed.  The row sum is a fixed xor-shuffle tree of the
 // 32 lanes' (chain0 + chain1); all CSR kernel variants use exactly this order (bitwise-equal results).
-// pf = 1: while reducing row t of a group, lane 0 has the bulk-copy engine prefetch row t+1's values
+// pf bit 0: while reducing row t of a group, lane 0 has the bulk-copy engine prefetch row t+1's values
 // and column data into L2, so the next row's loads hit L2 instead of DRAM (more bytes in flight per
-// warp without holding registers).
+// warp without holding registers).  pf bit 1: the matrix streams use the normal L2 priority instead of
+// evict-first (operators that fit in L2; DCsr::l2keep).
 template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp, Cols cols,
                                                  const double *__restrict__ v, const double *__restrict__ g,
@@ -628,7 +637,7 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t ngroups = (nrows + G - 1) / G;
-    const uint64_t pol = stream_policy();
+    const uint64_t pol = (pf & 2) ? keep_policy() : stream_policy();
     typename Epi::Acc dacc{};
     bool signalled = pp.gorder == nullptr || pp.nranks == 0;
     if (!signalled && warp < pp.nbnd) peer_wait_warp(pp);  // this warp has boundary groups
@@ -655,7 +664,7 @@ __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp,
         for (int t = 0; t < nr; t++) {
             const int64_t b = __shfl_sync(0xffffffffu, gb, t), e = __shfl_sync(0xffffffffu, ge, t);
             const int rs = __shfl_sync(0xffffffffu, grs, t);
-            if (pf && t + 1 < nr) {
+            if ((pf & 1) && t + 1 < nr) {
                 const int64_t nb = __shfl_sync(0xffffffffu, gb, t + 1), ne = __shfl_sync(0xffffffffu, ge, t + 1);
                 // rows are padded to 8 entries: every stream's range is 16-byte aligned
                 if (lane == 0 && ne > nb && (nb & 7) == 0 && ((ne - nb) & 7) == 0) {
@@ -959,9 +968,10 @@ __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ so
 }
 
 // ------------------------------------------------------------------------------------------------
-// SELL-VI core (layout 2): 32-row slices, ONE ROW PER LANE, one 32-bit word per stored entry = 16-bit
-// column offset from the row's smallest column | 16-bit index into the operator's distinct-value table
-// (CSR-VI above).  Slice s stores W4_s = ⌈(its longest row)/4⌉ columns of 32 quads: quad q of lane t
+// SELL-VI core (layout 2): 32-row slices, ONE ROW PER LANE, one 32-bit word per stored entry = column
+// offset from the row's smallest column (low `obits` bits) | index into the operator's distinct-value
+// table (CSR-VI above; the high 32 − obits bits).  obits is the operator's: 16 at C3, 18 for the wider
+// rows of C4/C5.  Slice s stores W4_s = ⌈(its longest row)/4⌉ columns of 32 quads: quad q of lane t
 // holds entries 4q..4q+3 of row 32s+t (padding: offset 0, the index of 0.0), so one 128-bit load per
 // lane fetches 4 entries and a warp load is 512 contiguous bytes.
 //
@@ -998,8 +1008,9 @@ __device__ __forceinline__ double tab_at(const double *t, unsigned i) {
 template <int U, class Epi, bool kSmem>
 __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
                                                    const int *__restrict__ rbase, const double *__restrict__ gtable,
-                                                   int nvals, const double *__restrict__ g, int64_t nrows, Epi epi,
-                                                   DotCtx dc, P2P pp) {
+                                                   int nvals, int obits, const double *__restrict__ g, int64_t nrows,
+                                                   Epi epi, DotCtx dc, P2P pp) {
+    const unsigned omask = (1u << obits) - 1u;
     const double *table = gtable;
     if constexpr (kSmem) {
         for (int i = threadIdx.x; i < nvals; i += blockDim.x) sellvi_table[i] = __ldg(gtable + i);
@@ -1049,11 +1060,11 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> 16);
+                for (int j = 0; j < 4; j++) va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> obits);
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) xa[4 * u + j] = ld_gather(g + (b + (int)(quad_at(wa[u], j) & 0xffffu)));
+                for (int j = 0; j < 4; j++) xa[4 * u + j] = ld_gather(g + (b + (int)(quad_at(wa[u], j) & omask)));
 #pragma unroll
             for (int u = 0; u < 4 * U; u += 2) {
                 s0 = fma(va[u], xa[u], s0);
@@ -1068,9 +1079,9 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
             const uint4 wq = ld_stream(wp + (int64_t)q * 32, pol);
             double va[4], xa[4];
 #pragma unroll
-            for (int j = 0; j < 4; j++) va[j] = tab_at<kSmem>(table, quad_at(wq, j) >> 16);
+            for (int j = 0; j < 4; j++) va[j] = tab_at<kSmem>(table, quad_at(wq, j) >> obits);
 #pragma unroll
-            for (int j = 0; j < 4; j++) xa[j] = ld_gather(g + (b + (int)(quad_at(wq, j) & 0xffffu)));
+            for (int j = 0; j < 4; j++) xa[j] = ld_gather(g + (b + (int)(quad_at(wq, j) & omask)));
             s0 = fma(va[0], xa[0], s0);
             s1 = fma(va[1], xa[1], s1);
             s0 = fma(va[2], xa[2], s0);

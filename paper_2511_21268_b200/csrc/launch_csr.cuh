@@ -42,7 +42,7 @@ void launch_csr2_gu(DevState &D, const DCsr &A, const Cols &cols, const double *
         1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, (int64_t)per_sm * D.nsm));
     dev::k_csr2<G, U, Epi, Cols><<<grid, dev::kBlock, 0, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
                                                                (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)),
-                                                               A.mult >= 8 ? A.pf : 0);
+                                                               (A.mult >= 8 ? A.pf : 0) | (A.l2keep ? 2 : 0));
 }
 
 template <class Epi, class Cols>

@@ -14,8 +14,10 @@ void launch_csr_vi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStr
     else launch_csr_cols(D, A, dev::ColsI32V32{A.ci, A.vidx, A.vtab}, g, epi, st, dotkind);
 }
 
-// Value tables of up to kSellviSmemVals entries (32 KB) are staged in shared memory per CTA.
-constexpr int64_t kSellviSmemVals = 4096;
+// Value tables of up to kSellviSmemVals entries (64 KB) are staged in shared memory per CTA (C3's K₀:
+// 1,054 values; C4's: 4,147).  At U = 4 the kernel's 80 registers allow 3 CTAs of 256 threads per SM,
+// and 3 × 64 KB still fits the SM's shared memory, so staging never lowers the occupancy there.
+constexpr int64_t kSellviSmemVals = 8192;
 
 template <int U, class Epi, bool kSmem>
 void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
@@ -25,13 +27,16 @@ void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cuda
     // resident CTAs per SM of this instantiation at this table size (cached for the last size seen)
     static int per_sm = 0, per_sm_smem = -1;
     if (per_sm_smem != smem) {
+        if (kSmem)
+            CUDA_OK(cudaFuncSetAttribute(dev::k_sellvi<U, Epi, kSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kSellviSmemVals * 8)));
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sellvi<U, Epi, kSmem>, dev::kBlock, smem));
         per_sm = std::max(per_sm, 1);
         per_sm_smem = smem;
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
     dev::k_sellvi<U, Epi, kSmem><<<grid, dev::kBlock, smem, st>>>(
-        A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase, A.vtab, (int)A.nvals, g, A.nrows, epi,
+        A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase, A.vtab, (int)A.nvals, A.obits, g, A.nrows, epi,
         dotctx(D, dotkind), (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
 }
 

@@ -172,6 +172,25 @@ def test_sellvi_layout():
     assert seen >= 1  # at least C2's K_0 (159 distinct values) qualifies
 
 
+def test_sellvi_wide_offsets():
+    """SELL-VI words with more than 16 offset bits (rows spanning > 65535 columns, as at C4 and C5):
+    an SPD operator with couplings at distance 70000 (obits = 17, 15-bit value index) applied through
+    the SELL-VI core matches scipy's product."""
+    amg = _amg()
+    import scipy.sparse as sp
+    n, far = 150000, 70000
+    A = (sp.diags([4.0], [0], shape=(n, n)) - sp.diags([1.0, 1.0], [-1, 1], shape=(n, n))
+         - sp.diags([0.5, 0.5], [-far, far], shape=(n, n))).tocsr()
+    A.sort_indices()
+    H = amg.Hierarchy(A, amg.params(2, format=6))
+    c = H.op_config(0, 0)
+    assert c["layout"] == "sellvi"
+    x = np.random.default_rng(4).uniform(-1, 1, n)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    H.apply(0, 0, dev(x), y)
+    assert np.allclose(y.cpu().numpy(), A @ x, rtol=0, atol=1e-13 * 7)
+
+
 def test_value_index_table():
     """CSR-VI (kernel bit 3): the value table of C2's K_0 holds exactly the distinct stored values
     (the operator's values and the 0.0 of the row padding, counted here by numpy on the host K), the

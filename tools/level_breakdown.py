@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--solves", type=int, default=3)
+    ap.add_argument("--per-rank-setup", action="store_true",
+                    help="every rank builds the global hierarchy itself (no shared setup)")
     args = ap.parse_args()
     os.environ.setdefault("AMG_GRAPHS", "0")
     os.environ.setdefault("AMG_PROF_LEVELS", "1")
@@ -33,10 +35,16 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
     c = amg_inputs.CONFIGS[args.config]
-    K, F = amg.iga_poisson(c["dim"], c["p"], c["n"], rhs=2)
+    amg.set_num_threads(len(os.sched_getaffinity(0)))
+    K, F = amg.iga_poisson(c["dim"], c["p"], c["n"], rhs=2, geometry=c.get("geometry", 0))
     prm = amg.params(c["p"], krylov=1, coarse_solver=1)
-    H = amg.Hierarchy(K, prm, dist=amg.make_dist(rank, world, device=int(os.environ.get("LOCAL_RANK", "0")))
-                      if world > 1 else None)
+    if world > 1 and args.per_rank_setup:
+        H = amg.Hierarchy(K, prm, dist=amg.make_dist(rank, world, device=int(os.environ.get("LOCAL_RANK", "0"))))
+    elif world > 1:  # one host setup (rank 0), shares to every rank
+        H = amg.setup_distributed(K if rank == 0 else None, prm, rank, world,
+                                  device=int(os.environ.get("LOCAL_RANK", "0")))
+    else:
+        H = amg.Hierarchy(K, prm)
     b, e = H.local_rows()
     Fd = torch.from_numpy(np.ascontiguousarray(F[b:e])).cuda()
     H.solve(Fd)
@@ -47,7 +55,9 @@ def main():
     t = H.level_times()
     out = {"rank": rank, "world": world, "transport": os.environ.get("AMG_TRANSPORT", "p2p"),
            "iters_per_solve": its / args.solves, "ms_per_vcycle_by_level": [round(v, 4) for v in t],
-           "total_ms_per_vcycle": round(sum(t), 4), "levels_N": H.info()["N"]}
+           "total_ms_per_vcycle": round(sum(t), 4), "levels_N": H.info()["N"],
+           "ops": [[(lambda c: f'{c["layout"]}/{c["kernel"]}/G{c["G"]}U{c["U"]}')(H.op_config(l, k))
+                    for k in range(3) if l + 1 < len(t) or k == 0] for l in range(len(t) - 1)]}
     if world > 1:
         parts = [None] * world
         dist.all_gather_object(parts, out)
