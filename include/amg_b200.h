@@ -111,7 +111,8 @@ typedef struct {
     int max_levels;         /* 20                                                                 */
     int format;             /* device matrix format: 0 auto (K_l and P̄_l with >= 2e6 non-zeros whose
                                column offsets (>= 16 bits, <= 24) and distinct-value indices fit one
-                               32-bit word, and <= 50 % slice padding: SELL-VI, a fixed rule; every
+                               32-bit word, <= 50 % slice padding, sampled row-to-row locality and, for
+                               rows longer than 64 entries, <= 8192 distinct values: SELL-VI, a fixed rule; every
                                other operator: CSR rows padded to 8 with the
                                kernel, column and value source autotuned), 1 CSR warp-per-row,
                                2 SELL-32 (row per lane), 3 TMA-staged CSR, 4 CSR with 16-bit column

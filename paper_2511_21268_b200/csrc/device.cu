@@ -344,6 +344,11 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
             }
         }
         if (samples == 0 || (lines + 0.5 * vals) / (double)samples > 12.0) return false;
+        // Long rows with a table too large for shared memory: every lookup is an L2 gather, and a K_ℓ
+        // with ~700 entries per row then runs ≈ 3× slower than in CSR (a coarse K₁ share on an interior
+        // rank of a 4-GPU C3 run passed the test above with < 65,536 values; level 1 took 3.0 instead of
+        // 0.95 ms per V-cycle).  Short rows (P̄_ℓ, ≤ 64 entries) keep SELL-VI with a global table.
+        if ((int64_t)tab.size() > kSellviSmemVals && nnz > 64 * n) return false;
     }
     uint32_t zero = 0;
     for (size_t t = 0; t < tab.size(); t++) {

@@ -33,6 +33,11 @@ struct DevBuf {
 //   SELL-VI (fmt 2): 32-row slices, one row per lane, one 32-bit word per entry (16-bit column offset
 //     from rbase | 16-bit value index into vtab) in lane-interleaved quads; soff = slice offsets in
 //     quads per lane; G = 32.
+// SELL-VI value tables of up to kSellviSmemVals entries (64 KB) are staged in shared memory per CTA
+// (C3's K₀: 1,054 values; C4's: 4,147).  At U = 4 the kernel's 80 registers allow 3 CTAs of 256 threads
+// per SM, and 3 × 64 KB still fits the SM's shared memory, so staging never lowers the occupancy there.
+constexpr int64_t kSellviSmemVals = 8192;
+
 struct DCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
     int fmt = 0;

@@ -14,10 +14,7 @@ void launch_csr_vi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStr
     else launch_csr_cols(D, A, dev::ColsI32V32{A.ci, A.vidx, A.vtab}, g, epi, st, dotkind);
 }
 
-// Value tables of up to kSellviSmemVals entries (64 KB) are staged in shared memory per CTA (C3's K₀:
-// 1,054 values; C4's: 4,147).  At U = 4 the kernel's 80 registers allow 3 CTAs of 256 threads per SM,
-// and 3 × 64 KB still fits the SM's shared memory, so staging never lowers the occupancy there.
-constexpr int64_t kSellviSmemVals = 8192;
+// Value tables of up to kSellviSmemVals entries are staged in shared memory per CTA (devstate.cuh).
 
 template <int U, class Epi, bool kSmem>
 void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {

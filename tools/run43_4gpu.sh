@@ -2,6 +2,7 @@
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build43.log 2>&1; echo build=$?
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -k "sellvi" > gpurun_out/parity43.log 2>&1; echo parity=$?; tail -2 gpurun_out/parity43.log
 export AMG_TUNE_CACHE=$PWD/gpurun_out/tune43.txt
 run() {  # name, extra env..., then args
   name=$1; shift
