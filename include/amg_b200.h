@@ -236,6 +236,11 @@ typedef struct {
     int64_t nnz;
     int64_t n_values;
     int value_index_bytes;
+    int sellvi_parts;       /* SELL-VI: quad-range parts (1, 2, 4; one warp each) of the 32-row slices of
+                               the last round of work items, so that round is short (env
+                               AMG_SELLVI_PARTS=k forces 2^k parts on every slice); the rows of a split
+                               slice sum their parts' chains in part order.  0 other layouts */
+    int offset_bits;        /* SELL-VI: column-offset bits of an entry word (16..24); 0 other layouts */
 } amg_op_config;
 amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
 /* Force the kernel configuration of one CSR-layout operator (experiments and the kernel-equivalence

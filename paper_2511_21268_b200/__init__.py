@@ -342,7 +342,8 @@ class Hierarchy:
             name = "sellvi"
         return dict(layout=("csr", "sell32", "sellvi")[c.layout], kernel=name, kernel_bits=k, G=c.G, U=c.U,
                     stored=c.stored, nnz=c.nnz, alg_bytes=c.alg_bytes, tuned_us=round(c.tuned_us, 2),
-                    n_values=c.n_values, value_index_bytes=c.value_index_bytes)
+                    n_values=c.n_values, value_index_bytes=c.value_index_bytes, sellvi_parts=c.sellvi_parts,
+                    offset_bits=c.offset_bits)
 
     def set_op_config(self, level: int, op: int, kernel: int, G: int, U: int) -> None:
         check(lib().amg_operator_set_config(self._h, level, op, kernel, G, U))

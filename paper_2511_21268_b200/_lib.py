@@ -63,7 +63,7 @@ class amg_kernel_stats(C.Structure):
 class amg_op_config(C.Structure):
     _fields_ = [("layout", C.c_int), ("kernel", C.c_int), ("G", C.c_int), ("U", C.c_int), ("stored", C.c_int64),
                 ("tuned_us", C.c_double), ("alg_bytes", C.c_double), ("nnz", C.c_int64), ("n_values", C.c_int64),
-                ("value_index_bytes", C.c_int)]
+                ("value_index_bytes", C.c_int), ("sellvi_parts", C.c_int), ("offset_bits", C.c_int)]
 
 
 class amg_dist_view(C.Structure):

@@ -384,6 +384,35 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     CUDA_OK(cudaMemcpy(out.vpk, w.data(), sizeof(uint32_t) * stored, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.rbase, base.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(out.vtab, tab.data(), sizeof(double) * out.nvals, cudaMemcpyHostToDevice));
+    // Tail split (k_sellvi): a slice is one warp's work item, and with few slices per resident warp the
+    // last round runs a handful of slices on an idle GPU — a 4-GPU share of C3's K₀ has 7,353 slices
+    // for ≈ 3,552 resident warps (24 per SM at U = 4): 3 rounds for 2.07 rounds of work.  The slices of
+    // that last round (counted against the nominal 24 · n_SM warps, not the tuned grid, so the split
+    // is a function of the operator alone) are split into 2^lparts ranges of consecutive quads (≤ 4
+    // parts of ≥ 8 quads, enough items to fill the round).  A split slice sums its parts' chains in
+    // part order — fixed, never dependent on timing; dot epilogues keep whole slices.
+    {
+        const int64_t wnom = 24 * (int64_t)D.nsm, tail = nsl % wnom;
+        const int64_t avgq = (stored / 128) / std::max<int64_t>(nsl, 1);
+        int lp = 0;
+        // only where the tail is a large share of the work (≤ 4 full rounds: the multi-GPU shares); at
+        // C3 on 1 GPU (8 full rounds) the split items' fence, atomic and dependent epilogue load cost
+        // as much as the shortened tail saves (232.7 vs 230.1 µs, run 48)
+        const bool few = nsl / wnom <= 4;
+        while (few && tail > 0 && lp < 2 && (tail << lp) < wnom && avgq >= 8 * (2 << lp)) lp++;
+        int64_t nwhole = nsl - tail;
+        if (const char *e = std::getenv("AMG_SELLVI_PARTS")) {  // experiments / tests: every slice split
+            lp = std::max(0, std::min(3, std::atoi(e)));
+            nwhole = 0;
+        }
+        out.lparts = lp;
+        out.nwhole = lp ? nwhole : nsl;
+        if (lp > 0) {
+            out.partial = D.alloc_n<double2>((nsl * 32) << lp);
+            out.sticket = D.alloc_n<unsigned>(nsl);
+            CUDA_OK(cudaMemset(out.sticket, 0, sizeof(unsigned) * nsl));
+        }
+    }
     return true;
 }
 
@@ -1861,6 +1890,8 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     cfg->nnz = A.nnz;
     cfg->n_values = A.nvals;
     cfg->value_index_bytes = !A.vtab ? 0 : (A.fmt == 2 || (A.vpk && (A.kern & 2))) ? 2 : 4;
+    cfg->sellvi_parts = A.fmt == 2 ? 1 << A.lparts : 0;
+    cfg->offset_bits = A.fmt == 2 ? A.obits : 0;
     return AMG_OK;
     API_END
 }

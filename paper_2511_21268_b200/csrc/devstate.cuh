@@ -65,6 +65,13 @@ struct DCsr {
     uint32_t *vidx = nullptr;
     uint32_t *vpk = nullptr;
     int obits = 16;  // SELL-VI: column-offset bits of a word (the value index takes the other 32 − obits)
+    // SELL-VI: the slices of the last (partial) round — slice positions >= nwhole — are split into
+    // 2^lparts parts of consecutive quads, one warp each, so the tail round is short; partial = the
+    // parts' two chains per row, sticket = per-slice arrival counters (zero between launches)
+    int lparts = 0;
+    int64_t nwhole = 0;
+    double2 *partial = nullptr;
+    unsigned *sticket = nullptr;
     // bytes one application must stream from HBM for this operator (values of the nnz stored entries
     // or their value indices + the value table, the column data of the chosen source, row pointers);
     // vectors are counted by the caller

@@ -1009,7 +1009,8 @@ template <int U, class Epi, bool kSmem>
 __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
                                                    const int *__restrict__ rbase, const double *__restrict__ gtable,
                                                    int nvals, int obits, const double *__restrict__ g, int64_t nrows,
-                                                   Epi epi, DotCtx dc, P2P pp) {
+                                                   Epi epi, DotCtx dc, P2P pp, int64_t nwhole, int lparts,
+                                                   double2 *partial, unsigned *sticket) {
     const unsigned omask = (1u << obits) - 1u;
     const double *table = gtable;
     if constexpr (kSmem) {
@@ -1025,22 +1026,36 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
     typename Epi::Acc dacc{};
     bool signalled = pp.gorder == nullptr || pp.nranks == 0;
     if (!signalled && warp < pp.nbnd) peer_wait_warp(pp);
-    for (int64_t pos = warp; pos < nslices; pos += nwarps) {
-        if (!signalled && pos >= pp.nbnd) {
+    // work items: slice positions [0, nwhole) whole, then every later position split into 2^lparts parts
+    const int64_t nitems = nwhole + ((nslices - nwhole) << lparts);
+    const int64_t nbnd_items = pp.nbnd <= nwhole ? pp.nbnd : nwhole + ((pp.nbnd - nwhole) << lparts);
+    for (int64_t it = warp; it < nitems; it += nwarps) {
+        if (!signalled && it >= nbnd_items) {
             peer_signal_warp(pp);
             signalled = true;
         }
+        int64_t pos = it;
+        int part = 0, lp = 0;
+        if (it >= nwhole) {
+            pos = nwhole + ((it - nwhole) >> lparts);
+            part = (int)((it - nwhole) & ((1 << lparts) - 1));
+            lp = lparts;
+        }
+        const int parts = 1 << lp;
         const int64_t sl = pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos;
         const int64_t off = __ldg(soff + sl);
-        const int W4 = (int)(__ldg(soff + sl + 1) - off);
+        const int W4s = (int)(__ldg(soff + sl + 1) - off);
+        // this item's quads [q0, q0 + W4) of the slice (the whole slice when parts == 1)
+        const int q0 = (int)(((int64_t)W4s * part) >> lp);
+        const int W4 = (int)(((int64_t)W4s * (part + 1)) >> lp) - q0;
         const int64_t row = (sl << 5) + lane;
         typename Epi::Pre pre{};
         int b = 0;
         if (row < nrows) {
             b = __ldg(rbase + row);
-            pre = epi.load(row);
+            if (parts == 1) pre = epi.load(row);
         }
-        const uint4 *wp = w + (off << 5) + lane;
+        const uint4 *wp = w + ((off + q0) << 5) + lane;
         double s0 = 0.0, s1 = 0.0;
         int q = 0;
         // software pipeline: the next batch's words are requested before this batch's gathers, so the
@@ -1087,7 +1102,32 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
             s0 = fma(va[2], xa[2], s0);
             s1 = fma(va[3], xa[3], s1);
         }
-        if (row < nrows) acc_add(dacc, epi(row, s0 + s1, pre));
+        if (parts == 1) {
+            if (row < nrows) acc_add(dacc, epi(row, s0 + s1, pre));
+            continue;
+        }
+        // split slice: deposit this part's two chains; the warp completing the slice's last part sums
+        // the parts' chains in part order (fixed, whichever warp arrives last) and runs the epilogue
+        const int64_t npad = nslices << 5;
+        __stcg(partial + (int64_t)part * npad + row, make_double2(s0, s1));
+        __threadfence();
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) last = atomicAdd(sticket + sl, 1u) == (unsigned)(parts - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+        double c0 = 0.0, c1 = 0.0;
+        for (int j = 0; j < parts; j++) {
+            const double2 v = __ldcg(partial + (int64_t)j * npad + row);
+            c0 += v.x;
+            c1 += v.y;
+        }
+        if (lane == 0) sticket[sl] = 0u;  // every part has arrived: reset for the next launch
+        if (row < nrows) {
+            pre = epi.load(row);
+            acc_add(dacc, epi(row, c0 + c1, pre));
+        }
     }
     if (!signalled) peer_signal_warp(pp);
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);

@@ -31,10 +31,14 @@ void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cuda
         per_sm = std::max(per_sm, 1);
         per_sm_smem = smem;
     }
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
+    const int lparts = Epi::kDot ? 0 : A.lparts;  // dot epilogues keep whole slices (fixed dot order)
+    const int64_t nwhole = lparts ? A.nwhole : nsl;
+    const int64_t nitems = nwhole + ((nsl - nwhole) << lparts);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nitems + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
     dev::k_sellvi<U, Epi, kSmem><<<grid, dev::kBlock, smem, st>>>(
         A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase, A.vtab, (int)A.nvals, A.obits, g, A.nrows, epi,
-        dotctx(D, dotkind), (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
+        dotctx(D, dotkind), (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)),
+        nwhole, lparts, A.partial, A.sticket);
 }
 
 template <int U, class Epi>

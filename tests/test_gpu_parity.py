@@ -197,6 +197,37 @@ def test_sellvi_wide_offsets():
     assert np.allclose(y.cpu().numpy(), A @ x, rtol=0, atol=1e-13 * 12)
 
 
+@pytest.mark.parametrize("lparts", [1, 2, 3])
+def test_sellvi_split_slices(lparts, monkeypatch):
+    """SELL-VI slices split into 2^lparts quad ranges, one warp each (the tail round's setting, forced
+    on every slice here by AMG_SELLVI_PARTS): K_0 of C2 matches the oracle's SpMV, the solve converges in the
+    unsplit solve's iterations to the same solution (only the order of the two partial sums per part
+    changes), and U does not change the bits."""
+    amg = _amg()
+    K, F, H0, Ho = build("C2", 6)
+    monkeypatch.setenv("AMG_SELLVI_PARTS", str(lparts))
+    H = amg.Hierarchy(amg.iga_poisson(*CASES["C2"])[0], amg.params(CASES["C2"][1], format=6))
+    c = H.op_config(0, 0)
+    assert c["layout"] == "sellvi" and c["sellvi_parts"] == 1 << lparts
+    A = Ho.levels[0].K.tocsr()
+    x = dev(np.random.default_rng(12).uniform(-1, 1, A.shape[0]))
+    ys = []
+    for U in (1, 2, 4):
+        H.set_op_config(0, 0, 0, 32, U)
+        y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+        H.apply(0, 0, x, y)
+        ys.append(y.cpu().numpy())
+    xo = x.cpu().numpy()
+    assert all(np.array_equal(y, ys[0]) for y in ys)
+    assert np.all(np.abs(ys[0] - oracle.spmv(A, xo)) <= 1e-13 * (abs(A) @ np.abs(xo)) + 1e-300)
+    Fd = dev(F)
+    u0, it0 = H0.solve(Fd, rtol=1e-8, maxit=200)[:2]
+    u1, it1 = H.solve(Fd, rtol=1e-8, maxit=200)[:2]
+    assert it1 == it0
+    u0, u1 = u0.cpu().numpy(), u1.cpu().numpy()
+    assert np.linalg.norm(u1 - u0) <= 1e-10 * np.linalg.norm(u0)
+
+
 def test_value_index_table():
     """CSR-VI (kernel bit 3): the value table of C2's K_0 holds exactly the distinct stored values
     (the operator's values and the 0.0 of the row padding, counted here by numpy on the host K), the

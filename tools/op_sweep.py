@@ -28,10 +28,13 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--sell", action="store_true", help="also time the SELL-32 layout")
     ap.add_argument("--format", type=int, default=0, help="amg_params.format of the swept hierarchy")
+    ap.add_argument("--n", type=int, default=0, help="override the config's elements per direction")
     args = ap.parse_args()
     import torch
     import paper_2511_21268_b200 as amg
-    c = amg_inputs.CONFIGS[args.config]
+    c = dict(amg_inputs.CONFIGS[args.config])
+    if args.n:
+        c["n"] = args.n
     K, F = amg.iga_poisson(c["dim"], c["p"], c["n"])
     H = amg.Hierarchy(K, amg.params(c["p"], format=args.format))
     del K
