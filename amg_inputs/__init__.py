@@ -19,6 +19,7 @@ C5     3    2    250+  weak scaling, ~16M DOFs per GPU (n = 250/315/398/502)
 C5s    3    2    158+  weak scaling, ~4M DOFs per GPU (n = 158/200/252/317)
 R3     3    3    96    thick quarter ring (NEXT-3, Table 3)
 R4     3    4    96    thick quarter ring, the paper's GPU ring case
+L3     3    3    96    three-patch L-shape, the paper's GPU multipatch case (NEXT-4, Table 2)
 =====  ===  ===  ====  =====================================================
 """
 from __future__ import annotations
@@ -41,6 +42,9 @@ CONFIGS = {
     "R3": dict(dim=3, p=3, n=96, geometry=1),
     # the paper's GPU ring case (k=96 p=4, 970,200 DOFs; 6.234 s on one A30)
     "R4": dict(dim=3, p=4, n=96, geometry=1),
+    # NEXT-4: the three-patch L-shape, the paper's GPU multipatch case (P:L2674,
+    # L2779: k=96 p=3, Table 2b 2,775,752 DOFs; 4.636 s on one A30); the paper's L-shape data
+    "L3": dict(dim=3, p=3, n=96, geometry=2),
 }
 C5_WEAK_N = {1: 250, 2: 315, 4: 398, 8: 502}
 C5S_WEAK_N = {1: 158, 2: 200, 4: 252, 8: 317}

@@ -345,14 +345,16 @@ def run_gpu(args) -> None:
             "scaling": wl["scaling"],
             "vs_baseline": None,
             "dtype": "f64",
-            "data": ("synthetic: generated quarter-ring IgA system with the paper's ring data (u = e^x sin(xy) cos z, "
+            "data": ("synthetic: generated three-patch L-shape IgA system with the paper's L-shape data (u = e^x "
+                     "sin(xy) cos z, projected Dirichlet + Neumann loads)" if paper and geom == 2 else
+                     "synthetic: generated quarter-ring IgA system with the paper's ring data (u = e^x sin(xy) cos z, "
                      "projected Dirichlet + Neumann loads)" if paper and geom == 1 else
                      "synthetic: generated IgA system with the paper's own cube data (f = −e^{x+z} sin y, "
                      "projected Dirichlet + Neumann loads)" if paper else
                      "synthetic: generated quarter-ring IgA system, seeded uniform(−1,1) RHS" if geom == 1 else
                      "synthetic (generated IgA Poisson system, manufactured-solution RHS)"),
             "config": {
-                "workload": f"{args.config}: {dim}-D Poisson on the " + ("thick quarter ring" if geom == 1 else "cube")
+                "workload": f"{args.config}: {dim}-D Poisson on the " + ("thick quarter ring" if geom == 1 else "three-patch L-shape" if geom == 2 else "cube")
                             + f", B-spline p={p}, n={n} elements/dir, {N} free DOFs, "
                             + ("the paper's experiment (its data, FCG, §5.1 coarse CG)" if paper else
                                "random RHS, PCG" if geom == 1 else "manufactured sine RHS, PCG") + f", rtol {args.rtol}",
@@ -421,6 +423,12 @@ def _oracle_sample(cfg: str):
     if wl.get("geometry", 0) == 1:
         from oracle import ring
         return ring.assemble_ring(wl["p"], wl["n"])
+    if wl.get("geometry", 0) == 2:
+        # the L-shape operator is input data for the timed oracle sweeps: the library's generator is
+        # bitwise lshape.assemble_lshape (test_lshape_operator_bitwise_equal_to_oracle), whose numpy
+        # gluing needs ~10 GB of index arrays at k = 96
+        import paper_2511_21268_b200 as amg
+        return amg.iga_poisson(wl["dim"], wl["p"], wl["n"], rhs=1, geometry=2)[0].to_scipy()
     return oracle.assemble(wl["dim"], wl["p"], wl["n"])
 
 

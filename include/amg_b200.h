@@ -76,6 +76,18 @@ typedef struct {
  *          once), entry ((A·B)·M + (C·D)·M) + (E·B)·K.  rhs = 1: F = 0; rhs = 2: the paper's ring data
  *          (u = e^x sin(xy) cos z, f and g_N of eq:Lshapedcoeff; g_D by one L2 projection
  *          onto sides 1-3; source by (p+1)³ Gauss points through the map).
+ *
+ * geometry = 2: the three-patch thick L-shape (multipatch gluing P:L575-583; readings
+ *          N4.a/N4.b of DESIGN.md §3; dim 3, dirichlet_sides must be 0x7 and is otherwise unused):
+ *          patches A = [0,1]³, B = [1,2]×[0,1]², C = [0,1]×[1,2]×[0,1], each the unit-cube space of
+ *          degree p on n³ elements, interface functions identified (C⁰).  Control lattice
+ *          0 ≤ x, y ≤ 2m−2, 0 ≤ z ≤ m−1 without x, y ≥ m (m = n+p); Dirichlet faces x=0, y=0, x=2, y=2,
+ *          z=0, z=1; Neumann faces y=1 (on B) and x=1 (on C).  Free DOFs lexicographic, x fastest
+ *          (sizes: Table 2b).  Entries: Σ over the patches holding both functions, in order A, B, C,
+ *          of the cube entry.  rhs = 0: F_i = ∫ φ_i (f = 1, homogeneous data); rhs = 1: F = 0;
+ *          rhs = 2: the paper's L-shape data (u = e^x sin(xy) cos z, its f, g_N on the
+ *          two Neumann faces, g_D by one joint L2 projection onto the glued Dirichlet faces, lifting;
+ *          fp64 (p+1)-point Gauss).
  */
 typedef struct {
     int dim;
@@ -83,7 +95,7 @@ typedef struct {
     int n_elem;
     uint32_t dirichlet_sides;
     int rhs;
-    int geometry; /* 0 unit square / cube, 1 thick quarter ring (dim 3) */
+    int geometry; /* 0 unit square / cube, 1 thick quarter ring (dim 3), 2 three-patch L-shape (dim 3) */
 } amg_iga_desc;
 
 amg_status amg_iga_poisson(const amg_iga_desc *desc, amg_csr **K, double **F);

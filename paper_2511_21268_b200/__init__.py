@@ -48,7 +48,8 @@ def _from_c(ptr) -> HostCsr:
 
 
 def iga_poisson(dim: int, p: int, n: int, dirichlet_sides: int = 0b000111, rhs: int = 0, geometry: int = 0):
-    """amg_iga_poisson: (K as HostCsr, F as numpy fp64).  geometry 1 = the thick quarter ring (dim 3)."""
+    """amg_iga_poisson: (K as HostCsr, F as numpy fp64).  geometry 1 = the thick quarter ring (dim 3),
+    geometry 2 = the three-patch L-shape (dim 3; rhs 0: f = 1, 1: F = 0, 2: its paper data)."""
     d = _lib.amg_iga_desc(dim, p, n, dirichlet_sides, rhs, geometry)
     Kp = C.POINTER(_lib.amg_csr)()
     Fp = C.POINTER(C.c_double)()

@@ -98,7 +98,10 @@ amg_status amg_iga_poisson(const amg_iga_desc *d, amg_csr **K, double **F) {
     if (d->n_elem < 1) throw Error{AMG_EINVAL, "n_elem must be >= 1"};
     if (d->dirichlet_sides >> (2 * d->dim)) throw Error{AMG_EINVAL, "dirichlet_sides names a side > 2*dim"};
     if (d->rhs < 0 || d->rhs > 2) throw Error{AMG_EINVAL, "rhs must be 0, 1 or 2"};
-    if (d->geometry < 0 || d->geometry > 1) throw Error{AMG_EINVAL, "geometry must be 0 (cube) or 1 (quarter ring)"};
+    if (d->geometry < 0 || d->geometry > 2)
+        throw Error{AMG_EINVAL, "geometry must be 0 (cube), 1 (quarter ring) or 2 (three-patch L-shape)"};
+    if (d->geometry == 2 && (d->dim != 3 || d->dirichlet_sides != 0b000111u))
+        throw Error{AMG_EINVAL, "the L-shape is 3-D with its fixed boundary layout (dirichlet_sides = 0x7)"};
     if (d->geometry == 1 && (d->dim != 3 || d->rhs == 0 || d->dirichlet_sides != 0b000111u))
         throw Error{AMG_EINVAL, "the quarter ring is 3-D with Dirichlet sides 1,2,3 and rhs = 1 (F = 0) or 2 (its paper data)"};
     HCsr A;

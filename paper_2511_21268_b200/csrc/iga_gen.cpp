@@ -552,11 +552,264 @@ void paper_ring_load(int p, int n, const RingTables &RT, const int *lo, const in
     }
 }
 
+// Three-patch thick L-shape (geometry 2; PAPER.md P:L575-583 gluing, P:L1074-1089 the benchmark;
+// readings N4.a/N4.b of DESIGN.md §3).  Patches A = [0,1]³, B = [1,2]×[0,1]², C = [0,1]×[1,2]×[0,1],
+// each the unit-cube B-spline space of degree p on n³ elements (identity Jacobian).  Control lattice
+// {0 ≤ x, y ≤ 2m−2, 0 ≤ z ≤ m−1} minus {x ≥ m and y ≥ m}; patch lattice offsets (0,0), (m−1,0),
+// (0,m−1); the re-entrant edge x = y = m−1 belongs to all three.  Dirichlet faces: x = 0, y = 0,
+// x = 2m−2 (B), y = 2m−2 (C), z = 0, z = m−1.  Free DOFs lexicographic, x fastest.  An entry is the
+// sum over the patches holding both functions, in patch order A, B, C, of the cube entry
+// ((K·M)·M + (M·K)·M) + (M·M)·K in local indices — structurally present when some patch holds both.
+// rhs = 0: F = ∫ φ_i (source f = 1, homogeneous data); rhs = 1: F = 0.
+void lshape_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
+    const int p = d.degree, n = d.n_elem, m = n + p, bw = 2 * p + 1, Mx = 2 * m - 1;
+    const Tables1D T = physical_tables(p, n);
+    const double *M1 = T.M.data(), *K1 = T.K.data();
+    auto inside = [&](int x, int y) { return !(x >= m && y >= m); };
+    auto dirichlet = [&](int x, int y, int z) {
+        return x == 0 || y == 0 || (x == Mx - 1 && y <= m - 1) || (y == Mx - 1 && x <= m - 1) || z == 0 || z == m - 1;
+    };
+    const int ox[3] = {0, m - 1, 0}, oy[3] = {0, 0, m - 1};
+    auto holds = [&](int P, int x, int y) { return x >= ox[P] && x <= ox[P] + m - 1 && y >= oy[P] && y <= oy[P] + m - 1; };
+    const size_t lat = (size_t)Mx * Mx * m;
+    std::vector<int64_t> idx(lat, -1);
+    std::vector<int32_t> px, py, pz;
+    int64_t N = 0;
+    for (int z = 0; z < m; z++)
+        for (int y = 0; y < Mx; y++)
+            for (int x = 0; x < Mx; x++)
+                if (inside(x, y) && !dirichlet(x, y, z)) {
+                    idx[((size_t)z * Mx + y) * Mx + x] = N++;
+                    px.push_back(x); py.push_back(y); pz.push_back(z);
+                }
+    if (N > INT32_MAX) throw Error{AMG_EINVAL, "more than 2^31-1 free DOFs (int32 columns)"};
+    auto tab = [&](const double *t, int a, int a2) { return t[(size_t)a * bw + (a2 - a + p)]; };
+    // visit the columns of row r in ascending order; emit(col, value)
+    auto row_visit = [&](int64_t r, auto &&emit) {
+        const int x = px[r], y = py[r], z = pz[r];
+        for (int z2 = std::max(z - p, 0); z2 <= std::min(z + p, m - 1); z2++)
+            for (int y2 = std::max(y - p, 0); y2 <= std::min(y + p, Mx - 1); y2++)
+                for (int x2 = std::max(x - p, 0); x2 <= std::min(x + p, Mx - 1); x2++) {
+                    const int64_t col = idx[((size_t)z2 * Mx + y2) * Mx + x2];
+                    if (col < 0) continue;
+                    double val = 0.0;
+                    bool any = false;
+                    for (int P = 0; P < 3; P++) {
+                        if (!holds(P, x, y) || !holds(P, x2, y2)) continue;
+                        const int a = x - ox[P], a2 = x2 - ox[P], b = y - oy[P], b2 = y2 - oy[P];
+                        const double t1 = (tab(K1, a, a2) * tab(M1, b, b2)) * tab(M1, z, z2);
+                        const double t2 = (tab(M1, a, a2) * tab(K1, b, b2)) * tab(M1, z, z2);
+                        const double t3 = (tab(M1, a, a2) * tab(M1, b, b2)) * tab(K1, z, z2);
+                        val += (t1 + t2) + t3;
+                        any = true;
+                    }
+                    if (any) emit(col, val);
+                }
+    };
+    K.nrows = K.ncols = N;
+    K.rp.alloc(N + 1);
+    K.rp[0] = 0;
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t r = 0; r < N; r++) {
+        int64_t cnt = 0;
+        row_visit(r, [&](int64_t, double) { cnt++; });
+        K.rp[r + 1] = cnt;
+    }
+    for (int64_t r = 0; r < N; r++) K.rp[r + 1] += K.rp[r];
+    K.ci.alloc(K.rp[N]);
+    K.v.alloc(K.rp[N]);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t r = 0; r < N; r++) {
+        int64_t k = K.rp[r];
+        row_visit(r, [&](int64_t col, double v) { K.ci[k] = (int32_t)col; K.v[k] = v; k++; });
+    }
+    F.alloc(N);
+    if (d.rhs == 1) {
+        std::memset(F.data(), 0, sizeof(double) * N);
+        return;
+    }
+    if (d.rhs == 2) {
+        // The paper's L-shape data (reading N4.b): u = e^x sin(xy) cos z,
+        // f = cos z · e^x [−2y cos(xy) + (x²+y²) sin(xy)], g_N = ∂u/∂y on y=1 (B), ∂u/∂x on x=1 (C),
+        // g_D = u by one joint L2 projection onto the glued Dirichlet faces (Jacobi-CG to round-off),
+        // F_free = (source + Neumann)_free − (K_all u_D)_free.  fp64 (p+1)-point Gauss per element.
+        const int nq = n * (p + 1);
+        std::vector<q128> gx, gw;
+        gauss_legendre_q(p + 1, gx, gw);
+        std::vector<double> qx(nq), qw(nq), qv((size_t)nq * (p + 1));
+        std::vector<int> qe(nq);
+        {
+            q128 val[16], der[16];
+            for (int e = 0; e < n; e++)
+                for (int q = 0; q <= p; q++) {
+                    const int k = e * (p + 1) + q;
+                    basis_and_derivs(e + p, e + gx[q], p, n, val, der);
+                    qx[k] = (double)((e + gx[q]) / n);
+                    qw[k] = (double)(gw[q] / n);
+                    qe[k] = e;
+                    for (int i = 0; i <= p; i++) qv[(size_t)k * (p + 1) + i] = (double)val[i];
+                }
+        }
+        const size_t lat = (size_t)Mx * Mx * m;
+        auto L = [&](int x, int y, int z) { return ((size_t)z * Mx + y) * Mx + x; };
+        // 2-D moments G[u][v] = ∫∫ g(s, t) N_u(s) N_v(t) over the unit square
+        auto moments2 = [&](auto &&g) {
+            std::vector<double> G((size_t)m * m, 0.0);
+            for (int i = 0; i < nq; i++)
+                for (int j = 0; j < nq; j++) {
+                    const double gv = g(qx[i], qx[j]) * qw[i] * qw[j];
+                    for (int a = 0; a <= p; a++)
+                        for (int b = 0; b <= p; b++)
+                            G[(size_t)(qe[i] + a) * m + qe[j] + b] += gv * qv[(size_t)i * (p + 1) + a] * qv[(size_t)j * (p + 1) + b];
+                }
+            return G;
+        };
+        std::vector<double> Cz(m, 0.0);
+        for (int i = 0; i < nq; i++)
+            for (int a = 0; a <= p; a++) Cz[qe[i] + a] += std::cos(qx[i]) * qw[i] * qv[(size_t)i * (p + 1) + a];
+        auto uex = [](double x, double y, double z) { return std::exp(x) * std::sin(x * y) * std::cos(z); };
+        std::vector<double> Fall(lat, 0.0);
+        for (int P = 0; P < 3; P++) {  // source: G_P(a, b) · Cz(c)
+            const double sx = P == 1 ? 1.0 : 0.0, sy = P == 2 ? 1.0 : 0.0;
+            const std::vector<double> G = moments2([&](double s, double t) {
+                const double x = sx + s, y = sy + t;
+                return std::exp(x) * (-2.0 * y * std::cos(x * y) + (x * x + y * y) * std::sin(x * y));
+            });
+            for (int c = 0; c < m; c++)
+                for (int b = 0; b < m; b++)
+                    for (int a = 0; a < m; a++) Fall[L(a + ox[P], b + oy[P], c)] += G[(size_t)a * m + b] * Cz[c];
+        }
+        {  // Neumann: B's face y=1 (local b = m−1; in-face x, z), C's face x=1 (local a = m−1; in-face y, z)
+            const std::vector<double> GB = moments2([&](double s, double t) {
+                const double x = 1.0 + s;
+                return x * std::exp(x) * std::cos(x) * std::cos(t);
+            });
+            const std::vector<double> GC = moments2([&](double s, double t) {
+                const double y = 1.0 + s;
+                return std::cos(t) * M_E * (std::sin(y) + y * std::cos(y));
+            });
+            for (int c = 0; c < m; c++)
+                for (int u = 0; u < m; u++) {
+                    Fall[L(u + ox[1], m - 1, c)] += GB[(size_t)u * m + c];
+                    Fall[L(m - 1, u + oy[2], c)] += GC[(size_t)u * m + c];
+                }
+        }
+        // Dirichlet patch faces: (patch, fixed axis, end); in-face axes ascending
+        struct Face { int P, ax, end; };
+        const Face dfaces[12] = {{0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 2, 1}, {1, 0, 1}, {1, 1, 0},
+                                 {1, 2, 0}, {1, 2, 1}, {2, 0, 0}, {2, 1, 1}, {2, 2, 0}, {2, 2, 1}};
+        auto face_lat = [&](const Face &f, int u, int v) {  // lattice index of face-local (u, v)
+            int loc[3];
+            const int fa0 = f.ax == 0 ? 1 : 0, fa1 = f.ax == 2 ? 1 : 2;
+            loc[f.ax] = f.end ? m - 1 : 0;
+            loc[fa0] = u;
+            loc[fa1] = v;
+            return L(loc[0] + ox[f.P], loc[1] + oy[f.P], loc[2]);
+        };
+        std::vector<double> rhs(lat, 0.0), diag(lat, 0.0);
+        for (const Face &f : dfaces) {
+            const int fa0 = f.ax == 0 ? 1 : 0, fa1 = f.ax == 2 ? 1 : 2;
+            const double off[3] = {f.P == 1 ? 1.0 : 0.0, f.P == 2 ? 1.0 : 0.0, 0.0};
+            const std::vector<double> G = moments2([&](double s, double t) {
+                double X[3];
+                X[f.ax] = f.end ? 1.0 : 0.0;
+                X[fa0] = s;
+                X[fa1] = t;
+                return uex(X[0] + off[0], X[1] + off[1], X[2] + off[2]);
+            });
+            for (int u = 0; u < m; u++)
+                for (int v = 0; v < m; v++) {
+                    rhs[face_lat(f, u, v)] += G[(size_t)u * m + v];
+                    diag[face_lat(f, u, v)] += tab(M1, u, u) * tab(M1, v, v);
+                }
+        }
+        auto apply_bnd = [&](const std::vector<double> &x, std::vector<double> &y) {
+            std::fill(y.begin(), y.end(), 0.0);
+            for (const Face &f : dfaces) {  // serial: ≈ 12·m²·(2p+1)² flops, cheaper than 12 fork/joins
+                for (int u = 0; u < m; u++)
+                    for (int v = 0; v < m; v++) {
+                        double acc = 0.0;
+                        for (int u2 = std::max(0, u - p); u2 <= std::min(m - 1, u + p); u2++)
+                            for (int v2 = std::max(0, v - p); v2 <= std::min(m - 1, v + p); v2++)
+                                acc += tab(M1, u, u2) * tab(M1, v, v2) * x[face_lat(f, u2, v2)];
+                        y[face_lat(f, u, v)] += acc;  // one face's rows are distinct
+                    }
+            }
+        };
+        std::vector<double> xs(lat, 0.0), r(lat), z(lat), pp(lat), q(lat);
+        double rr = 0.0, bb = 0.0;
+        for (size_t i = 0; i < lat; i++) {
+            r[i] = rhs[i];
+            z[i] = diag[i] > 0.0 ? r[i] / diag[i] : 0.0;
+            pp[i] = z[i];
+            rr += r[i] * z[i];
+            bb += rhs[i] * rhs[i];
+        }
+        for (int it = 0; it < 100000 && bb > 0.0; it++) {
+            apply_bnd(pp, q);
+            double pq = 0.0;
+            for (size_t i = 0; i < lat; i++) pq += pp[i] * q[i];
+            if (!(pq > 0.0)) break;
+            const double alpha = rr / pq;
+            double rn = 0.0, rz = 0.0;
+            for (size_t i = 0; i < lat; i++) {
+                xs[i] += alpha * pp[i];
+                r[i] -= alpha * q[i];
+                rn += r[i] * r[i];
+                z[i] = diag[i] > 0.0 ? r[i] / diag[i] : 0.0;
+                rz += r[i] * z[i];
+            }
+            if (rn <= 1e-30 * bb) break;
+            const double beta = rz / rr;
+            for (size_t i = 0; i < lat; i++) pp[i] = z[i] + beta * pp[i];
+            rr = rz;
+        }
+        // lifting: F_free[r] = Fall[r] − Σ_j K_all(r, j) u_D[j] over the Dirichlet lattice points j
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t row = 0; row < N; row++) {
+            const int x = px[row], y = py[row], z0 = pz[row];
+            double lift = 0.0;
+            for (int z2 = std::max(z0 - p, 0); z2 <= std::min(z0 + p, m - 1); z2++)
+                for (int y2 = std::max(y - p, 0); y2 <= std::min(y + p, Mx - 1); y2++)
+                    for (int x2 = std::max(x - p, 0); x2 <= std::min(x + p, Mx - 1); x2++) {
+                        if (!inside(x2, y2) || !dirichlet(x2, y2, z2)) continue;
+                        const double u = xs[L(x2, y2, z2)];
+                        if (u == 0.0) continue;
+                        for (int P = 0; P < 3; P++) {
+                            if (!holds(P, x, y) || !holds(P, x2, y2)) continue;
+                            const int a = x - ox[P], a2 = x2 - ox[P], b = y - oy[P], b2 = y2 - oy[P];
+                            const double t1 = (tab(K1, a, a2) * tab(M1, b, b2)) * tab(M1, z0, z2);
+                            const double t2 = (tab(M1, a, a2) * tab(K1, b, b2)) * tab(M1, z0, z2);
+                            const double t3 = (tab(M1, a, a2) * tab(M1, b, b2)) * tab(K1, z0, z2);
+                            lift += ((t1 + t2) + t3) * u;
+                        }
+                    }
+            F[row] = Fall[L(x, y, z0)] - lift;
+        }
+        return;
+    }
+    // ∫ N_a over [0,1] = Σ_b M1[a, b] (partition of unity), summed in ascending b
+    std::vector<double> w1(m, 0.0);
+    for (int a = 0; a < m; a++)
+        for (int b = std::max(a - p, 0); b <= std::min(a + p, m - 1); b++) w1[a] += tab(M1, a, b);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < N; r++) {
+        double v = 0.0;
+        for (int P = 0; P < 3; P++)
+            if (holds(P, px[r], py[r])) v += (w1[px[r] - ox[P]] * w1[py[r] - oy[P]]) * w1[pz[r]];
+        F[r] = v;
+    }
+}
+
 }  // namespace
 
 void iga_tables_hat(int p, int n, double *mhat, double *khat) { hat_tables(p, n, mhat, khat); }
 
 void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
+    if (d.geometry == 2) {
+        lshape_assemble(d, K, F);
+        return;
+    }
     const int dim = d.dim, p = d.degree, n = d.n_elem, m = n + p, bw = 2 * p + 1;
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, nf[3] = {1, 1, 1};
     for (int ax = 0; ax < dim; ax++) {

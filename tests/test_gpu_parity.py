@@ -447,3 +447,43 @@ def test_ring_paper_experiment(p, n):
     assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
     ud = u.cpu().numpy()
     assert np.linalg.norm(F - oracle.spmv(K.to_scipy(), ud)) <= 1.05e-6 * np.linalg.norm(F)
+
+
+@pytest.mark.parametrize("p,n", [(2, 8), (3, 6)])
+def test_lshape_solve_matches_oracle(p, n):
+    """NEXT-4, the three-patch L-shape with a seeded random RHS: V-cycle to 1e-12, the
+    PCG iterate after the oracle's iteration count to 1e-10, counts ±1."""
+    from oracle import lshape
+    amg = _amg()
+    K, _ = amg.iga_poisson(3, p, n, rhs=1, geometry=2)
+    H = amg.Hierarchy(K, amg.params(p))
+    Ho = oracle.setup(lshape.assemble_lshape(p, n), oracle.OParams.for_degree(p))
+    r = amg_inputs.uniform_pm1(K.shape[0], seed=37)
+    zo = oracle.vcycle(Ho, r)
+    assert np.abs(H.vcycle(dev(r)).cpu().numpy() - zo).max() <= 1e-12 * np.abs(zo).max()
+    uo, ito, rro, histo, rco = oracle.pcg(Ho, r, rtol=1e-6, maxit=200)
+    u, it, rr, hist, st = H.solve(dev(r), rtol=1e-6, maxit=200)
+    assert rco == 0 and st == 0 and abs(it - ito) <= 1
+    u2 = H.solve(dev(r), rtol=0.0, maxit=ito)[0].cpu().numpy()
+    assert np.linalg.norm(u2 - uo) <= 1e-10 * np.linalg.norm(uo)
+
+
+@pytest.mark.parametrize("p,n", [(2, 8), (3, 6)])
+def test_lshape_paper_experiment(p, n):
+    """The paper's L-shape data (library rhs = 2 vs the oracle's load: source, Neumann faces y=1 on B
+    and x=1 on C, joint L2 Dirichlet projection, lifting), FCG with the §5.1 coarse CG: counts ±1 of the oracle, converged
+    true residual, and the discrete solution close to u = e^x sin(xy) cos z."""
+    from oracle import lshape
+    amg = _amg()
+    K, F = amg.iga_poisson(3, p, n, rhs=2, geometry=2)
+    Fo, uD = lshape.paper_lshape_rhs(p, n)
+    assert np.abs(F - Fo).max() <= 1e-13 * np.abs(Fo).max()
+    H = amg.Hierarchy(K, amg.params(p, krylov=1, coarse_solver=1))
+    Ho = oracle.setup(lshape.assemble_lshape(p, n), oracle.OParams.for_degree(p, coarse_solver=1))
+    uo, ito, rro, histo, rco = oracle.fcg(Ho, F, rtol=1e-6, maxit=200)
+    u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6, maxit=200)
+    assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
+    ud = u.cpu().numpy()
+    assert np.linalg.norm(F - oracle.spmv(K.to_scipy(), ud)) <= 1.05e-6 * np.linalg.norm(F)
+    norm_u = lshape.l2_error_full(p, n, np.zeros_like(ud), np.zeros_like(uD), exact=lshape.exact_u)
+    assert lshape.l2_error_full(p, n, ud, uD) <= 1e-3 * norm_u

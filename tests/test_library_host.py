@@ -191,3 +191,61 @@ def test_paper_ring_load_matches_oracle(p, n):
     K, F = amg.iga_poisson(3, p, n, rhs=2, geometry=1)
     Fo, _ = ring.paper_ring_rhs(p, n)
     assert np.abs(F - Fo).max() <= 1e-13 * np.abs(Fo).max()
+
+
+@pytest.mark.parametrize("p,n", [(1, 3), (2, 3), (3, 4), (4, 2)])
+def test_lshape_operator_bitwise_equal_to_oracle(p, n):
+    """geometry = 2 (three-patch L-shape, NEXT-4): patch entries summed in patch order on both sides,
+    so K is bitwise the oracle's glued Σ_P S_Pᵀ K_cube S_P restricted to the free DOFs; the f = 1 load
+    (rhs = 0) agrees with the oracle's quadrature to 1e-13."""
+    from oracle import lshape
+    K, F = amg.iga_poisson(3, p, n, rhs=0, geometry=2)
+    Ko = lshape.assemble_lshape(p, n)
+    assert np.array_equal(K.indptr, Ko.indptr) and np.array_equal(K.indices, Ko.indices)
+    assert np.array_equal(K.data.view(np.uint64), Ko.data.view(np.uint64))
+    free, _, _ = lshape.free_lists(p, n)
+    zero = lambda x, y, z: 0.0 * x  # noqa: E731
+    Fo = lshape.load_all(p, n, f=lambda x, y, z: 1.0 + 0.0 * x, gN4=zero, gN6=zero)[free]
+    assert np.abs(F - Fo).max() <= 1e-13 * np.abs(Fo).max()
+    assert not amg.iga_poisson(3, p, n, rhs=1, geometry=2)[1].any()
+
+
+def test_lshape_sizes_table2b():
+    """Library sizes at k = 12 against Table 2b (p = 5 is the table's misprint 11,024 → 11,040)."""
+    for p, size in [(2, 5772), (3, 7280), (4, 9030), (5, 11040), (6, 13328)]:
+        assert amg.iga_poisson(3, p, 12, rhs=1, geometry=2)[0].shape[0] == size
+
+
+def test_lshape_hierarchy_bitwise_equal_to_oracle():
+    from oracle import lshape
+    p, n = 3, 6
+    K, _ = amg.iga_poisson(3, p, n, rhs=1, geometry=2)
+    H = amg.Hierarchy(K, amg.params(p, host_only=1))
+    Ho = oracle.setup(lshape.assemble_lshape(p, n), oracle.OParams.for_degree(p))
+    assert H.info()["levels"] == Ho.nlevels
+    for l, L in enumerate(Ho.levels):
+        e = H.export(l)
+        assert np.array_equal(e["K"].indices, L.K.indices)
+        assert np.array_equal(e["K"].data.view(np.uint64), L.K.data.view(np.uint64))
+        if L.P is not None:
+            assert np.array_equal(e["agg"], L.agg)
+            assert np.array_equal(e["P"].data.view(np.uint64), L.P.data.view(np.uint64))
+
+
+def test_lshape_rejects_bad_combinations():
+    with pytest.raises(amg.AmgError):
+        amg.iga_poisson(2, 2, 4, rhs=1, geometry=2)
+    with pytest.raises(amg.AmgError):
+        amg.iga_poisson(3, 2, 4, dirichlet_sides=0, rhs=1, geometry=2)
+    with pytest.raises(amg.AmgError):
+        amg.iga_poisson(3, 2, 4, rhs=1, geometry=3)
+
+
+@pytest.mark.parametrize("p,n", [(1, 3), (2, 3), (3, 4), (4, 2)])
+def test_paper_lshape_load_matches_oracle(p, n):
+    """rhs = 2 on the L-shape: the library's source, Neumann faces, joint Dirichlet projection (its own
+    Jacobi-CG) and lifting agree with the oracle's (sparse direct projection) to 1e-13."""
+    from oracle import lshape
+    _, F = amg.iga_poisson(3, p, n, rhs=2, geometry=2)
+    Fo, _ = lshape.paper_lshape_rhs(p, n)
+    assert np.abs(F - Fo).max() <= 1e-13 * np.abs(Fo).max()
