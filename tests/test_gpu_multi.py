@@ -36,9 +36,10 @@ def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg", fmt=0)
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
         import paper_2511_21268_b200 as amg
         import amg_inputs
-        dim, p, n = case
+        dim, p, n = case[:3]
+        geom = case[3] if len(case) > 3 else 0  # 2: the three-patch L-shape (NEXT-4)
         paper = solver == "fcg"  # the paper's own experiment: its data, FCG, §5.1 coarse CG
-        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0)
+        K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0, geometry=geom)
         kw = dict(krylov=1, coarse_solver=1) if paper else {}
         if fmt:
             kw["format"] = fmt
@@ -79,7 +80,8 @@ def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg", fmt=0)
 
 @pytest.mark.parametrize("transport", ["p2p", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case,rep_nnz", [((3, 3, 12), 100000), ((3, 2, 32), 200000), ((3, 2, 20), 10 ** 12)])
+@pytest.mark.parametrize("case,rep_nnz", [((3, 3, 12), 100000), ((3, 2, 32), 200000), ((3, 2, 20), 10 ** 12),
+                                           ((3, 2, 12, 2), 100000)])
 def test_distributed_solve_matches_single_gpu(world, case, rep_nnz, transport):
     """transport p2p: ghost values pushed from the producing kernels' epilogues into peer memory and a
     cross-GPU kernel lock-step (no NCCL in the solve); nccl: NCCL send/recv halos and all-reduces."""
@@ -153,17 +155,18 @@ def test_distributed_sellvi(transport):
         assert np.linalg.norm(u8 - u1_8) <= 1e-10 * np.linalg.norm(u1_8)
 
 
+@pytest.mark.parametrize("case", [(3, 3, 12), (3, 3, 8, 2)])
 @pytest.mark.parametrize("transport", ["p2p", "nccl"])
-def test_distributed_paper_experiment(transport):
-    """The paper's configuration (its cube data, FCG outer, §5.1 coarse CG on the replicated coarsest
-    level) at 2 GPUs vs 1 GPU."""
+def test_distributed_paper_experiment(transport, case):
+    """The paper's configuration (its cube or L-shape data, FCG outer, §5.1 coarse CG on the replicated
+    coarsest level) at 2 GPUs vs 1 GPU."""
     world = 2
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, (3, 3, 12), 100000, transport, q, "fcg"))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, 100000, transport, q, "fcg"))
              for r in range(world)]
     for pr in procs:
         pr.start()
