@@ -132,14 +132,14 @@ class ClockSampler:
 def ncu_traffic(cfg: str, key: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     (profiles/ncu_dominant.json, written by tools/ncu_dominant.py) if it profiled this kernel variant."""
-    path = os.path.join(ROOT, "profiles", "ncu_dominant.json")
-    try:
-        with open(path) as f:
-            d = json.load(f)
-        if d.get("workload") == cfg and d.get("kernel_key") == key:
-            return d.get("dram_bytes_per_launch")
-    except Exception:  # noqa: BLE001
-        pass
+    for name in ("ncu_dominant.json", f"ncu_dominant_{cfg}.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                d = json.load(f)
+            if d.get("workload") == cfg and d.get("kernel_key") == key:
+                return d.get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            pass
     return None
 
 

@@ -34,8 +34,9 @@ def _worker(rank, world, port, case, rep_nnz, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_2511_21268_b200 as amg
         import amg_inputs
-        dim, p, n = case
-        K, F = amg.iga_poisson(dim, p, n)
+        dim, p, n = case[:3]
+        geom = case[3] if len(case) > 3 else 0  # 2: the three-patch L-shape
+        K, F = amg.iga_poisson(dim, p, n, rhs=1 if geom else 0, geometry=geom)
         H = amg.Hierarchy(K, amg.params(p, host_only=1), dist=amg.make_dist(rank, world, nccl_id=bytes(128)))
         info = H.info()
         checked = 0
@@ -115,7 +116,8 @@ def _worker(rank, world, port, case, rep_nnz, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,rep_nnz", [((3, 2, 12), 1000), ((3, 3, 10), 20000), ((2, 2, 16), 100)])
+@pytest.mark.parametrize("case,rep_nnz", [((3, 2, 12), 1000), ((3, 3, 10), 20000), ((2, 2, 16), 100),
+                                           ((3, 2, 6, 2), 1000)])
 def test_partition_and_halo_plans_world2(case, rep_nnz):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -164,14 +166,15 @@ def _same(a, b):
 
 
 @pytest.mark.parametrize("case,world,rep_nnz", [((3, 2, 12), 2, 1000), ((3, 3, 10), 3, 20000),
-                                                ((2, 2, 16), 4, 100)])
+                                                ((2, 2, 16), 4, 100), ((3, 2, 6, 2), 2, 1000)])
 def test_share_equals_per_rank_setup(case, world, rep_nnz, monkeypatch):
     """A rank's hierarchy rebuilt from its share has exactly the plan, local operators (bitwise values)
     and sizes that amg_setup with that rank's amg_dist builds from the full K."""
     monkeypatch.setenv("AMG_REPLICATE_NNZ", str(rep_nnz))
     import paper_2511_21268_b200 as amg
-    dim, p, n = case
-    K, _ = amg.iga_poisson(dim, p, n)
+    dim, p, n = case[:3]
+    geom = case[3] if len(case) > 3 else 0
+    K, _ = amg.iga_poisson(dim, p, n, rhs=1 if geom else 0, geometry=geom)
     G = amg.Hierarchy(K, amg.params(p, host_only=1))
     for r in range(world):
         d = amg.make_dist(r, world, nccl_id=bytes(128))

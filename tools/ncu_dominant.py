@@ -57,7 +57,9 @@ def main():
     main_l = launches[-1]
     key = kernel_key(main_l["kernel"])
     dram = sum(l["dram__bytes_read.sum"] + l["dram__bytes_write.sum"] for l in launches) / len(launches)
-    with open(os.path.join(ROOT, "profiles", "ncu_dominant.json"), "w") as f:
+    # C3 (the bench default) keeps the historical file name; other workloads get their own file
+    name = "ncu_dominant.json" if cfg == "C3" else f"ncu_dominant_{cfg}.json"
+    with open(os.path.join(ROOT, "profiles", name), "w") as f:
         json.dump({"workload": cfg, "kernel_key": key, "kernel": main_l["kernel"], "launches": len(launches),
                    "dram_bytes_per_launch": dram, "source": os.path.basename(rep)}, f, indent=1)
     with open(md, "w") as f:

@@ -26,7 +26,8 @@ def main():
     import paper_2511_21268_b200 as amg
     os.environ.setdefault("AMG_TUNE_CACHE", os.path.join(ROOT, "profiles", f"tune_{args.config}.txt"))
     c = amg_inputs.CONFIGS[args.config]
-    K, F = amg.iga_poisson(c["dim"], c["p"], c["n"])
+    geom = c.get("geometry", 0)
+    K, F = amg.iga_poisson(c["dim"], c["p"], c["n"], rhs=2 if geom else 0, geometry=geom)
     H = amg.Hierarchy(K, amg.params(c["p"], format=args.format))
     Fd = torch.from_numpy(F).cuda()
     u = torch.zeros_like(Fd)
