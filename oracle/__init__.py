@@ -13,7 +13,10 @@ Contents (each function cites the PAPER.md passage it follows):
   * ``oracle.c``   — Kronecker assembly (c.4), compatible weighted matching + aggregation +
     smoothed prolongator + Galerkin RAP (c.6-c.15), Chebyshev-ℓ1-Jacobi V-cycle (c.16-c.18) and
     PCG (c.19), single-threaded, ``-O2 -ffp-contract=off``;
-  * ``core.py``    — ctypes wrapper returning numpy / scipy objects.
+  * ``core.py``    — ctypes wrapper returning numpy / scipy objects;
+  * ``cube_paper.py`` — the paper's cube data (NEXT-1): projected Dirichlet data, Neumann loads, lifting;
+  * ``ring.py``    — the thick quarter ring (NEXT-3): NURBS map, weighted tables, its data;
+  * ``lshape.py``  — the three-patch L-shape (NEXT-4): conforming gluing, its data.
 
 Parity status of each function (pins in tests/test_oracle_*.py) is listed in DESIGN.md §4.
 """
