@@ -584,6 +584,22 @@ void lshape_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
                 }
     if (N > INT32_MAX) throw Error{AMG_EINVAL, "more than 2^31-1 free DOFs (int32 columns)"};
     auto tab = [&](const double *t, int a, int a2) { return t[(size_t)a * bw + (a2 - a + p)]; };
+    // K_all entry of lattice points (x, y, z), (x2, y2, z2): Σ over the patches holding both, in patch
+    // order, of the cube entry ((K·M)·M + (M·K)·M) + (M·M)·K; *any = some patch holds both
+    auto pair_value = [&](int x, int y, int z, int x2, int y2, int z2, bool *any) {
+        double val = 0.0;
+        *any = false;
+        for (int P = 0; P < 3; P++) {
+            if (!holds(P, x, y) || !holds(P, x2, y2)) continue;
+            const int a = x - ox[P], a2 = x2 - ox[P], b = y - oy[P], b2 = y2 - oy[P];
+            const double t1 = (tab(K1, a, a2) * tab(M1, b, b2)) * tab(M1, z, z2);
+            const double t2 = (tab(M1, a, a2) * tab(K1, b, b2)) * tab(M1, z, z2);
+            const double t3 = (tab(M1, a, a2) * tab(M1, b, b2)) * tab(K1, z, z2);
+            val += (t1 + t2) + t3;
+            *any = true;
+        }
+        return val;
+    };
     // visit the columns of row r in ascending order; emit(col, value)
     auto row_visit = [&](int64_t r, auto &&emit) {
         const int x = px[r], y = py[r], z = pz[r];
@@ -592,17 +608,8 @@ void lshape_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
                 for (int x2 = std::max(x - p, 0); x2 <= std::min(x + p, Mx - 1); x2++) {
                     const int64_t col = idx[((size_t)z2 * Mx + y2) * Mx + x2];
                     if (col < 0) continue;
-                    double val = 0.0;
-                    bool any = false;
-                    for (int P = 0; P < 3; P++) {
-                        if (!holds(P, x, y) || !holds(P, x2, y2)) continue;
-                        const int a = x - ox[P], a2 = x2 - ox[P], b = y - oy[P], b2 = y2 - oy[P];
-                        const double t1 = (tab(K1, a, a2) * tab(M1, b, b2)) * tab(M1, z, z2);
-                        const double t2 = (tab(M1, a, a2) * tab(K1, b, b2)) * tab(M1, z, z2);
-                        const double t3 = (tab(M1, a, a2) * tab(M1, b, b2)) * tab(K1, z, z2);
-                        val += (t1 + t2) + t3;
-                        any = true;
-                    }
+                    bool any;
+                    const double val = pair_value(x, y, z, x2, y2, z2, &any);
                     if (any) emit(col, val);
                 }
     };
@@ -775,14 +782,8 @@ void lshape_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F) {
                         if (!inside(x2, y2) || !dirichlet(x2, y2, z2)) continue;
                         const double u = xs[L(x2, y2, z2)];
                         if (u == 0.0) continue;
-                        for (int P = 0; P < 3; P++) {
-                            if (!holds(P, x, y) || !holds(P, x2, y2)) continue;
-                            const int a = x - ox[P], a2 = x2 - ox[P], b = y - oy[P], b2 = y2 - oy[P];
-                            const double t1 = (tab(K1, a, a2) * tab(M1, b, b2)) * tab(M1, z0, z2);
-                            const double t2 = (tab(M1, a, a2) * tab(K1, b, b2)) * tab(M1, z0, z2);
-                            const double t3 = (tab(M1, a, a2) * tab(M1, b, b2)) * tab(K1, z0, z2);
-                            lift += ((t1 + t2) + t3) * u;
-                        }
+                        bool any;
+                        lift += pair_value(x, y, z0, x2, y2, z2, &any) * u;
                     }
             F[row] = Fall[L(x, y, z0)] - lift;
         }
