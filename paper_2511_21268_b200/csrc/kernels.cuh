@@ -1025,10 +1025,13 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
     const uint64_t pol = stream_policy();
     typename Epi::Acc dacc{};
     bool signalled = pp.gorder == nullptr || pp.nranks == 0;
-    if (!signalled && warp < pp.nbnd) peer_wait_warp(pp);
     // work items: slice positions [0, nwhole) whole, then every later position split into 2^lparts parts
     const int64_t nitems = nwhole + ((nslices - nwhole) << lparts);
     const int64_t nbnd_items = pp.nbnd <= nwhole ? pp.nbnd : nwhole + ((pp.nbnd - nwhole) << lparts);
+    // a warp with boundary ITEMS waits for the neighbours (with split slices there are more boundary
+    // items than boundary slice positions: waiting on `warp < nbnd` let the warps in between read
+    // ghost values before the neighbours had published them)
+    if (!signalled && warp < nbnd_items) peer_wait_warp(pp);
     for (int64_t it = warp; it < nitems; it += nwarps) {
         if (!signalled && it >= nbnd_items) {
             peer_signal_warp(pp);
