@@ -218,8 +218,10 @@ amg_status amg_hierarchy_export(const amg_hierarchy *H, int level, amg_csr **K_l
                                 int32_t **aggregate_of, double **dhat, double *omega);
 
 /* Kernel timing of the dominant kernel (the fused Chebyshev step on level 0), recorded with CUDA
- * events on the launching stream while enabled.  bytes_per_launch is the ALGORITHMIC byte count
- * 12·nnz(K_0) + 64·N_0. */
+ * events on the launching stream while enabled.  bytes_per_launch is the ALGORITHMIC byte count of
+ * one launch: the level-0 operator's alg_bytes in the format it is stored in (amg_op_config.alg_bytes:
+ * 4 B per stored entry + table + row bases + slice offsets for SELL-VI; 8 B value + the column source
+ * + 8 B row pointers per row for CSR) plus the epilogue's 56·N_0 vector bytes. */
 typedef struct {
     int64_t launches;
     double total_ms;
@@ -230,7 +232,10 @@ amg_status amg_set_profiling(amg_hierarchy *H, int enable); /* enable resets the
 amg_status amg_get_kernel_stats(amg_hierarchy *H, amg_kernel_stats *st);
 
 /* Device kernel chosen for operator op (0 K_l, 1 P̄_l, 2 R_l) of level l: layout (0 padded CSR,
- * 1 SELL-32, 2 SELL-VI: row per lane, column offset + value index in one 32-bit word per entry), kernel (bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
+ * 1 SELL-32, 2 SELL-VI: row per lane, column offset + value index in one 32-bit word per entry,
+ * 3 windowed SELL-VI (single GPU): the multiplied vector's window of each block of 8 slices staged in
+ * shared memory by TMA, window position + value index per word; its `kernel` = windows staged per CTA,
+ * 1 or 2), kernel (CSR layouts: bit 0: 0 register-batched warp-per-row CSR, 1 TMA-staged CSR; bit 1: column
  * source, 0 int32 columns, 1 16-bit column offsets from a per-row base; bit 2: register core with an L2
  * bulk prefetch of the next row; bit 3: value source, 0 streamed fp64 values, 1 value index into the
  * operator's table of distinct values — CSR-VI, register core only), rows per warp group G, pairs per
@@ -252,7 +257,8 @@ typedef struct {
                                the last round of work items, so that round is short (env
                                AMG_SELLVI_PARTS=k forces 2^k parts on every slice); the rows of a split
                                slice sum their parts' chains in part order.  0 other layouts */
-    int offset_bits;        /* SELL-VI: column-offset bits of an entry word (16..24); 0 other layouts */
+    int offset_bits;        /* SELL-VI: column-offset bits of an entry word (16..24); windowed SELL-VI:
+                               window-position bits; 0 other layouts */
 } amg_op_config;
 amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_config *cfg);
 /* Force the kernel configuration of one CSR-layout operator (experiments and the kernel-equivalence
@@ -261,7 +267,8 @@ amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_confi
  * (prefetch) needs the register core and rows padded to 8; bit 3 (value index) needs the register core
  * and a value table (built at setup for format 0 operators with >= 2e6 stored entries, >= 4 entries per
  * distinct value and <= 2^21 distinct values, unless env AMG_VALUE_INDEX=0); a SELL-VI operator
- * (layout 2) takes kernel 0, G 32 and U in {1, 2, 4} only; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
+ * (layout 2) takes kernel 0, G 32 and U in {1, 2, 4} only, a windowed one (layout 3) kernel 1 or 2 (windows
+ * staged per CTA), G 32 and U in {1, 2, 4}; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
  * sums each row in the same order, so results are bitwise unchanged.  Drops captured PCG graphs.
  * AMG_EINVAL for a bad level/op or an unavailable configuration. */
 amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);

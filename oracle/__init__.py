@@ -27,6 +27,7 @@ from .core import (  # noqa: F401
     build_liboracle,
     cij,
     fcg,
+    galerkin_pairwise,
     pairwise,
     pcg,
     setup,

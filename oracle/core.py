@@ -37,7 +37,8 @@ class _Params(C.Structure):
     _fields_ = [("agg_steps", C.c_int), ("smooth_prolong", C.c_int), ("match_threshold", C.c_double),
                 ("filter_theta", C.c_double), ("cheb_degree", C.c_int), ("coarse_sweeps", C.c_int),
                 ("coarse_size", C.c_int64), ("max_levels", C.c_int), ("coarse_solver", C.c_int),
-                ("coarse_tol", C.c_double), ("coarse_maxit", C.c_int)]
+                ("coarse_tol", C.c_double), ("coarse_maxit", C.c_int), ("tie_break", C.c_int),
+                ("omega_norm", C.c_int)]
 
 
 class _Level(C.Structure):
@@ -47,6 +48,7 @@ class _Level(C.Structure):
 
 
 _lib = None
+ITER_CB = C.CFUNCTYPE(C.c_int, C.c_int, C.c_void_p)
 
 
 def lib():
@@ -65,11 +67,14 @@ def lib():
         L.or_smooth.argtypes = [C.c_void_p, C.c_int, dp, dp, C.c_int]
         L.or_pcg.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp, dp]
         L.or_fcg.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp, dp]
+        L.or_fcg_cb.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp, dp, ITER_CB,
+                                C.c_void_p]
         L.or_cij.argtypes = [C.c_double] * 5
         L.or_cij.restype = C.c_double
         L.or_pairwise.argtypes = [C.POINTER(_CSR), dp, C.c_double, C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32), dp, dp]
         L.or_pairwise.restype = C.c_int64
+        L.or_galerkin_pairwise.argtypes = [C.POINTER(_CSR), C.POINTER(C.c_int32), dp, C.c_int64, C.POINTER(_CSR)]
         L.or_csr_new.restype = C.POINTER(_CSR)
         L.or_csr_delete.argtypes = [C.POINTER(_CSR)]
         _lib = L
@@ -148,6 +153,20 @@ def pairwise(A: sp.csr_matrix, w: np.ndarray, threshold: float = 1.0):
     return mate, agg, pv, wn[:nc].copy()
 
 
+def galerkin_pairwise(A: sp.csr_matrix, agg: np.ndarray, pv: np.ndarray, nc: int) -> sp.csr_matrix:
+    """c.10: the intermediate Galerkin operator sym(P_sᵀ A P_s) of one pairwise step."""
+    b = _Borrowed(A)
+    agg = np.ascontiguousarray(agg, dtype=np.int32)
+    pv = np.ascontiguousarray(pv, dtype=np.float64)
+    out = lib().or_csr_new()
+    rc = lib().or_galerkin_pairwise(C.byref(b.c), agg.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(pv), nc, out)
+    if rc:
+        raise RuntimeError(f"or_galerkin_pairwise failed: {rc}")
+    Ac = _csr_to_scipy(out.contents)
+    lib().or_csr_delete(out)
+    return Ac
+
+
 @dataclass
 class OParams:
     agg_steps: int = 3
@@ -161,6 +180,8 @@ class OParams:
     coarse_solver: int = 0      # 0: ℓ1-Jacobi sweeps (§4, c.17); 1: diagonal-PCG to coarse_tol (§5.1)
     coarse_tol: float = 1e-4
     coarse_maxit: int = 30
+    tie_break: int = 0          # study knobs (oracle/scripts/opc_study.py); 0 = the canonical reading
+    omega_norm: int = 0
 
     @staticmethod
     def for_degree(p: int, **kw) -> "OParams":
@@ -220,7 +241,7 @@ def setup(K: sp.csr_matrix, prm: OParams | None = None) -> OHierarchy:
     b = _Borrowed(K)
     cp = _Params(prm.agg_steps, prm.smooth_prolong, prm.match_threshold, prm.filter_theta,
                  prm.cheb_degree, prm.coarse_sweeps, prm.coarse_size, prm.max_levels,
-                 prm.coarse_solver, prm.coarse_tol, prm.coarse_maxit)
+                 prm.coarse_solver, prm.coarse_tol, prm.coarse_maxit, prm.tie_break, prm.omega_norm)
     h = C.c_void_p()
     rc = lib().or_setup(C.byref(b.c), C.byref(cp), C.byref(h))
     if rc:
@@ -255,12 +276,18 @@ def pcg(H: OHierarchy, F: np.ndarray, rtol: float = 1e-6, maxit: int = 200, u0: 
     return u, it.value, rr.value, hist[: it.value + 1], rc
 
 
-def fcg(H: OHierarchy, F: np.ndarray, rtol: float = 1e-6, maxit: int = 200, u0: np.ndarray | None = None):
-    """Flexible CG, Notay's FCG(1) → (u, iters, relres, history, status)."""
+def fcg(H: OHierarchy, F: np.ndarray, rtol: float = 1e-6, maxit: int = 200, u0: np.ndarray | None = None,
+        observer=None):
+    """Flexible CG, Notay's FCG(1) → (u, iters, relres, history, status).
+    observer(k) -> bool, if given, is called after iteration k (timing only); True stops the solve."""
     F = np.ascontiguousarray(F, dtype=np.float64)
     u = np.zeros_like(F) if u0 is None else np.array(u0, dtype=np.float64)
     it = C.c_int(0)
     rr = C.c_double(0.0)
     hist = np.full(maxit + 1, np.nan)
-    rc = lib().or_fcg(H._h, _dptr(F), _dptr(u), rtol, maxit, C.byref(it), C.byref(rr), _dptr(hist))
+    if observer is None:
+        rc = lib().or_fcg(H._h, _dptr(F), _dptr(u), rtol, maxit, C.byref(it), C.byref(rr), _dptr(hist))
+    else:
+        cb = ITER_CB(lambda k, _ctx: 1 if observer(k) else 0)
+        rc = lib().or_fcg_cb(H._h, _dptr(F), _dptr(u), rtol, maxit, C.byref(it), C.byref(rr), _dptr(hist), cb, None)
     return u, it.value, rr.value, hist[: it.value + 1], rc

@@ -91,31 +91,58 @@ def patch_map(m: int, P: str) -> np.ndarray:
 
 def assemble_all(p: int, n: int) -> sp.csr_matrix:
     """K_all (all lattice DOFs, no elimination): Σ_P S_Pᵀ K_cube S_P, summed in patch order."""
-    m = n + p
-    Kc = assemble(3, p, n, dirichlet_sides=0).tocoo()
-    _, _, Nall = free_lists(p, n)
-    keys, vals = [], []
-    for P in PATCHES:
-        g = patch_map(m, P)
-        keys.append(g[Kc.row] * Nall + g[Kc.col])
-        vals.append(Kc.data)
-    ukeys = np.unique(np.concatenate(keys))  # the union pattern, row-major
-    v = np.zeros(len(ukeys))
-    for k, d in zip(keys, vals):  # ((0 + v_A) + v_B) + v_C
-        vp = np.zeros(len(ukeys))
-        vp[np.searchsorted(ukeys, k)] = d
-        v = v + vp
-    rows, cols = ukeys // Nall, ukeys % Nall
-    indptr = np.zeros(Nall + 1, dtype=np.int64)
-    np.add.at(indptr, rows + 1, 1)
-    return sp.csr_matrix((v, cols.astype(np.int32), np.cumsum(indptr)), shape=(Nall, Nall))
+    return _assemble(p, n, restrict_free=False)
 
 
-def assemble_lshape(p: int, n: int) -> sp.csr_matrix:
+def assemble_lshape(p: int, n: int, chunk_rows: int = 1 << 16) -> sp.csr_matrix:
     """K of the free DOFs (Dirichlet DOFs eliminated)."""
-    free, _, _ = free_lists(p, n)
-    K = assemble_all(p, n)[free][:, free].tocsr()
-    K.sort_indices()
+    return _assemble(p, n, restrict_free=True, chunk_rows=chunk_rows)
+
+
+def _assemble(p: int, n: int, restrict_free: bool, chunk_rows: int = 1 << 16) -> sp.csr_matrix:
+    """Σ_P S_Pᵀ K_cube S_P over blocks of `chunk_rows` global rows (memory ∝ the block, not the
+    whole operator: the k = 96 L-shape has ~10⁹ non-zeros).  Per entry, the values of the patches
+    that hold it are summed in patch order, ((0 + v_A) + v_B) + v_C; the union pattern is kept (also
+    entries whose sum is 0).  Each S_P is increasing in the local index, so the local rows of a block
+    of global rows are a contiguous range of K_cube's rows."""
+    m = n + p
+    Kc = assemble(3, p, n, dirichlet_sides=0)
+    free, _, Nall = free_lists(p, n)
+    if restrict_free:
+        pos = -np.ones(Nall, dtype=np.int64)
+        pos[free] = np.arange(len(free))
+    maps = [patch_map(m, P) for P in PATCHES]
+    rp, ci, vv, nnz = [np.zeros(1, dtype=np.int64)], [], [], 0
+    nrow_out = len(free) if restrict_free else Nall
+    for g0 in range(0, Nall, chunk_rows):
+        g1 = min(Nall, g0 + chunk_rows)
+        keys, vals = [], []
+        for g in maps:
+            lo, hi = np.searchsorted(g, g0), np.searchsorted(g, g1)
+            blk = Kc[lo:hi].tocoo()
+            keys.append(g[blk.row + lo] * Nall + g[blk.col])
+            vals.append(blk.data)
+        ukeys = np.unique(np.concatenate(keys))  # the union pattern of the block, row-major
+        v = np.zeros(len(ukeys))
+        for k, d in zip(keys, vals):  # ((0 + v_A) + v_B) + v_C
+            vp = np.zeros(len(ukeys))
+            vp[np.searchsorted(ukeys, k)] = d
+            v = v + vp
+        rows, cols = ukeys // Nall, ukeys % Nall
+        if restrict_free:
+            keep = (pos[rows] >= 0) & (pos[cols] >= 0)
+            rows, cols, v = pos[rows[keep]], pos[cols[keep]], v[keep]
+            r_lo = int(np.searchsorted(free, g0))
+            r_hi = int(np.searchsorted(free, g1))
+        else:
+            r_lo, r_hi = g0, g1
+        cnt = np.bincount(rows - r_lo, minlength=r_hi - r_lo)
+        rp.append(nnz + np.cumsum(cnt))
+        nnz += len(v)
+        ci.append(cols.astype(np.int32))
+        vv.append(v)
+    K = sp.csr_matrix((np.concatenate(vv), np.concatenate(ci), np.concatenate(rp)), shape=(nrow_out, nrow_out))
+    K.has_sorted_indices = True
     return K
 
 

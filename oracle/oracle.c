@@ -56,6 +56,14 @@ typedef struct {
     int coarse_solver;
     double coarse_tol;      /* 1e-4 */
     int coarse_maxit;       /* 30 */
+    /* Study knobs for readings the paper leaves open (c.8 / c.12); 0 = the canonical
+     * reading every parity test uses.  Only oracle/scripts/opc_study.py sets them.
+     *   tie_break : order of edges with equal c_ij.  0: (i asc, j asc) for i < j — each vertex prefers
+     *               its smaller-index partner; 1: (j desc, i desc) — prefers the larger index;
+     *               2 + s: a fixed pseudo-random order (splitmix64 of (i, j) with seed s, then i, j).
+     *   omega_norm: 0: λ̂ = ‖D_f⁻¹K_f‖∞ of the filtered matrix (c.12); 1: ‖D⁻¹K‖∞ of K itself. */
+    int tie_break;
+    int omega_norm;
 } oparams;
 
 typedef struct {
@@ -319,11 +327,32 @@ void or_spmv(const ocsr *A, const double *x, double *y) {
 
 typedef struct { double c; int32_t i, j; } oedge;
 
-/* Strict total order: c descending, then i ascending, then j ascending (c.8). */
+static int g_tie_break = 0; /* oparams.tie_break of the running or_setup (study knob; 0 = canonical) */
+
+static uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* Strict total order: c descending, then i ascending, then j ascending (c.8).  (tie_break 1 / 2:
+ * the study orders of the oparams comment.) */
 static int cmp_edge(const void *pa, const void *pb) {
     const oedge *a = (const oedge *)pa, *b = (const oedge *)pb;
     if (a->c > b->c) return -1;
     if (a->c < b->c) return 1;
+    if (g_tie_break == 1) {
+        if (a->j != b->j) return a->j > b->j ? -1 : 1;
+        if (a->i != b->i) return a->i > b->i ? -1 : 1;
+        return 0;
+    }
+    if (g_tie_break >= 2) { /* seed = tie_break − 2 */
+        const uint64_t seed = (uint64_t)(g_tie_break - 2) * 0xD1B54A32D192ED03ull;
+        uint64_t ha = mix64(seed ^ (((uint64_t)(uint32_t)a->i << 32) | (uint32_t)a->j));
+        uint64_t hb = mix64(seed ^ (((uint64_t)(uint32_t)b->i << 32) | (uint32_t)b->j));
+        if (ha != hb) return ha < hb ? -1 : 1;
+    }
     if (a->i != b->i) return a->i < b->i ? -1 : 1;
     if (a->j != b->j) return a->j < b->j ? -1 : 1;
     return 0;
@@ -473,7 +502,7 @@ static int filter_matrix(const ocsr *K, double theta, ocsr *Kf) {
 /* P̄ = (I − ω D⁻¹ K_f) P with D = diag(K_f), ω = 4/(3 λ̂), λ̂ = ‖D⁻¹K_f‖_∞ (c.12).
  *   t_iJ = Σ_{j in K_f row i, asc} K_f[i,j]·P[j,J];   P̄[i,J] = P[i,J] − (ω·t_iJ)/K_f[i,i]. */
 static int smoothed_prolongator(const ocsr *K, const int32_t *agg, const double *pt, int64_t nc,
-                                double theta, ocsr *Pb, double *omega_out) {
+                                double theta, int omega_norm, ocsr *Pb, double *omega_out) {
     ocsr Kf;
     int rc = filter_matrix(K, theta, &Kf);
     if (rc) return rc;
@@ -482,10 +511,14 @@ static int smoothed_prolongator(const ocsr *K, const int32_t *agg, const double 
     if (!df) return -2;
     if (get_diag(&Kf, df)) return -5;
     double lam = 0.0;
+    const ocsr *Kn = omega_norm == 1 ? K : &Kf; /* study knob: norm of K itself instead of K_f */
     for (int64_t i = 0; i < N; i++) {
-        double s = 0.0;
-        for (int64_t k = Kf.rp[i]; k < Kf.rp[i + 1]; k++) s = s + fabs(Kf.v[k]);
-        double q = s / df[i];
+        double s = 0.0, dii = 0.0;
+        for (int64_t k = Kn->rp[i]; k < Kn->rp[i + 1]; k++) {
+            s = s + fabs(Kn->v[k]);
+            if (Kn->ci[k] == i) dii = Kn->v[k];
+        }
+        double q = s / (omega_norm == 1 ? dii : df[i]);
         if (q > lam) lam = q;
     }
     double omega = 4.0 / (3.0 * lam);
@@ -568,6 +601,7 @@ int or_setup(const ocsr *K0, const oparams *prm, ohier **out) {
     ohier *H = (ohier *)calloc(1, sizeof(ohier));
     if (!H) return -2;
     H->prm = *prm;
+    g_tie_break = prm->tie_break;
     int rc = csr_copy(K0, &H->lev[0].K);
     if (rc) return rc;
     int64_t N0 = K0->nrows;
@@ -622,7 +656,7 @@ int or_setup(const ocsr *K0, const oparams *prm, ohier **out) {
         L->ptent = pt;
         /* c.12 */
         if (prm->smooth_prolong) {
-            rc = smoothed_prolongator(&L->K, agg, pt, nc, prm->filter_theta, &L->P, &L->omega);
+            rc = smoothed_prolongator(&L->K, agg, pt, nc, prm->filter_theta, prm->omega_norm, &L->P, &L->omega);
             if (rc) return rc;
         } else {
             if (csr_alloc(&L->P, N, nc, N)) return -2;
@@ -642,6 +676,7 @@ int or_setup(const ocsr *K0, const oparams *prm, ohier **out) {
         C->w = (double *)realloc(w, (size_t)(nc > 0 ? nc : 1) * sizeof(double));
         l++;
     }
+    g_tie_break = 0;
     *out = H;
     return 0;
 }
@@ -839,8 +874,19 @@ done:
  * (p_kᵀ q_k)) p_k.  With a fixed SPD preconditioner it generates the CG iterates; it stays a descent
  * method when the preconditioner varies (the §5.1 coarse CG makes the V-cycle nonlinear).  Same
  * stopping test, history and return codes as or_pcg; breakdown if pᵀKp <= 0. */
+typedef int (*or_iter_cb)(int k, void *ctx);
+int or_fcg_cb(const ohier *H, const double *F, double *u, double rtol, int maxit, int *iters,
+              double *relres, double *hist, or_iter_cb cb, void *ctx);
 int or_fcg(const ohier *H, const double *F, double *u, double rtol, int maxit, int *iters,
            double *relres, double *hist) {
+    return or_fcg_cb(H, F, u, rtol, maxit, iters, relres, hist, 0, 0);
+}
+/* or_fcg with an observer: cb(k, ctx) is called after iteration k's stopping test (not after the
+ * final, converged one); a non-zero return stops the solve there (return code 1, as at maxit).  The
+ * observer only reads the clock (bench.py's oracle arm times the iterations one by one); the
+ * arithmetic is or_fcg's. */
+int or_fcg_cb(const ohier *H, const double *F, double *u, double rtol, int maxit, int *iters,
+              double *relres, double *hist, or_iter_cb cb, void *ctx) {
     const olevel *L = &H->lev[0];
     const int64_t N = L->N;
     double *r = (double *)malloc((size_t)N * sizeof(double));
@@ -879,6 +925,7 @@ int or_fcg(const ohier *H, const double *F, double *u, double rtol, int maxit, i
         *relres = rn / nF;
         if (hist) hist[k] = rn / nF;
         if (rn <= rtol * nF) { rc = 0; break; }
+        if (cb && cb(k, ctx)) break;
         or_vcycle(H, r, z);
         const double beta = -dot(N, z, q) / pq;
         for (int64_t i = 0; i < N; i++) p[i] = z[i] + beta * p[i];
@@ -895,6 +942,11 @@ done:
 ocsr *or_csr_new(void) { return (ocsr *)calloc(1, sizeof(ocsr)); }
 void or_csr_delete(ocsr *A) { if (A) { csr_free(A); free(A); } }
 int or_hier_nlevels(const ohier *H) { return H->nlevels; }
+/* c.10 on its own (for its pin, tests/test_oracle_setup.py): the intermediate Galerkin operator of
+ * one pairwise step, written into *Ac (free with or_csr_delete). */
+int or_galerkin_pairwise(const ocsr *A, const int32_t *agg, const double *pv, int64_t nc, ocsr *Ac) {
+    return galerkin_pairwise(A, agg, pv, nc, Ac);
+}
 const olevel *or_hier_level(const ohier *H, int l) { return &H->lev[l]; }
 
 /* Smoother alone (tests): x <- S(b, x) on level l (c.16). */

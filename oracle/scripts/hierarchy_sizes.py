@@ -12,6 +12,8 @@ import os
 import sys
 import time
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
@@ -41,8 +43,13 @@ def main(cfg: str) -> None:
         H2 = oracle.setup(K, oracle.OParams.for_degree(c["p"], coarse_solver=1))
         t0 = time.perf_counter()
         u2, it2, rr2, h2, rc2 = oracle.fcg(H2, Fp, rtol=1e-6, maxit=200)
+        # the converged iterate (the it2-th) sampled every 997th row (+ the last row) and the residual
+        # history, for the full-size GPU parity test (tests/test_gpu_parity.py::test_c3_paper_solve_vs_oracle_artifact)
+        idx = list(range(0, len(u2), 997)) + [len(u2) - 1]
         paper = dict(oracle_iters_paper=it2, oracle_relres_paper=rr2,
-                     oracle_solve_paper_s=round(time.perf_counter() - t0, 2))
+                     oracle_solve_paper_s=round(time.perf_counter() - t0, 2),
+                     oracle_hist_paper=[float(h) for h in h2], u_sample_stride=997,
+                     u_sample_paper=[float(u2[i]) for i in idx], u_norm_paper=float(np.linalg.norm(u2)))
     out = dict(workload=cfg, oracle_iters=iters, oracle_relres=relres, oracle_solve_s=round(t_solve, 2), **paper,
                levels=H.nlevels, N=[L.N for L in H.levels], nnz=[L.K.nnz for L in H.levels],
                nnz_P=[(L.P.nnz if L.P is not None else 0) for L in H.levels], opc=H.opc(),

@@ -341,7 +341,9 @@ class Hierarchy:
             (f"_vi{8 * c.value_index_bytes}" if k & 8 else "") + ("_pf" if k & 4 else "")
         if c.layout == 2:
             name = "sellvi"
-        return dict(layout=("csr", "sell32", "sellvi")[c.layout], kernel=name, kernel_bits=k, G=c.G, U=c.U,
+        if c.layout == 3:
+            name = f"sellviw_b{k}"  # windows staged per CTA
+        return dict(layout=("csr", "sell32", "sellvi", "sellviw")[c.layout], kernel=name, kernel_bits=k, G=c.G, U=c.U,
                     stored=c.stored, nnz=c.nnz, alg_bytes=c.alg_bytes, tuned_us=round(c.tuned_us, 2),
                     n_values=c.n_values, value_index_bytes=c.value_index_bytes, sellvi_parts=c.sellvi_parts,
                     offset_bits=c.offset_bits)

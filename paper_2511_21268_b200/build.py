@@ -70,8 +70,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             f.result()
     if force or _newer(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-lquadmath", "-lnccl",
-              "-lcudart"], verbose)
+        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-Xlinker", "--no-undefined",
+              "-lgomp", "-lquadmath", "-lnccl", "-lcudart"], verbose)
         os.replace(tmp, LIB)
     return LIB
 

@@ -12,6 +12,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -34,7 +38,9 @@ void set_allocator(amg_alloc_fn a, amg_free_fn f) {
 
 void *DevState::alloc(size_t bytes) {
     void *p = nullptr;
-    if (bytes == 0) bytes = 16;
+    // 256-B units: vectors may be read (never written) up to the next 16-B boundary past their end
+    // by the window copies of k_sellviw
+    bytes = (std::max<size_t>(bytes, 16) + 255) & ~(size_t)255;
     if (g_alloc) {
         p = g_alloc(bytes, device, nullptr);
         if (!p) throw Error{AMG_ENOMEM, "device allocation (hook) failed"};
@@ -55,6 +61,8 @@ DevState::~DevState() {
     if (hS) cudaFreeHost(hS);
     for (auto &s : seg)
         if (s.exec) cudaGraphExecDestroy(s.exec);
+    if (loop.exec) cudaGraphExecDestroy(loop.exec);
+    if (hctl) cudaFreeHost(hctl);
     if (cap) cudaStreamDestroy(cap);
     for (char *p : peer_slabs) cudaIpcCloseMemHandle(p);
     if (slab) {
@@ -356,18 +364,93 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
         std::memcpy(&b, &tab[t], 8);
         if (b == 0) zero = (uint32_t)t;
     }
+    // Windowed variant (k_sellviw): blocks of kWinSlices consecutive slices; the union of a block's
+    // columns as runs of even length starting at even columns (gaps of <= kWinGap columns are staged
+    // rather than split), each entry's word = its column's position in the block's window.  Single-GPU
+    // layout only (the staged vector must be 16-B aligned at column 0; the distributed vectors carry
+    // ghost slots before the owned block).  AMG_SELLVI_WIN=0 keeps the plain SELL-VI words.
+    bool win = D.nranks <= 1 && A.ncols == n;
+    if (const char *e = std::getenv("AMG_SELLVI_WIN"))
+        if (std::atoi(e) == 0) win = false;
+    const int64_t nblk = (nsl + kWinSlices - 1) / kWinSlices;
+    std::vector<std::vector<int4>> bruns;
+    int64_t wmax = 0;
+    if (win) {
+        bruns.resize(nblk);
+        bool ok = true;
+#pragma omp parallel for schedule(dynamic, 16) reduction(max : wmax) reduction(&& : ok)
+        for (int64_t b = 0; b < nblk; b++) {
+            const int64_t r0 = b * kWinSlices * 32, r1 = std::min(n, r0 + kWinSlices * 32);
+            std::vector<int32_t> cols(A.ci.data() + A.rp[r0], A.ci.data() + A.rp[r1]);
+            std::sort(cols.begin(), cols.end());
+            cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+            std::vector<int4> &R = bruns[b];
+            int64_t tot = 0;
+            for (size_t k = 0; k < cols.size();) {
+                int64_t lo = cols[k] & ~1, hi = cols[k];
+                size_t j = k + 1;
+                while (j < cols.size() && (int64_t)cols[j] <= hi + 1 + kWinGap) hi = cols[j++];
+                // inclusive and odd: an even length from an even start.  With an odd column count the
+                // last run may end one double past the vector: device vectors are allocated in 256-B
+                // units (DevState::alloc), so that double is inside the allocation (its value meets only
+                // padding entries' 0.0 weights — never: no entry references it)
+                hi |= 1;
+                if (!R.empty() && lo <= (int64_t)R.back().x + R.back().y - 1 + kWinGap) {  // adjoining after rounding
+                    const int64_t nhi = std::max<int64_t>(hi, R.back().x + R.back().y - 1);
+                    tot += nhi - (R.back().x + R.back().y - 1);
+                    R.back().y = (int)(nhi - R.back().x + 1);
+                } else {
+                    R.push_back(int4{(int)lo, (int)(hi - lo + 1), (int)tot, 0});
+                    tot += hi - lo + 1;
+                }
+                k = j;
+            }
+            wmax = std::max<int64_t>(wmax, tot);
+            ok = ok && tot <= kWinMax;
+        }
+        if (!ok || wmax == 0) win = false;
+    }
+    int pbits = 1;
+    while (((int64_t)1 << pbits) < wmax) pbits++;
+    if (win && (int64_t)tab.size() > ((int64_t)1 << (32 - pbits))) win = false;
     Buf<uint32_t> w(stored);
 #pragma omp parallel for schedule(static)
     for (int64_t s = 0; s < nsl; s++) {
         const int64_t W = (soff[s + 1] - soff[s]) * 4;
+        const std::vector<int4> *R = win ? &bruns[s / kWinSlices] : nullptr;
         for (int t = 0; t < 32; t++) {
             const int64_t i = s * 32 + t;
             const int64_t b = i < n ? A.rp[i] : 0, len = i < n ? A.rp[i + 1] - A.rp[i] : 0;
+            size_t r = 0;
             for (int64_t k = 0; k < W; k++) {  // entry k of lane t: quad k/4, component k%4
                 const int64_t dst = ((soff[s] + k / 4) * 32 + t) * 4 + k % 4;
-                w[dst] = k < len ? (uint32_t)(A.ci[b + k] - base[i]) | (idx[b + k] << obits) : zero << obits;
+                if (!win) {
+                    w[dst] = k < len ? (uint32_t)(A.ci[b + k] - base[i]) | (idx[b + k] << obits) : zero << obits;
+                } else if (k < len) {
+                    const int32_t c = A.ci[b + k];  // ascending within the row: the run index only grows
+                    while ((int64_t)(*R)[r].x + (*R)[r].y <= c) r++;
+                    w[dst] = (uint32_t)((*R)[r].z + (c - (*R)[r].x)) | (idx[b + k] << pbits);
+                } else {
+                    w[dst] = zero << pbits;  // position 0 (a staged value), value 0.0
+                }
             }
         }
+    }
+    if (win) {
+        std::vector<int4> binfo(nblk), runs;
+        for (int64_t b = 0; b < nblk; b++) {
+            const int64_t tot = bruns[b].empty() ? 0 : bruns[b].back().z + bruns[b].back().y;
+            binfo[b] = int4{(int)runs.size(), (int)(runs.size() + bruns[b].size()), (int)tot, 0};
+            runs.insert(runs.end(), bruns[b].begin(), bruns[b].end());
+        }
+        out.win = true;
+        out.pbits = pbits;
+        out.wmax = (int)((wmax + 1) & ~1);
+        out.nruns = (int64_t)runs.size();
+        out.binfo = D.alloc_n<int4>(nblk);
+        out.wruns = D.alloc_n<int4>(std::max<int64_t>(1, (int64_t)runs.size()));
+        CUDA_OK(cudaMemcpy(out.binfo, binfo.data(), sizeof(int4) * nblk, cudaMemcpyHostToDevice));
+        if (!runs.empty()) CUDA_OK(cudaMemcpy(out.wruns, runs.data(), sizeof(int4) * runs.size(), cudaMemcpyHostToDevice));
     }
     out.fmt = 2;
     out.obits = obits;
@@ -405,6 +488,7 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
             lp = std::max(0, std::min(3, std::atoi(e)));
             nwhole = 0;
         }
+        if (out.win) lp = 0;  // the windowed core keeps whole slices (single GPU: 8+ full rounds at C3)
         out.lparts = lp;
         out.nwhole = lp ? nwhole : nsl;
         if (lp > 0) {
@@ -560,9 +644,16 @@ bool tune_lookup(const TuneKey &k, DCsr &A) {
     bool hit = false;
     while (std::fscanf(f, "%d %d %d %d %lld %lld %d %d %d %d %f", &r, &nr, &l, &ro, &n, &z, &kern, &G, &U, &pf, &us) == 11) {
         if (r == k.rank && nr == k.nranks && l == k.level && ro == k.role && n == k.nrows && z == k.nnz) {
-            // kern 16 marks a SELL-VI entry; skip entries of another layout or for encodings this operator lacks
-            if ((kern == 16) != (A.fmt == 2) || ((kern & 2) && !A.off16) || ((kern & 8) && !A.vtab)) continue;
-            if (kern == 16) kern = 0;
+            // kern 16 marks a SELL-VI entry, 17 a windowed SELL-VI one (pf = windows staged per CTA);
+            // skip entries of another layout or for encodings this operator lacks
+            if ((kern == 16) != (A.fmt == 2 && !A.win) || (kern == 17) != (A.fmt == 2 && A.win) ||
+                ((kern & 2) && kern < 16 && !A.off16) || ((kern & 8) && kern < 16 && !A.vtab))
+                continue;
+            if (kern == 17) {
+                A.nbuf = pf == 1 ? 1 : 2;
+                pf = 0;
+            }
+            if (kern >= 16) kern = 0;
             A.kern = kern;
             A.G = G;
             A.U = U;
@@ -575,14 +666,44 @@ bool tune_lookup(const TuneKey &k, DCsr &A) {
     return hit;
 }
 void tune_store(const TuneKey &k, const DCsr &A) {
+    // appending is opt-in (AMG_TUNE_CACHE_WRITE=1): a committed cache read by the bench is never
+    // modified by a run, and concurrent ranks never interleave lines in it
     const char *path = std::getenv("AMG_TUNE_CACHE");
-    if (!path) return;
+    const char *wr = std::getenv("AMG_TUNE_CACHE_WRITE");
+    if (!path || !wr || std::strcmp(wr, "1") != 0) return;
     if (FILE *f = std::fopen(path, "a")) {
         std::fprintf(f, "%d %d %d %d %lld %lld %d %d %d %d %.2f\n", k.rank, k.nranks, k.level, k.role,
-                     (long long)k.nrows, (long long)k.nnz, A.fmt == 2 ? 16 : A.kern, A.G, A.U, A.pf, A.tuned_us);
+                     (long long)k.nrows, (long long)k.nnz, A.fmt == 2 ? (A.win ? 17 : 16) : A.kern, A.G, A.U,
+                     A.fmt == 2 && A.win ? A.nbuf : A.pf, A.tuned_us);
         std::fclose(f);
     }
 }
+
+}  // namespace
+
+int resident_ctas(const void *fn, int block, int smem, int smem_attr) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, int, int, int, int>, int> cache;
+    static std::map<std::pair<const void *, int>, int> attr;  // the attribute only ever grows per (kernel, device)
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(fn, dev, block, smem, smem_attr);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int &cur = attr[std::make_pair(fn, dev)];
+    if (smem_attr > cur) {
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_attr));
+        cur = smem_attr;
+    }
+    int per_sm = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+    per_sm = std::max(per_sm, 1);
+    cache.emplace(key, per_sm);
+    return per_sm;
+}
+
+namespace {
 
 float time_role(DevState &D, DCsr &A, int role, double *x, double *y1, double *y2, double *y3, cudaEvent_t e0,
                 cudaEvent_t e1) {
@@ -609,18 +730,25 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
     cudaEvent_t e0, e1;
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
-    if (A.fmt == 2) {  // SELL-VI: entries in flight per lane (bitwise-equal results for every U)
+    if (A.fmt == 2) {  // SELL-VI: entries in flight per lane (bitwise-equal results for every U) and,
+                       // windowed, the windows staged per CTA
         float best = 1e30f;
-        int bu = A.U;
-        for (int U : {1, 2, 4}) {
-            A.U = U;
-            const float ms = time_role(D, A, role, x, y1, y2, y3, e0, e1);
-            if (ms < best) {
-                best = ms;
-                bu = U;
+        int bu = A.U, bb = A.nbuf;
+        for (int nb : {2, 1}) {
+            if (nb == 1 && !A.win) continue;
+            for (int U : {1, 2, 4}) {
+                A.U = U;
+                A.nbuf = nb;
+                const float ms = time_role(D, A, role, x, y1, y2, y3, e0, e1);
+                if (ms < best) {
+                    best = ms;
+                    bu = U;
+                    bb = nb;
+                }
             }
         }
         A.U = bu;
+        A.nbuf = bb;
         A.tuned_us = best / 3.f * 1000.f;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
@@ -812,22 +940,14 @@ void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStrea
             const size_t full2 = base2 + (size_t)L.K.stored * 12 + sizeof(int) * (size_t)(n + 1);
             const int staged2 = full2 <= 200 * 1024 ? 1 : 0;
             const size_t smem2 = staged2 ? full2 : base2;
-            static size_t attr2 = 0;
-            if (smem2 > 48 * 1024 && smem2 > attr2) {
-                CUDA_OK(cudaFuncSetAttribute(dev::k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-                attr2 = smem2;
-            }
+            if (smem2 > 48 * 1024) (void)resident_ctas((const void *)dev::k_coarse_cg, 1024, (int)smem2, (int)smem2);
             dev::k_coarse_cg<<<1, 1024, smem2, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.diag, b, x, D.coarse_tol,
                                                     D.coarse_maxit, staged2, p2p_of(D, first_rep));
             D.launches_total++;
             CUDA_OK(cudaGetLastError());
             return;
         }
-        static size_t attr = 0;
-        if (smem > 48 * 1024 && smem > attr) {
-            CUDA_OK(cudaFuncSetAttribute(dev::k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = smem;
-        }
+        if (smem > 48 * 1024) (void)resident_ctas((const void *)dev::k_coarse_solve, 1024, (int)smem, (int)smem);
         dev::k_coarse_solve<<<1, 1024, smem, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps, staged,
                                                   p2p_of(D, first_rep));
         D.launches_total++;
@@ -1241,6 +1361,11 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
     D.pp.flags_off = (long long)kFlagsOff;
     D.pp.dslot_off = (long long)kDslotOff;
     D.pp.wait_mask = ~0u;
+    D.pp.spin_max = 1ll << 26;
+    if (const char *sm = std::getenv("AMG_P2P_SPIN_MAX")) {
+        const long long v = std::atoll(sm);
+        if (v > 0) D.pp.spin_max = v;
+    }
     // every rank has mapped every slab before any kernel may store into one
     std::vector<int64_t> one(1, 1);
     (void)nccl_allgather_i64(D, one);
@@ -1286,6 +1411,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         D->coarse_tol = H.prm.coarse_tol;
         D->coarse_maxit = H.prm.coarse_maxit;
         if (const char *e = std::getenv("AMG_GRAPHS")) D->graphs = std::atoi(e) != 0;
+        if (const char *e = std::getenv("AMG_DEVICE_LOOP")) D->dev_loop = std::atoi(e) != 0;
         if (const char *e = std::getenv("AMG_PROF_LEVELS")) D->lvl_prof = std::atoi(e) != 0 && !D->graphs;
         const int nr = dist ? dist->nranks : 1;
         D->rank = dist ? dist->rank : 0;
@@ -1520,17 +1646,33 @@ static void prof_collect(DevState &D, size_t ev0 = 0, size_t ev1 = (size_t)-1, b
     if (reset) D.ev_used = 0;
 }
 
+// Every captured graph (per-iteration segments, the device loop): dropped when a launch
+// configuration changes.
+void drop_graphs(DevState &D) {
+    for (auto &sg : D.seg)
+        if (sg.exec) {
+            cudaGraphExecDestroy(sg.exec);
+            sg.exec = nullptr;
+        }
+    if (D.loop.exec) {
+        cudaGraphExecDestroy(D.loop.exec);
+        D.loop.exec = nullptr;
+    }
+}
+
 // One PCG iteration on the device: z = V(r) with ρ = rᵀz (kind 0: initial, 1: with β), p = z + βp,
 // q = Kp with α = ρ/pᵀq, u += αp, r −= αq, ‖r‖², and the 64-byte scalar block copied to pinned host
-// memory.  No host decision inside, so it is captured once into a CUDA graph and replayed.
-static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
+// memory.  No host decision inside, so it is captured once into a CUDA graph and replayed.  In the
+// device loop (ctl != nullptr) the first-iteration choice is read from the loop control and the scalars
+// stay on the device.
+static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st, dev::LoopCtl *ctl = nullptr) {
     DLevel &L0 = D.lev[0];
     const int64_t n = L0.n;
     const int flex = D.krylov == 1;
     if (flex) vcycle(D, D.r, D.z, st, dev::DOT_ZQ, D.q);  // FCG: zᵀq_prev (all-reduced)
     else vcycle(D, D.r, D.z, st, dev::DOT_RZ);            // CG: ρ = rᵀz (all-reduced)
     dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0, flex,
-                                                           push_of(D, L0.K, D.p), p2p_of(D, L0.K));
+                                                           push_of(D, L0.K, D.p), p2p_of(D, L0.K), ctl);
     dev::k_roll_rho<<<1, 1, 0, st>>>(D.S);
     D.launches_total += 2;
     {
@@ -1549,7 +1691,58 @@ static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st) {
     D.launches_total++;
     allreduce_dot(D, dev::DOT_RR, st);
     CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
+    if (!ctl) CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));
+}
+
+// The whole iteration loop as ONE graph launch: a conditional WHILE node (default 1, re-armed at every
+// launch) whose body is one iteration (enqueue_segment with the device loop control) followed by
+// k_loop_ctl, which counts, records ‖r_k‖/‖F‖ and clears the condition on convergence, breakdown or
+// maxit.  No host round trip per iteration (the paper names launch latency as what
+// dominates at small local sizes).
+static void run_device_loop(DevState &D, double *u, cudaStream_t st) {
+    if (!D.loop.exec || D.loop.u != u) {
+        if (D.loop.exec) {
+            cudaGraphExecDestroy(D.loop.exec);
+            D.loop.exec = nullptr;
+        }
+        if (!D.cap) CUDA_OK(cudaStreamCreateWithFlags(&D.cap, cudaStreamNonBlocking));
+        cudaGraph_t g = nullptr;
+        CUDA_OK(cudaGraphCreate(&g, 0));
+        try {
+            cudaGraphConditionalHandle h;
+            CUDA_OK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            CUDA_OK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            const int64_t nk0 = D.launches_total;
+            CUDA_OK(cudaStreamBeginCaptureToGraph(D.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_segment(D, 1, u, D.cap, D.ctl);
+                dev::k_loop_ctl<<<1, 1, 0, D.cap>>>(D.S, D.ctl, D.krylov == 1 ? 1 : 0, h);
+                CUDA_OK(cudaGetLastError());
+            } catch (...) {
+                cudaGraph_t gb;
+                cudaStreamEndCapture(D.cap, &gb);
+                throw;
+            }
+            cudaGraph_t gb;
+            CUDA_OK(cudaStreamEndCapture(D.cap, &gb));
+            D.loop.nk = D.launches_total - nk0 + 1;
+            D.launches_total = nk0;
+            CUDA_OK(cudaGraphInstantiate(&D.loop.exec, g, 0));
+        } catch (...) {
+            cudaGraphDestroy(g);
+            throw;
+        }
+        CUDA_OK(cudaGraphDestroy(g));
+        D.loop.u = u;
+    }
+    CUDA_OK(cudaGraphLaunch(D.loop.exec, st));
 }
 
 static void run_segment(DevState &D, int kind, double *u, cudaStream_t st) {
@@ -1644,6 +1837,37 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     if (rn <= rtol * nF) return AMG_OK;
     prof_collect(D);
     amg_status status = AMG_NOT_CONVERGED;
+    // device loop: graphs on, no per-kernel profiling events, one GPU or the P2P transport (NCCL calls
+    // stay out of conditional bodies)
+    if (maxit > 0 && D.graphs && D.dev_loop && !D.prof && !D.lvl_prof && (D.nranks <= 1 || D.p2p)) {
+        if (D.hist_cap < maxit + 1) {
+            D.hist_cap = std::max(maxit + 1, 256);
+            D.dhist = D.alloc_n<double>(D.hist_cap);
+        }
+        if (!D.ctl) {
+            D.ctl = D.alloc_n<dev::LoopCtl>(1);
+            CUDA_OK(cudaMallocHost(&D.hctl, sizeof(dev::LoopCtl)));
+        }
+        *D.hctl = dev::LoopCtl{0, maxit, 1, 1, nF, rtol * nF, D.dhist};
+        CUDA_OK(cudaMemcpyAsync(D.ctl, D.hctl, sizeof(dev::LoopCtl), cudaMemcpyHostToDevice, st));
+        run_device_loop(D, u, st);
+        CUDA_OK(cudaMemcpyAsync(D.hctl, D.ctl, sizeof(dev::LoopCtl), cudaMemcpyDeviceToHost, st));
+        std::vector<double> hh;
+        if (hist) {
+            hh.resize(maxit + 1);
+            CUDA_OK(cudaMemcpyAsync(hh.data(), D.dhist, sizeof(double) * (maxit + 1), cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_OK(cudaStreamSynchronize(st));
+        const int k = D.hctl->k;
+        const bool brk = D.hctl->status == -5;
+        const int kl = brk ? k - 1 : k;  // the last iteration whose residual was recorded
+        D.launches_total += D.loop.nk * k;
+        *iters = k;
+        if (kl >= 1) CUDA_OK(cudaMemcpy(relres, D.dhist + kl, sizeof(double), cudaMemcpyDeviceToHost));
+        if (hist)
+            for (int j = 1; j <= kl; j++) hist[j] = hh[j];
+        return brk ? AMG_ENOTSPD : D.hctl->status == 0 ? AMG_OK : AMG_NOT_CONVERGED;
+    }
     for (int k = 1; k <= maxit; k++) {
         // iteration k: [z = V(r); ρ = rᵀz; p = z + βp] then q = Kp, α, u += αp, r −= αq, ‖r‖²
         run_segment(D, k == 1 ? 0 : 1, u, st);
@@ -1836,17 +2060,14 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
     if (op > 0 && level == D->nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
     DLevel &L = D->lev[level];
     DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
-    if (A.fmt == 2) {  // SELL-VI: only U (entries in flight per lane) is free
-        if (kernel != 0 || G != 32 || !(U == 1 || U == 2 || U == 4))
-            throw Error{AMG_EINVAL, "SELL-VI operator: kernel 0, G 32 and U 1, 2 or 4"};
+    if (A.fmt == 2) {  // SELL-VI: only U (entries in flight per lane) is free; windowed: kernel = windows staged
+        if ((A.win ? !(kernel == 1 || kernel == 2) : kernel != 0) || G != 32 || !(U == 1 || U == 2 || U == 4))
+            throw Error{AMG_EINVAL, "SELL-VI operator: kernel 0 (windowed: 1 or 2), G 32 and U 1, 2 or 4"};
         CUDA_OK(cudaDeviceSynchronize());
         A.U = U;
+        if (A.win) A.nbuf = kernel;
         A.tuned_us = 0.f;
-        for (auto &sg : D->seg)
-            if (sg.exec) {
-                cudaGraphExecDestroy(sg.exec);
-                sg.exec = nullptr;
-            }
+        drop_graphs(*D);
         return AMG_OK;
     }
     if (A.fmt != 0) throw Error{AMG_EINVAL, "operator is not in a CSR layout"};
@@ -1863,11 +2084,7 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
     A.U = U;
     A.tuned_us = 0.f;
     build_gorder(*D, A);
-    for (auto &sg : D->seg)  // captured graphs hold the old launch configuration
-        if (sg.exec) {
-            cudaGraphExecDestroy(sg.exec);
-            sg.exec = nullptr;
-        }
+    drop_graphs(*D);  // captured graphs hold the old launch configuration
     if (level == 0 && op == 0) D->bytes_dominant = A.alg_bytes() + 56.0 * (double)L.n;
     return AMG_OK;
     API_END
@@ -1880,8 +2097,8 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     if (op > 0 && level == D->nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
     const DLevel &L = D->lev[level];
     const DCsr &A = op == 0 ? L.K : op == 1 ? L.P : L.R;
-    cfg->layout = A.fmt;
-    cfg->kernel = A.kern | (A.pf << 2);
+    cfg->layout = A.fmt == 2 && A.win ? 3 : A.fmt;
+    cfg->kernel = A.fmt == 2 ? (A.win ? A.nbuf : 0) : A.kern | (A.pf << 2);
     cfg->G = A.G;
     cfg->U = A.U;
     cfg->stored = A.stored;
@@ -1891,7 +2108,7 @@ extern "C" amg_status amg_operator_config(amg_hierarchy *H, int level, int op, a
     cfg->n_values = A.nvals;
     cfg->value_index_bytes = !A.vtab ? 0 : (A.fmt == 2 || (A.vpk && (A.kern & 2))) ? 2 : 4;
     cfg->sellvi_parts = A.fmt == 2 ? 1 << A.lparts : 0;
-    cfg->offset_bits = A.fmt == 2 ? A.obits : 0;
+    cfg->offset_bits = A.fmt == 2 ? (A.win ? A.pbits : A.obits) : 0;
     return AMG_OK;
     API_END
 }

@@ -37,6 +37,18 @@ struct DevBuf {
 // (C3's K₀: 1,054 values; C4's: 4,147).  At U = 4 the kernel's 80 registers allow 3 CTAs of 256 threads
 // per SM, and 3 × 64 KB still fits the SM's shared memory, so staging never lowers the occupancy there.
 constexpr int64_t kSellviSmemVals = 8192;
+// windowed SELL-VI (k_sellviw): slices per block (= warps per CTA), the largest staged window
+// (doubles; 2 buffers + a 1,054-value table = 104 KB at C3 where the windows are ≤ 5,950), and the
+// column gap below which two runs of a window are merged rather than copied separately
+constexpr int kWinSlices = dev::kBlock / 32;
+constexpr int64_t kWinMax = 7168;
+constexpr int64_t kWinGap = 8;
+
+// Resident CTAs per SM of kernel `fn` at (block, dynamic smem) on the CURRENT device, after raising
+// its max-dynamic-shared-memory attribute to `smem_attr` there (0: leave it).  Function attributes
+// are per device/context, so both are cached per (kernel, device, smem, smem_attr), under a mutex
+// (device.cu).
+int resident_ctas(const void *fn, int block, int smem, int smem_attr = 0);
 
 struct DCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;  // stored: entries incl. padding
@@ -65,6 +77,15 @@ struct DCsr {
     uint32_t *vidx = nullptr;
     uint32_t *vpk = nullptr;
     int obits = 16;  // SELL-VI: column-offset bits of a word (the value index takes the other 32 − obits)
+    // windowed SELL-VI (k_sellviw, single GPU): words hold (window position | value index << pbits);
+    // binfo per block of kWinSlices slices {first run, end run, window doubles, -}, wruns {first
+    // column, doubles, window offset, -}; wmax = the largest window (doubles)
+    bool win = false;
+    int pbits = 0, wmax = 0;
+    int64_t nruns = 0;
+    int4 *binfo = nullptr;
+    int4 *wruns = nullptr;
+    int nbuf = 2;  // windows staged per CTA: 2 (double-buffered) or 1 (autotuned with U)
     // SELL-VI: the slices of the last (partial) round — slice positions >= nwhole — are split into
     // 2^lparts parts of consecutive quads, one warp each, so the tail round is short; partial = the
     // parts' two chains per row, sticket = per-slice arrival counters (zero between launches)
@@ -77,6 +98,9 @@ struct DCsr {
     // vectors are counted by the caller
     double alg_bytes() const {
         const double z = (double)nnz, rows = (double)nrows;
+        if (fmt == 2 && win)  // windowed SELL-VI: 4 B word per entry, the table, slice offsets, block runs
+            return 4.0 * z + 8.0 * (double)nvals + 8.0 * (double)((nrows + 31) / 32 + 1) +
+                   16.0 * (double)(nruns + (nrows + 32 * kWinSlices - 1) / (32 * kWinSlices));
         if (fmt == 2)  // SELL-VI: 4 B word per entry, the value table, row bases, slice offsets
             return 4.0 * z + 8.0 * (double)nvals + 4.0 * rows + 8.0 * (double)((nrows + 31) / 32 + 1);  // padding excluded
         if (kern & 8) {
@@ -185,6 +209,18 @@ struct DevState {
         size_t ev0 = 0, ev1 = 0;
         int64_t nk = 0;
     } seg[2];
+    // device-side loop (AMG_DEVICE_LOOP, default on with graphs, 1 GPU or the P2P transport): one
+    // graph with a conditional WHILE node around one iteration + k_loop_ctl
+    bool dev_loop = true;
+    dev::LoopCtl *ctl = nullptr;   // device
+    dev::LoopCtl *hctl = nullptr;  // pinned host mirror
+    double *dhist = nullptr;       // device history, capacity hist_cap
+    int hist_cap = 0;
+    struct Loop {
+        cudaGraphExec_t exec = nullptr;
+        double *u = nullptr;
+        int64_t nk = 0;  // kernels per iteration
+    } loop;
 
     void *alloc(size_t bytes);  // through the allocator hook (device.cu)
     template <class T>

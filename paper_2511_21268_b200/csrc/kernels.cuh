@@ -34,6 +34,18 @@ struct Scalars {
     double pad;
 };
 
+// Device-side Krylov loop (one CUDA graph per solve: a conditional WHILE node whose body is one
+// iteration + k_loop_ctl, which takes the stopping decision on the device and sets the condition).
+struct LoopCtl {
+    int k;         // iterations completed
+    int maxit;
+    int status;    // amg_status of the loop: 0 converged, 1 maxit reached, -5 breakdown
+    int first;     // 1 until the first iteration's p = z has run
+    double nF;     // ‖F‖₂
+    double thr;    // rtol·‖F‖₂
+    double *hist;  // [maxit + 1] device: ‖r_k‖/‖F‖
+};
+
 enum DotKind { DOT_NONE = 0, DOT_FF, DOT_RR, DOT_PQ, DOT_RZ, DOT_PR, DOT_ZQ, DOT_NKINDS };
 
 __device__ __forceinline__ double *scalar_slot(Scalars *S, int kind) {
@@ -84,6 +96,7 @@ struct P2P {
     const int *gorder;
     long long nbnd;
     unsigned *bticket;           // own slab: warp ticket of the early publication (zero between launches)
+    long long spin_max;          // polls (100 ns apart) before a wait traps: AMG_P2P_SPIN_MAX, default 2^26 ≈ 7 s
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -98,7 +111,8 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 // Kernel prologue: wait until every rank in wait_mask has completed as many participating kernels as
 // this one.  A kernel that gathers ghosts pushed by rank q, or pushes into rank q's ghost slots, has q in
 // its mask (RAW and WAR across ranks); dot products and the all-gather wait for every rank.
-// Bounded: a peer that never arrives (a dead rank) traps after ~10 s instead of hanging the GPU.
+// Bounded: a peer that never arrives (a dead rank) traps after pp.spin_max polls (AMG_P2P_SPIN_MAX;
+// default ≈ 7 s) instead of hanging the GPU.  Callers enter a solve on every rank within that bound.
 __device__ __forceinline__ void peer_wait(const P2P &pp) {
     if (pp.nranks == 0) return;
     if (threadIdx.x == 0) {
@@ -108,7 +122,7 @@ __device__ __forceinline__ void peer_wait(const P2P &pp) {
             long long spins = 0;
             while (ld_acquire_sys(pp.flags + q) < e) {
                 __nanosleep(100);
-                if (++spins > (1ll << 26)) __trap();
+                if (++spins > pp.spin_max) __trap();
             }
         }
     }
@@ -125,7 +139,7 @@ __device__ __forceinline__ void peer_wait_warp(const P2P &pp) {
             long long spins = 0;
             while (ld_acquire_sys(pp.flags + q) < e) {
                 __nanosleep(100);
-                if (++spins > (1ll << 26)) __trap();
+                if (++spins > pp.spin_max) __trap();
             }
         }
     }
@@ -1137,6 +1151,132 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
     peer_signal(pp);
 }
 
+// ------------------------------------------------------------------------------------------------
+// The windowed SELL-VI core k_sellviw: the gathered vector staged in shared memory by TMA.
+// ------------------------------------------------------------------------------------------------
+// k_sellvi is bound by the L1 data pipe, not by HBM (ncu, C3 level 0: 78-82 % of the LSU wavefronts,
+// 64 % of DRAM): a warp's x-gather of 32 consecutive doubles at an arbitrary offset costs ≈ 2.9 L1
+// wavefronts (3 lines) plus tag work, the table lookup ≈ 1.6 and the word stream 1 per 32 entries.
+// Here a CTA's 8 warps take 8 CONSECUTIVE slices (a block of 256 rows) and the union of the columns
+// those rows touch — a few contiguous runs: for the 3-D stencil one run per z-offset, (rows + 2·p·m_x·
+// (m_y+1)) doubles — is copied into shared memory with cp.async.bulk (one bulk copy per run, completion
+// on an mbarrier) before the warps need it.  Each entry's word holds the POSITION of its column in the
+// staged window (pbits bits) instead of an offset from a row base, so the gather is one ld.shared of
+// 32 consecutive doubles: 2 wavefronts, conflict-free, no tag lookups, no L2 round trip on the
+// critical path.  NBUF = 2 stages block b+1's window while block b is computed (the copies of the
+// next block are issued at the top of the iteration, after the barrier that retired its buffer);
+// NBUF = 1 issues them after that barrier and relies on the other resident CTAs to cover the latency.
+// Block layout (host, device.cu upload_sellvi): binfo[b] = {first run, end run, window doubles, -};
+// runs[r] = {first column, doubles (even), window offset (even), -}; columns and lengths are even so
+// every copy is 16-B aligned (the vector must be 16-B aligned: single-GPU layout).  Summation order
+// is k_sellvi's (chain k & 1 per entry k of a row), so results are bitwise those of k_sellvi.
+template <int U, class Epi, int NBUF, bool kSmem>
+__global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
+                                                    const int4 *__restrict__ binfo, const int4 *__restrict__ runs,
+                                                    const double *__restrict__ gtable, int nvals, int pbits, int wmax,
+                                                    const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc) {
+    constexpr int WPB = kBlock / 32;  // warps per CTA = slices per block
+    extern __shared__ __align__(16) double wsm[];
+    __shared__ __align__(8) uint64_t bar[NBUF];
+    const int tabn = kSmem ? ((nvals + 1) & ~1) : 0;
+    double *tab = wsm;
+    double *xw = wsm + tabn;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t nslices = (nrows + 31) >> 5;
+    const int64_t nblk = (nslices + WPB - 1) / WPB;
+    const unsigned pmask = (1u << pbits) - 1u;
+    const uint64_t pol = stream_policy();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NBUF; k++) mbar_init(&bar[k], 1);
+        fence_mbar_init();
+    }
+    if constexpr (kSmem) {
+        for (int i = threadIdx.x; i < nvals; i += blockDim.x) tab[i] = __ldg(gtable + i);
+    }
+    __syncthreads();
+    const double *table = kSmem ? tab : gtable;
+    // warp 0 stages block `b` into buffer `buf`: lane 0 arms the barrier with the window's bytes, then
+    // the lanes issue one bulk copy per run
+    auto stage = [&](int64_t b, int buf) {
+        const int4 bi = __ldg(binfo + b);
+        if (lane == 0) mbar_arrive_expect_tx(&bar[buf], (uint32_t)bi.z * 8u);
+        __syncwarp();
+        for (int r = bi.x + lane; r < bi.y; r += 32) {
+            const int4 ru = __ldg(runs + r);
+            bulk_g2s(xw + (int64_t)buf * wmax + ru.z, g + ru.x, (uint32_t)ru.y * 8u, &bar[buf], keep_policy());
+        }
+    };
+    typename Epi::Acc dacc{};
+    int64_t blk = blockIdx.x;
+    if (wib == 0 && blk < nblk) stage(blk, 0);
+    for (int it = 0; blk < nblk; blk += gridDim.x, it++) {
+        const int buf = NBUF == 2 ? (it & 1) : 0;
+        if (NBUF == 2 && wib == 0 && blk + gridDim.x < nblk) stage(blk + gridDim.x, buf ^ 1);
+        const int64_t sl = blk * WPB + wib;
+        const int64_t row = (sl << 5) + lane;
+        typename Epi::Pre pre{};
+        if (sl < nslices && row < nrows) pre = epi.load(row);  // epilogue inputs in flight with the stream
+        mbar_wait(&bar[buf], (uint32_t)((it / NBUF) & 1));
+        if (sl < nslices) {
+            const double *xb = xw + (int64_t)buf * wmax;
+            const int64_t off = __ldg(soff + sl);
+            const int W4 = (int)(__ldg(soff + sl + 1) - off);
+            const uint4 *wp = w + (off << 5) + lane;
+            double s0 = 0.0, s1 = 0.0;
+            int q = 0;
+            uint4 wa[U], wn[U];
+            if (U <= W4) {
+#pragma unroll
+                for (int u = 0; u < U; u++) wa[u] = ld_stream(wp + (int64_t)u * 32, pol);
+            }
+            for (; q + U <= W4; q += U) {
+                const bool more = q + 2 * U <= W4;
+                if (more) {
+#pragma unroll
+                    for (int u = 0; u < U; u++) wn[u] = ld_stream(wp + (int64_t)(q + U + u) * 32, pol);
+                }
+                double va[4 * U], xa[4 * U];
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> pbits);
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) xa[4 * u + j] = xb[quad_at(wa[u], j) & pmask];
+#pragma unroll
+                for (int u = 0; u < 4 * U; u += 2) {
+                    s0 = fma(va[u], xa[u], s0);
+                    s1 = fma(va[u + 1], xa[u + 1], s1);
+                }
+                if (more) {
+#pragma unroll
+                    for (int u = 0; u < U; u++) wa[u] = wn[u];
+                }
+            }
+            for (; q < W4; q++) {
+                const uint4 wq = ld_stream(wp + (int64_t)q * 32, pol);
+                double va[4], xa[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) va[j] = tab_at<kSmem>(table, quad_at(wq, j) >> pbits);
+#pragma unroll
+                for (int j = 0; j < 4; j++) xa[j] = xb[quad_at(wq, j) & pmask];
+                s0 = fma(va[0], xa[0], s0);
+                s1 = fma(va[1], xa[1], s1);
+                s0 = fma(va[2], xa[2], s0);
+                s1 = fma(va[3], xa[3], s1);
+            }
+            if (row < nrows) acc_add(dacc, epi(row, s0 + s1, pre));
+        }
+        __syncthreads();  // every warp is done with `buf`: it may be refilled
+        if (NBUF == 1 && wib == 0 && blk + gridDim.x < nblk) {
+            fence_proxy_async();
+            stage(blk + gridDim.x, 0);
+        }
+    }
+    if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+}
+
 // Non-template kernels are defined in device.cu only (AMGB_PLAIN_KERNELS); the inst_*.cu units see
 // just the templated streaming cores above.
 #ifdef AMGB_PLAIN_KERNELS
@@ -1225,9 +1365,10 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *
 
 // a11: p = z + β p  (first iteration: p = z)
 __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__restrict__ z, double *__restrict__ p,
-                                                      const Scalars *__restrict__ S, int first, int flex, Push push,
-                                                      P2P pp) {
+                                                      const Scalars *__restrict__ S, int first_, int flex, Push push,
+                                                      P2P pp, const LoopCtl *__restrict__ ctl) {
     peer_wait(pp);
+    const int first = ctl ? ctl->first : first_;  // device loop: the first iteration is decided on the device
     // CG: β = ρ/ρ_prev; FCG(1): β = −zᵀq_prev / pᵀq_prev (S->pq still holds the previous iteration's)
     const double beta = first ? 0.0 : flex ? -S->zq / S->pq : S->rz / S->rz_prev;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
@@ -1240,6 +1381,32 @@ __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__
 
 // end of a PCG iteration: ρ_prev <- ρ (one thread; after every consumer of ρ in this iteration)
 __global__ void k_roll_rho(Scalars *S) { S->rz_prev = S->rz; }
+
+// Device loop control, after iteration k's ‖r‖² (c.19 stopping test, as the host loop takes it):
+// breakdown (CG: rᵀz <= 0; pᵀKp <= 0), ‖r_k‖ <= rtol·‖F‖, or k == maxit end the WHILE loop.  Every
+// rank holds the same all-reduced scalars, so every rank takes the same decision.
+__global__ void k_loop_ctl(const Scalars *__restrict__ S, LoopCtl *__restrict__ c, int flex,
+                           cudaGraphConditionalHandle h) {
+    const int k = c->k + 1;
+    c->k = k;
+    c->first = 0;
+    unsigned go = 1;
+    if ((!flex && !(S->rz > 0.0)) || !(S->pq > 0.0)) {
+        c->status = -5;
+        go = 0;
+    } else {
+        const double rn = sqrt(S->rr);
+        c->hist[k] = rn / c->nF;
+        if (rn <= c->thr) {
+            c->status = 0;
+            go = 0;
+        } else if (k >= c->maxit) {
+            c->status = 1;
+            go = 0;
+        }
+    }
+    cudaGraphSetConditional(h, go);
+}
 
 // gather/scatter helpers of the multi-GPU path
 __global__ void __launch_bounds__(kBlock) k_pack(int64_t n, const int *__restrict__ idx, const double *__restrict__ x,

@@ -9,18 +9,9 @@ template <int G, int U, class Epi, class Cols>
 void launch_csr4t_gu(DevState &D, const DCsr &A, const Cols &cols, const double *g, Epi epi, cudaStream_t st,
                      int dotkind) {
     constexpr int smem = dev::TmaCfg<U, Cols::kIdxBytes>::SMEM;
-    static bool attr_set = false;  // per instantiation; device-independent attribute
-    if (!attr_set) {
-        CUDA_OK(cudaFuncSetAttribute(dev::k_csr4t<G, U, Epi, Cols>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
-    }
     const int64_t ngroups = (A.nrows + G - 1) / G;
     const int64_t wpb = dev::kBlockT / 32;
-    static int per_sm = 0;  // resident CTAs per SM of this instantiation (registers + shared memory)
-    if (!per_sm) {
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_csr4t<G, U, Epi, Cols>, dev::kBlockT, smem));
-        per_sm = std::max(per_sm, 1);
-    }
+    const int per_sm = resident_ctas((const void *)dev::k_csr4t<G, U, Epi, Cols>, dev::kBlockT, smem, smem);
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
     dev::k_csr4t<G, U, Epi, Cols><<<grid, dev::kBlockT, smem, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
@@ -32,11 +23,7 @@ void launch_csr2_gu(DevState &D, const DCsr &A, const Cols &cols, const double *
                     int dotkind) {
     const int64_t ngroups = (A.nrows + G - 1) / G;
     const int64_t warps_per_block = dev::kBlock / 32;
-    static int per_sm = 0;  // resident CTAs per SM of this instantiation
-    if (!per_sm) {
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_csr2<G, U, Epi, Cols>, dev::kBlock, 0));
-        per_sm = std::max(per_sm, 1);
-    }
+    const int per_sm = resident_ctas((const void *)dev::k_csr2<G, U, Epi, Cols>, dev::kBlock, 0);
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, (int64_t)per_sm * D.nsm));
@@ -86,11 +73,7 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
         const double2 *v2 = reinterpret_cast<const double2 *>(A.v);
         const int64_t nsl = (A.nrows + 31) / 32;
         const int64_t wpb = dev::kBlock / 32;
-        static int per_sm = 0;
-        if (!per_sm) {
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sell2<Epi>, dev::kBlock, 0));
-            per_sm = std::max(per_sm, 1);
-        }
+        const int per_sm = resident_ctas((const void *)dev::k_sell2<Epi>, dev::kBlock, 0);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
         dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind),
                                                          (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));

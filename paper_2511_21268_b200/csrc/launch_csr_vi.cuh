@@ -16,21 +16,32 @@ void launch_csr_vi(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStr
 
 // Value tables of up to kSellviSmemVals entries are staged in shared memory per CTA (devstate.cuh).
 
+template <int U, class Epi, int NBUF, bool kSmem>
+void launch_sellviw(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    if (((uintptr_t)g & 15) != 0) throw Error{AMG_EINVAL, "windowed SELL-VI: the multiplied vector must be 16-B aligned"};
+    const int64_t nsl = (A.nrows + 31) / 32;
+    const int64_t nblk = (nsl + kWinSlices - 1) / kWinSlices;
+    const int tabn = kSmem ? (int)((A.nvals + 1) & ~1) : 0;
+    const int smem = 8 * (tabn + NBUF * A.wmax);
+    const int per_sm = resident_ctas((const void *)dev::k_sellviw<U, Epi, NBUF, kSmem>, dev::kBlock, smem, smem);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)per_sm * D.nsm));
+    dev::k_sellviw<U, Epi, NBUF, kSmem><<<grid, dev::kBlock, smem, st>>>(
+        A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.binfo, A.wruns, A.vtab, (int)A.nvals, A.pbits, A.wmax, g,
+        A.nrows, epi, dotctx(D, dotkind));
+}
+
 template <int U, class Epi, bool kSmem>
 void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream_t st, int dotkind) {
+    if (A.win) {
+        if (A.nbuf == 1) launch_sellviw<U, Epi, 1, kSmem>(D, A, g, epi, st, dotkind);
+        else launch_sellviw<U, Epi, 2, kSmem>(D, A, g, epi, st, dotkind);
+        return;
+    }
     const int64_t nsl = (A.nrows + 31) / 32;
     const int64_t wpb = dev::kBlock / 32;
     const int smem = kSmem ? (int)(A.nvals * 8) : 0;
-    // resident CTAs per SM of this instantiation at this table size (cached for the last size seen)
-    static int per_sm = 0, per_sm_smem = -1;
-    if (per_sm_smem != smem) {
-        if (kSmem)
-            CUDA_OK(cudaFuncSetAttribute(dev::k_sellvi<U, Epi, kSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kSellviSmemVals * 8)));
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sellvi<U, Epi, kSmem>, dev::kBlock, smem));
-        per_sm = std::max(per_sm, 1);
-        per_sm_smem = smem;
-    }
+    const int per_sm = resident_ctas((const void *)dev::k_sellvi<U, Epi, kSmem>, dev::kBlock, smem,
+                                     kSmem ? (int)(kSellviSmemVals * 8) : 0);
     const int lparts = Epi::kDot ? 0 : A.lparts;  // dot epilogues keep whole slices (fixed dot order)
     const int64_t nwhole = lparts ? A.nwhole : nsl;
     const int64_t nitems = nwhole + ((nsl - nwhole) << lparts);

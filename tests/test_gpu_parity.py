@@ -5,6 +5,8 @@ use FMA, so operator applications agree to a few ulps of Σ|a_ij x_j| (checked a
 that bound), one V-cycle to 1e-12 relative (max-norm), the PCG solution after the same number of
 iterations to 1e-10 relative, and PCG iteration counts at rtol 1e-6 within ±1 (north star).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -38,9 +40,11 @@ CASES = {
 _cache = {}
 
 
-# 1 CSR2 (warp per row group), 2 SELL2 (row per lane), 3 CSR4T (TMA-staged rows),
-# 4 CSR2 with 16-bit column offsets, 5 CSR4T with 16-bit column offsets, 6 SELL-VI wherever admissible
-FORMATS = [1, 2, 3, 4, 5, 6]
+# 0 the bench default (the fixed SELL-VI rule for the large K_l / P̄_l, autotuned CSR elsewhere: C2's
+# K_0 and P̄_0 are SELL-VI), 1 CSR2 (warp per row group), 2 SELL2 (row per lane), 3 CSR4T (TMA-staged
+# rows), 4 CSR2 with 16-bit column offsets, 5 CSR4T with 16-bit column offsets, 6 SELL-VI wherever
+# admissible
+FORMATS = [0, 1, 2, 3, 4, 5, 6]
 
 
 def build(case, fmt=0, **kw):
@@ -89,17 +93,18 @@ def test_kernel_configs_bitwise_equal(case):
             keep = H.op_config(l, op)
             x = dev(rng.uniform(-1, 1, A.shape[1]))
             ref = None
-            if keep["layout"] == "sellvi":  # SELL-VI: every U sums in the same order
+            if keep["layout"] in ("sellvi", "sellviw"):  # SELL-VI: every U (and window count) sums alike
                 ys = []
-                for U in (1, 2, 4):
-                    H.set_op_config(l, op, 0, 32, U)
-                    y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
-                    H.apply(l, op, x, y)
-                    ys.append(y.cpu().numpy())
+                for kb in ([1, 2] if keep["layout"] == "sellviw" else [0]):
+                    for U in (1, 2, 4):
+                        H.set_op_config(l, op, kb, 32, U)
+                        y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+                        H.apply(l, op, x, y)
+                        ys.append(y.cpu().numpy())
                 xo = x.cpu().numpy()
                 assert np.all(np.abs(ys[0] - oracle.spmv(A, xo)) <= 1e-13 * (abs(A) @ np.abs(xo)) + 1e-300)
                 assert all(np.array_equal(y, ys[0]) for y in ys)
-                H.set_op_config(l, op, 0, 32, keep["U"])
+                H.set_op_config(l, op, keep["kernel_bits"], 32, keep["U"])
                 continue
             kerns = [0, 1, 2, 3, 4, 6]  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch
             if keep["n_values"]:  # bit 3: value index (CSR-VI), register core
@@ -138,38 +143,85 @@ def test_d16_encoding_bytes():
     assert d16["alg_bytes"] == 10 * nnz + 4 * N + 8 * (N + 1)
 
 
-def test_sellvi_layout():
+@pytest.mark.parametrize("windowed", [0, 1])
+def test_sellvi_layout(windowed, monkeypatch):
     """SELL-VI (format 6; format 0 picks it for the large K_l): row per lane, one 32-bit word per entry
-    (16-bit column offset | 16-bit value index).  The table holds exactly the distinct values (+0.0 of
-    the padding), the reported bytes are 4 B per non-zero + the table + row bases + slice offsets, every U
-    gives bitwise the same y, and y matches the oracle's SpMV on every level's K_l, P̄_l and R_l."""
-    K, F, H, Ho = build("C2", 6)
+    (16-bit column offset | 16-bit value index; windowed: window position | value index).  The table
+    holds exactly the distinct values (+0.0 of the padding), the reported bytes are 4 B per non-zero +
+    the table + row bases + slice offsets (windowed: no row bases; + 16 B per block and per window run),
+    every U (and window count) gives bitwise the same y, and y matches the oracle's SpMV on every level's
+    K_l, P̄_l and R_l."""
+    monkeypatch.setenv("AMG_SELLVI_WIN", str(windowed))
+    amg = _amg()
+    dim, p, n = CASES["C2"]
+    K, F = amg.iga_poisson(dim, p, n)
+    H = amg.Hierarchy(K, amg.params(p, format=6))
+    Ho = build("C2", 6)[3]
+    layout = "sellviw" if windowed else "sellvi"
     rng = np.random.default_rng(11)
     seen = 0
     for l, L in enumerate(Ho.levels):
         ops = [(0, L.K)] + ([] if L.P is None else [(1, L.P), (2, L.R)])
         for op, A in ops:
             c = H.op_config(l, op)
-            if c["layout"] != "sellvi":
+            if c["layout"] not in ("sellvi", "sellviw"):
                 continue
+            if op == 0:
+                assert c["layout"] == layout, (l, op, c)  # every square K_l of C2 admits the windows
             seen += 1
             A = A.tocsr()
             bits = np.unique(np.concatenate([A.data.view(np.uint64), np.zeros(1, np.uint64)]))
             assert c["n_values"] == bits.size
             nr = A.shape[0]
-            assert c["alg_bytes"] == 4 * A.nnz + 8 * bits.size + 4 * nr + 8 * ((nr + 31) // 32 + 1)
+            nsl = (nr + 31) // 32
+            if c["layout"] == "sellvi":
+                assert c["alg_bytes"] == 4 * A.nnz + 8 * bits.size + 4 * nr + 8 * (nsl + 1)
+            else:
+                base = 4 * A.nnz + 8 * bits.size + 8 * (nsl + 1) + 16 * ((nsl + 7) // 8)
+                assert base + 16 * ((nsl + 7) // 8) <= c["alg_bytes"] <= base + 16 * 64 * ((nsl + 7) // 8)
             x = dev(rng.uniform(-1, 1, A.shape[1]))
             ys = []
-            for U in (1, 2, 4):
-                H.set_op_config(l, op, 0, 32, U)
-                y = torch.empty(nr, dtype=torch.float64, device="cuda")
-                H.apply(l, op, x, y)
-                ys.append(y.cpu().numpy())
-            H.set_op_config(l, op, 0, 32, c["U"])
+            for kb in ([1, 2] if c["layout"] == "sellviw" else [0]):
+                for U in (1, 2, 4):
+                    H.set_op_config(l, op, kb, 32, U)
+                    y = torch.empty(nr, dtype=torch.float64, device="cuda")
+                    H.apply(l, op, x, y)
+                    ys.append(y.cpu().numpy())
+            H.set_op_config(l, op, c["kernel_bits"], 32, c["U"])
             xo = x.cpu().numpy()
             assert all(np.array_equal(y, ys[0]) for y in ys)
             assert np.all(np.abs(ys[0] - oracle.spmv(A, xo)) <= 1e-13 * (abs(A) @ np.abs(xo)) + 1e-300)
     assert seen >= 1  # at least C2's K_0 (159 distinct values) qualifies
+
+
+def test_sellvi_windowed_bitwise_equals_plain(monkeypatch):
+    """The windowed core (x staged in shared memory, window positions in the words) sums every row in
+    the plain SELL-VI order: y = A·x on every level and one V-cycle are BITWISE those of the plain
+    layout (AMG_SELLVI_WIN=0), for the bench's format 0 and for format 6."""
+    amg = _amg()
+    dim, p, n = CASES["C2"]
+    for fmt in (0, 6):
+        Hs = {}
+        for wnd in (0, 1):
+            monkeypatch.setenv("AMG_SELLVI_WIN", str(wnd))
+            K, F = amg.iga_poisson(dim, p, n)
+            Hs[wnd] = amg.Hierarchy(K, amg.params(p, format=fmt))
+        assert Hs[1].op_config(0, 0)["layout"] == "sellviw" and Hs[0].op_config(0, 0)["layout"] == "sellvi"
+        info = Hs[0].info()
+        rng = np.random.default_rng(31)
+        for l in range(info["levels"]):
+            for op in ((0, 1, 2) if l + 1 < info["levels"] else (0,)):
+                nr = info["N"][l] if op < 2 else info["N"][l + 1]
+                ncol = info["N"][l] if op != 1 else info["N"][l + 1]
+                x = dev(rng.uniform(-1, 1, ncol))
+                ys = []
+                for wnd in (0, 1):
+                    y = torch.empty(nr, dtype=torch.float64, device="cuda")
+                    Hs[wnd].apply(l, op, x, y)
+                    ys.append(y.cpu().numpy())
+                assert np.array_equal(ys[0], ys[1]), (fmt, l, op)
+        r = dev(amg_inputs.uniform_pm1(info["N"][0], seed=41))
+        assert torch.equal(Hs[0].vcycle(r), Hs[1].vcycle(r)), fmt
 
 
 def test_sellvi_wide_offsets():
@@ -190,11 +242,19 @@ def test_sellvi_wide_offsets():
     n = A.shape[0]
     H = amg.Hierarchy(A, amg.params(2, format=6))
     c = H.op_config(0, 0)
-    assert c["layout"] == "sellvi"
+    assert c["layout"] == "sellviw"  # the windows (3 runs of ~650 columns per block) make the width moot
+    os.environ["AMG_SELLVI_WIN"] = "0"
+    try:
+        H0 = amg.Hierarchy(A, amg.params(2, format=6))
+    finally:
+        del os.environ["AMG_SELLVI_WIN"]
+    c = H0.op_config(0, 0)
+    assert c["layout"] == "sellvi" and c["offset_bits"] == 17
     x = np.random.default_rng(4).uniform(-1, 1, n)
-    y = torch.empty(n, dtype=torch.float64, device="cuda")
-    H.apply(0, 0, dev(x), y)
-    assert np.allclose(y.cpu().numpy(), A @ x, rtol=0, atol=1e-13 * 12)
+    for Hh in (H, H0):
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        Hh.apply(0, 0, dev(x), y)
+        assert np.allclose(y.cpu().numpy(), A @ x, rtol=0, atol=1e-13 * 12)
 
 
 @pytest.mark.parametrize("lparts", [1, 2, 3])
@@ -206,6 +266,7 @@ def test_sellvi_split_slices(lparts, monkeypatch):
     amg = _amg()
     K, F, H0, Ho = build("C2", 6)
     monkeypatch.setenv("AMG_SELLVI_PARTS", str(lparts))
+    monkeypatch.setenv("AMG_SELLVI_WIN", "0")  # the split is a feature of the plain (multi-GPU) layout
     H = amg.Hierarchy(amg.iga_poisson(*CASES["C2"])[0], amg.params(CASES["C2"][1], format=6))
     c = H.op_config(0, 0)
     assert c["layout"] == "sellvi" and c["sellvi_parts"] == 1 << lparts
@@ -359,6 +420,35 @@ def test_c3_full_size_properties(fmt):
     assert np.linalg.norm(F - oracle.spmv(Ks, ud)) <= 1.05e-6 * np.linalg.norm(F)
 
 
+def test_c3_paper_solve_vs_oracle_artifact():
+    """The bench's default solve at full size — C3 (k=96, p=3, 941,094 DOFs), the paper's experiment
+    (its data, FCG, §5.1 coarse CG), format 0 (SELL-VI K_0 / P̄_0, autotuned CSR elsewhere) — against
+    the oracle's own C3 solve committed in oracle/sizes_C3.json (written by the oracle-only script
+    oracle/scripts/hierarchy_sizes.py): level sizes and nnz equal, iteration count ±1, the residual
+    history of the oracle's iterations to 1e-8 relative, and the iterate after the oracle's iteration
+    count on every 997th row to 1e-10 of its max."""
+    import json
+    import os
+    amg = _amg()
+    with open(os.path.join(os.path.dirname(oracle.__file__), "sizes_C3.json")) as f:
+        art = json.load(f)
+    K, F = amg.iga_poisson(3, 3, 96, rhs=2)
+    H = amg.Hierarchy(K, amg.params(3, krylov=1, coarse_solver=1))
+    info = H.info()
+    assert info["N"] == art["N"] and info["nnz"] == art["nnz"]
+    Fd = dev(F)
+    ito = art["oracle_iters_paper"]
+    u, it, rr, hist, st = H.solve(Fd, rtol=1e-6, maxit=200)
+    assert st == 0 and abs(it - ito) <= 1, (it, ito)
+    u2, it2, _, hist2, _ = H.solve(Fd, rtol=0.0, maxit=ito)
+    assert it2 == ito
+    assert np.allclose(hist2, art["oracle_hist_paper"], rtol=1e-8, atol=0)
+    idx = list(range(0, K.shape[0], art["u_sample_stride"])) + [K.shape[0] - 1]
+    us = u2.cpu().numpy()[idx]
+    uo = np.array(art["u_sample_paper"])
+    assert np.abs(us - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
 # --- NEXT-1: the paper's own cube experiment (P:L1061-1072, P:L1107, P:L1114) --------------------
 def test_coarse_cg_vcycle_matches_oracle():
     """§5.1 coarsest solver (CG with one weighted-Jacobi sweep as preconditioner) inside the V-cycle:
@@ -406,6 +496,12 @@ def test_paper_cube_experiment(p, n):
     uo, ito, rro, histo, rco = oracle.fcg(Ho, F, rtol=1e-6, maxit=200)
     u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6, maxit=200)
     assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
+    # the iterate after the oracle's iteration count, and the residual history (the §5.1 coarse CG
+    # stops on its 1e-4 tolerance: a round-off change of its stop would show far above these bars)
+    u2, it2, _, hist2, _ = H.solve(dev(F), rtol=0.0, maxit=ito)
+    assert it2 == ito
+    assert np.linalg.norm(u2.cpu().numpy() - uo) <= 1e-9 * np.linalg.norm(uo)
+    assert np.allclose(hist2, histo, rtol=1e-7, atol=0)
     ud = u.cpu().numpy()
     Ks = K.to_scipy()
     assert np.linalg.norm(F - oracle.spmv(Ks, ud)) <= 1.05e-6 * np.linalg.norm(F)
@@ -445,6 +541,12 @@ def test_ring_paper_experiment(p, n):
     uo, ito, rro, histo, rco = oracle.fcg(Ho, F, rtol=1e-6, maxit=200)
     u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6, maxit=200)
     assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
+    # the iterate after the oracle's iteration count, and the residual history (the §5.1 coarse CG
+    # stops on its 1e-4 tolerance: a round-off change of its stop would show far above these bars)
+    u2, it2, _, hist2, _ = H.solve(dev(F), rtol=0.0, maxit=ito)
+    assert it2 == ito
+    assert np.linalg.norm(u2.cpu().numpy() - uo) <= 1e-9 * np.linalg.norm(uo)
+    assert np.allclose(hist2, histo, rtol=1e-7, atol=0)
     ud = u.cpu().numpy()
     assert np.linalg.norm(F - oracle.spmv(K.to_scipy(), ud)) <= 1.05e-6 * np.linalg.norm(F)
 
@@ -483,6 +585,12 @@ def test_lshape_paper_experiment(p, n):
     uo, ito, rro, histo, rco = oracle.fcg(Ho, F, rtol=1e-6, maxit=200)
     u, it, rr, hist, st = H.solve(dev(F), rtol=1e-6, maxit=200)
     assert rco == 0 and st == 0 and abs(it - ito) <= 1, (it, ito)
+    # the iterate after the oracle's iteration count, and the residual history (the §5.1 coarse CG
+    # stops on its 1e-4 tolerance: a round-off change of its stop would show far above these bars)
+    u2, it2, _, hist2, _ = H.solve(dev(F), rtol=0.0, maxit=ito)
+    assert it2 == ito
+    assert np.linalg.norm(u2.cpu().numpy() - uo) <= 1e-9 * np.linalg.norm(uo)
+    assert np.allclose(hist2, histo, rtol=1e-7, atol=0)
     ud = u.cpu().numpy()
     assert np.linalg.norm(F - oracle.spmv(K.to_scipy(), ud)) <= 1.05e-6 * np.linalg.norm(F)
     norm_u = lshape.l2_error_full(p, n, np.zeros_like(ud), np.zeros_like(uD), exact=lshape.exact_u)

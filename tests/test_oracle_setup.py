@@ -162,6 +162,56 @@ def test_worked_example_1d_laplacian():
     assert np.abs(H.levels[1].K.toarray() - Kc).max() <= 1e-15
 
 
+def _random_mmatrix(n: int, seed: int) -> sp.csr_matrix:
+    """A sparse SPD matrix with random negative couplings (no two c_ij equal, so round-off in the
+    check cannot flip a tie): graph Laplacian of a random graph + a random positive shift."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j in rng.choice(n, size=4, replace=False):
+            if j != i:
+                v = -rng.uniform(0.2, 2.0)
+                rows += [i, j]
+                cols += [j, i]
+                vals += [v, v]
+    A = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    A.sum_duplicates()
+    A = A + sp.diags(-np.asarray(A.sum(axis=1)).ravel() + rng.uniform(0.01, 0.1, n))
+    return sp.csr_matrix(A)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_intermediate_galerkin_c10_dense_and_step2_matching(seed):
+    """c.10 pinned directly: the intermediate operator of one pairwise step equals the
+    dense sym(P₁ᵀAP₁) (numpy matmul, an independent route) to round-off; the second matching step
+    run on that dense operator gives the aggregates a 2-step setup builds (composition of the two
+    steps); and the pattern is the structural pattern of P₁ᵀ|A|P₁."""
+    A = _random_mmatrix(300, seed)
+    w = np.ones(A.shape[0])  # w⁽⁰⁾ = 1 (c.6), as the setup below starts
+    mate, agg1, pv1, wn1 = oracle.pairwise(A, w)
+    nc = wn1.size
+    assert nc < A.shape[0]
+    Ac = oracle.galerkin_pairwise(A, agg1, pv1, nc)
+    P1 = np.zeros((A.shape[0], nc))
+    P1[np.arange(A.shape[0]), agg1] = pv1
+    G = P1.T @ A.toarray() @ P1
+    G = 0.5 * (G + G.T)
+    assert np.abs(Ac.toarray() - G).max() <= 1e-14 * np.abs(G).max()
+    pat = (np.abs(P1).T @ np.abs(A.toarray()) @ np.abs(P1)) > 0
+    Acs = Ac.copy()
+    Acs.data[:] = 1.0
+    assert np.array_equal(Acs.toarray() != 0, pat)  # stored pattern = structural P₁ᵀ|A|P₁
+    # step 2 on the dense operator (stored with the same pattern) with the carried test vector w₁
+    Gs = sp.csr_matrix(np.where(pat, G, 0.0))
+    mate2, agg2, pv2, wn2 = oracle.pairwise(Gs, wn1)
+    H = oracle.setup(A, oracle.OParams(agg_steps=2, smooth_prolong=0, coarse_size=1, max_levels=2,
+                                       cheb_degree=2))
+    L0 = H.levels[0]
+    assert np.array_equal(L0.agg, agg2[agg1])
+    assert np.allclose(L0.ptent, pv1 * pv2[agg1], rtol=1e-14, atol=0)
+    assert H.levels[1].N == wn2.size
+
+
 @pytest.fixture(scope="module")
 def c1_hier():
     K = oracle.assemble(2, 2, 16)
@@ -235,6 +285,47 @@ def test_opc_table1c(table1, k, p):
     H = oracle.setup(K, oracle.OParams.for_degree(p))
     assert abs(H.opc() - table1[(k, p)][1]) <= 0.02, H.opc()
     assert H.levels[-1].N <= 50 and H.levels[-2].N > 50
+
+
+def _study():
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "oracle", "opc_study.json")) as f:
+        st = json.load(f)
+    with open(os.path.join(root, "oracle", "sizes_C3.json")) as f:
+        c3 = json.load(f)
+    st["k96_p3"]["canonical"] = dict(opc=c3["opc"], N=c3["N"])
+    return st
+
+
+def test_opc_tie_order_study(table1):
+    """PAPER pin of the tie-order reading (DESIGN.md c.8t) on the committed study (written by the
+    oracle-only oracle/scripts/opc_study.py; oracle/sizes_C3.json for the canonical k = 96 setup):
+    Table 1c at (24,3), (48,3), (96,3) lies between the two kinds of tie order — the
+    pseudo-random order (3 seeds) within ±0.015 of the paper (printed to 2 decimals) at every k, the
+    index orders (canonical, and preferring the larger index) at most 0.035 below it and never above
+    it by more than 0.005."""
+    st = _study()
+    for k in (24, 48, 96):
+        paper = table1[(k, 3)][1]
+        r = st[f"k{k}_p3"]
+        hashed = [v["opc"] for n, v in r.items() if n.startswith("tie_hashed")]
+        assert hashed and all(abs(h - paper) <= 0.015 for h in hashed), (k, hashed, paper)
+        assert max(hashed) - min(hashed) <= 0.002
+        for n in ("canonical", "tie_larger_index"):
+            assert paper - 0.035 <= r[n]["opc"] <= paper + 0.005, (k, n, r[n]["opc"], paper)
+        assert r["canonical"]["N"][0] == table1[(k, 3)][0]
+
+
+@pytest.mark.slow
+def test_opc_table1c_k96(table1):
+    """Table 1c at the headline size (96,3), recomputed (~5 min, ~15 GB): the pseudo-random tie order
+    reproduces the paper's 1.34 within ±0.01 (the canonical index order: `test_opc_tie_order_study`)."""
+    K = oracle.assemble(3, 3, 96)
+    H = oracle.setup(K, oracle.OParams.for_degree(3, tie_break=2))
+    assert abs(H.opc() - table1[(96, 3)][1]) <= 0.01, H.opc()
+    assert H.levels[0].N == table1[(96, 3)][0]
 
 
 def test_setup_deterministic(c1_hier):

@@ -52,8 +52,9 @@ def main():
             kerns = [0, 1, 2, 3, 4, 6]  # bit 0 TMA, bit 1 16-bit columns, bit 2 L2 prefetch, bit 3 value index
             if chosen["n_values"]:
                 kerns += [8, 10, 12, 14]
-            sellvi = chosen["layout"] == "sellvi"
-            for kern in ([0] if sellvi else kerns):
+            sellvi = chosen["layout"] in ("sellvi", "sellviw")
+            sk = [1, 2] if chosen["layout"] == "sellviw" else [0]  # windowed: windows staged per CTA
+            for kern in (sk if sellvi else kerns):
                 for G in ((32,) if sellvi else (1, 4, 8, 32)):
                     for U in ((1, 2, 4) if sellvi else (2, 4, 6, 8)):
                         if (kern & 1) and U > 4:
@@ -72,7 +73,7 @@ def main():
                         us = e0.elapsed_time(e1) * 1e3 / args.reps
                         cfg = H.op_config(l, op)
                         gbs = (cfg["alg_bytes"] + 16.0 * nr) / (us * 1e-6) / 1e9
-                        print(json.dumps(dict(level=l, op=op, kernel="sellvi" if sellvi else kind_name(kern), G=G, U=U, us=round(us, 1),
+                        print(json.dumps(dict(level=l, op=op, kernel=(chosen["layout"] + (f"_b{kern}" if kern else "")) if sellvi else kind_name(kern), G=G, U=U, us=round(us, 1),
                                               GBps=round(gbs, 1), alg_bytes=cfg["alg_bytes"])), flush=True)
             H.set_op_config(l, op, chosen["kernel_bits"], chosen["G"], chosen["U"])
             print(json.dumps(dict(level=l, op=op, autotuned=chosen)), flush=True)
