@@ -407,6 +407,7 @@ def run_gpu(args) -> None:
             "step": "one FCG iteration (every §8(a) row once); solves restarted from u0 = 0 every `iters` steps",
             "relres": relres,
             "setup_s": round(t_setup, 3),
+            "host_max_rss_gib": round(__import__("resource").getrusage(__import__("resource").RUSAGE_SELF).ru_maxrss / 2 ** 20, 2),
             "setup_phases": getattr(H, "setup_phases", None),
             "generator_s": round(t_gen, 3),
             "vcycle_GBps": round(vcyc_gbs, 1),

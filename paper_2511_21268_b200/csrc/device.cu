@@ -1520,6 +1520,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                     for (int q = 0; q < nr; q++) want[k] = std::max(want[k], all[(size_t)q * want.size() + k]);
                 size_t bytes = kVecOff;
                 auto add = [&](int64_t lo, int64_t rest) {
+                    lo = (lo + 1) & ~(int64_t)1;  // as vec() below
                     bytes += ((size_t)std::max<int64_t>(lo + rest, 1) * 8 + 255) / 256 * 256;
                 };
                 for (int l = 0; l < H.nlevels; l++)
@@ -1532,8 +1533,11 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                 D->slab_bytes = bytes;
                 D->slab_used = kVecOff;
             }
-            // a vector with `lo` ghost slots below its owned block: the returned pointer is owned[0]
+            // a vector with `lo` ghost slots below its owned block: the returned pointer is owned[0],
+            // 16-B aligned (lo rounded up to even; the capacities are maxima over ranks, so the
+            // rounding keeps the slab offsets identical on every rank)
             auto vec = [&](int64_t lo, int64_t rest) -> double * {
+                lo = (lo + 1) & ~(int64_t)1;
                 double *p;
                 if (!want_p2p) {
                     p = D->alloc_n<double>(lo + rest);

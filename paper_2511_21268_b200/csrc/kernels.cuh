@@ -1169,7 +1169,8 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
 // Block layout (host, device.cu upload_sellvi): binfo[b] = {first run, end run, window doubles, -};
 // runs[r] = {first column, doubles (even), window offset (even), -}; columns and lengths are even so
 // every copy is 16-B aligned (the vector must be 16-B aligned: single-GPU layout).  Summation order
-// is k_sellvi's (chain k & 1 per entry k of a row), so results are bitwise those of k_sellvi.
+// is k_sellvi's (chain k & 1 per entry k of a row), so results are bitwise those of k_sellvi on
+// whole (unsplit) slices.
 template <int U, class Epi, int NBUF, bool kSmem>
 __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
                                                     const int4 *__restrict__ binfo, const int4 *__restrict__ runs,

@@ -197,9 +197,12 @@ def test_sellvi_layout(windowed, monkeypatch):
 def test_sellvi_windowed_bitwise_equals_plain(monkeypatch):
     """The windowed core (x staged in shared memory, window positions in the words) sums every row in
     the plain SELL-VI order: y = A·x on every level and one V-cycle are BITWISE those of the plain
-    layout (AMG_SELLVI_WIN=0), for the bench's format 0 and for format 6."""
+    layout (AMG_SELLVI_WIN=0), for the bench's format 0 and for format 6.  (The plain layout's tail
+    split — on at C2's few slices per warp — sums a row's parts separately, so it is switched off:
+    AMG_SELLVI_PARTS=0; the split against the unsplit sum is test_sellvi_split_slices.)"""
     amg = _amg()
     dim, p, n = CASES["C2"]
+    monkeypatch.setenv("AMG_SELLVI_PARTS", "0")
     for fmt in (0, 6):
         Hs = {}
         for wnd in (0, 1):

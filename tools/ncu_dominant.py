@@ -18,6 +18,10 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/TEX throughput %"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 LSU data-pipe wavefronts %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "of which shared memory %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "shared-load bank conflicts"),
+    ("lts__t_bytes.sum", "L2 bytes"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
@@ -33,6 +37,9 @@ def kernel_key(name: str) -> str:
     m = re.search(r"(k_csr2|k_csr4t)<(\d+), (\d+), [^,]+?(?:<[^>]*>)?, (Cols\w+)>", name)
     if m:
         return f"{m.group(1)}<{m.group(2)},{m.group(3)},{m.group(4)}>"
+    m = re.search(r"k_sellviw<(\d+), [\w:]+(?:<[^>]*>)?, (\d+), ", name)  # windowed: 'k_sellviw<U,NBUF>'
+    if m:
+        return f"k_sellviw<{m.group(1)},{m.group(2)}>"
     m = re.search(r"k_sellvi<(\d+), ", name)  # 'void k_sellvi<2, EpiCheb<0>>(...)' -> 'k_sellvi<2>'
     return f"k_sellvi<{m.group(1)}>" if m else name
 
