@@ -18,6 +18,7 @@ import sys
 from collections import defaultdict
 
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+        "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "KB": 1e3, "MB": 1e6, "GB": 1e9, "B": 1.0,
         "second": 1.0, "%": 1.0, "": 1.0, "register/thread": 1.0}
 
 
