@@ -452,8 +452,9 @@ def run_gpu(args) -> None:
 # stands (assembly, setup and solve all by oracle/), single-threaded, iterations timed one by one
 # ------------------------------------------------------------------------------------------------
 # workloads whose oracle setup fits the bench's budget (the C3 oracle setup takes ~4-5 min on one
-# core); the larger ones (C4, C5, R4, L3) run their oracle leg only with --cpu-baseline-force
-ORACLE_DEFAULT = ("C1", "C2", "C3", "R3")
+# core); the others (C4, C5, R3, R4, L3: larger, or assembled from decimal tables) run their oracle leg only
+# with --cpu-baseline-force
+ORACLE_DEFAULT = ("C1", "C2", "C3")
 
 
 def oracle_start(cfg: str, problem: str, warmup: int, steps: int, force: bool = False):
