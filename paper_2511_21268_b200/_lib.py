@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libamg_b200.so")
+# AMG_LIB=checked loads the checked build (device-side invariant checks, build.py --checked)
+LIB_PATH = os.path.join(HERE, "libamg_b200_checked.so" if os.environ.get("AMG_LIB") == "checked" else "libamg_b200.so")
 
 AMG_OK, AMG_NOT_CONVERGED = 0, 1
 STATUS = {0: "AMG_OK", 1: "AMG_NOT_CONVERGED", -1: "AMG_EINVAL", -2: "AMG_ENOMEM", -3: "AMG_ECUDA",

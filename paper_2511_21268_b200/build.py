@@ -1,6 +1,6 @@
 """In-tree build of libamg_b200.so (host setup in C++/OpenMP, solve kernels in CUDA for sm_100a).
 
-    python -m paper_2511_21268_b200.build [--force] [--verbose]
+    python -m paper_2511_21268_b200.build [--force] [--verbose] [--checked]
 
 Host files are compiled with -ffp-contract=off (the canonical arithmetic contract of DESIGN.md §3:
 no FMA contraction in the generator or the setup).  Device code is compiled for sm_100a only.
@@ -18,6 +18,9 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libamg_b200.so")
+# checked build: device-side invariant checks (AMG_CHECKS in kernels.cuh), loaded with AMG_LIB=checked
+BUILD_CHECKED = os.path.join(HERE, "_build_checked")
+LIB_CHECKED = os.path.join(HERE, "libamg_b200_checked.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
@@ -46,36 +49,37 @@ def _run(cmd: list[str], verbose: bool) -> None:
         print(r.stdout + r.stderr)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    build_dir, lib_out = (BUILD_CHECKED, LIB_CHECKED) if checked else (BUILD, LIB)
+    os.makedirs(build_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "amg_b200.h")]
     jobs, objs = [], []
     for src in HOST_SRCS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
             jobs.append(["g++", "-O2", "-std=gnu++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
                          "-Wall", "-Wno-unknown-pragmas", "-I", INCLUDE, "-c", s, "-o", o])
     for src in CUDA_SRCS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
             jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                         *(["-DAMG_CHECKS"] if checked else []),
                          "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off", "-I", INCLUDE, "-c", s, "-o", o])
     # the translation units are independent: compile them in parallel
     with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         for f in [ex.submit(_run, j, verbose) for j in jobs]:
             f.result()
-    if force or _newer(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    if force or _newer(lib_out, objs):
+        tmp = lib_out + f".tmp{os.getpid()}"
         _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-Xlinker", "--no-undefined",
               "-lgomp", "-lquadmath", "-lnccl", "-lcudart"], verbose)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, checked="--checked" in sys.argv))

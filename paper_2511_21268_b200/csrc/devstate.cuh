@@ -258,7 +258,7 @@ inline dev::DotCtx dotctx(DevState &D, int dotkind) {
 // push descriptor of `buf` (a vector in the own slab) along operator A's push plan
 inline dev::Push push_of(const DevState &D, const DCsr &A, const double *buf) {
     if (!D.p2p || !A.push_ptr || !buf) return dev::Push{};
-    return dev::Push{A.push_ptr, A.push_dst, D.d_base, (long long)((const char *)buf - D.slab)};
+    return dev::Push{A.push_ptr, A.push_dst, D.d_base, (long long)((const char *)buf - D.slab), D.nranks};
 }
 
 // y-side epilogue applied to A·g for a CSR-layout (autotuned kernel / column source) or SELL2 operator.

@@ -20,6 +20,24 @@ namespace dev {
 
 constexpr int kBlock = 256;
 
+// Checked build (AMG_CHECKS; libamg_b200_checked.so, `python -m paper_2511_21268_b200.build --checked`):
+// device-side invariants of the index structures — window positions and copies, value indices, split
+// parts and their tickets, ghost-push destinations — print the failing condition and trap.  The
+// product build compiles them out.  (compute-sanitizer is not available on the B200 pool: these
+// checks and the oracle comparisons stand in for it.)
+#ifdef AMG_CHECKS
+#define AMG_DCHECK(c)                                                                                    \
+    do {                                                                                                 \
+        if (!(c)) {                                                                                      \
+            printf("AMG_CHECKS: %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, (int)blockIdx.x, \
+                   (int)threadIdx.x);                                                                    \
+            __trap();                                                                                    \
+        }                                                                                                \
+    } while (0)
+#else
+#define AMG_DCHECK(c) ((void)0)
+#endif
+
 // Device scalar block.  Reductions only deposit sums (per rank; the multi-GPU path all-reduces the
 // slot right after the kernel); consumers derive α = ρ/pᵀq and β = ρ/ρ_prev themselves, so the
 // same kernels serve 1 and N GPUs.  The host reads the whole block once per iteration.
@@ -193,11 +211,14 @@ struct Push {
     const int2 *dst;
     char *const *base;
     long long voff;
+    int nranks = 0;  // checked build: destination ranks are < nranks
     __device__ __forceinline__ void put(int64_t i, double v) const {
         if (!ptr) return;
         const int b = ptr[i], e = ptr[i + 1];
+        AMG_DCHECK(b <= e);
         for (int t = b; t < e; t++) {
             const int2 d = dst[t];
+            AMG_DCHECK(d.x >= 0 && (nranks == 0 || d.x < nranks));
             *reinterpret_cast<double *>(base[d.x] + voff + 8ll * d.y) = v;
         }
     }
@@ -1092,7 +1113,10 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> obits);
+                for (int j = 0; j < 4; j++) {
+                    AMG_DCHECK((int)(quad_at(wa[u], j) >> obits) < nvals);
+                    va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> obits);
+                }
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
@@ -1126,11 +1150,16 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
         // split slice: deposit this part's two chains; the warp completing the slice's last part sums
         // the parts' chains in part order (fixed, whichever warp arrives last) and runs the epilogue
         const int64_t npad = nslices << 5;
+        AMG_DCHECK(part >= 0 && part < parts && q0 + W4 <= W4s);
         __stcg(partial + (int64_t)part * npad + row, make_double2(s0, s1));
         __threadfence();
         __syncwarp();
         unsigned last = 0;
-        if (lane == 0) last = atomicAdd(sticket + sl, 1u) == (unsigned)(parts - 1);
+        if (lane == 0) {
+            const unsigned tk = atomicAdd(sticket + sl, 1u);
+            AMG_DCHECK(tk < (unsigned)parts);  // a ticket left over from an earlier launch would show here
+            last = tk == (unsigned)(parts - 1);
+        }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) continue;
         __threadfence();
@@ -1202,8 +1231,11 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
         const int4 bi = __ldg(binfo + b);
         if (lane == 0) mbar_arrive_expect_tx(&bar[buf], (uint32_t)bi.z * 8u);
         __syncwarp();
+        AMG_DCHECK(bi.x <= bi.y && bi.z >= 0 && bi.z <= wmax);
         for (int r = bi.x + lane; r < bi.y; r += 32) {
             const int4 ru = __ldg(runs + r);
+            AMG_DCHECK(ru.y > 0 && (ru.x & 1) == 0 && (ru.y & 1) == 0 && (ru.z & 1) == 0 && ru.z + ru.y <= bi.z &&
+                       ru.x >= 0 && (int64_t)ru.x + ru.y <= nrows + 1);
             bulk_g2s(xw + (int64_t)buf * wmax + ru.z, g + ru.x, (uint32_t)ru.y * 8u, &bar[buf], keep_policy());
         }
     };
@@ -1220,6 +1252,9 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
         mbar_wait(&bar[buf], (uint32_t)((it / NBUF) & 1));
         if (sl < nslices) {
             const double *xb = xw + (int64_t)buf * wmax;
+#ifdef AMG_CHECKS
+            const int wlen = __ldg(binfo + blk).z;  // the staged window of this block
+#endif
             const int64_t off = __ldg(soff + sl);
             const int W4 = (int)(__ldg(soff + sl + 1) - off);
             const uint4 *wp = w + (off << 5) + lane;
@@ -1240,7 +1275,10 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
 #pragma unroll
                 for (int u = 0; u < U; u++)
 #pragma unroll
-                    for (int j = 0; j < 4; j++) va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> pbits);
+                    for (int j = 0; j < 4; j++) {
+                        AMG_DCHECK((int)(quad_at(wa[u], j) >> pbits) < nvals && (int)(quad_at(wa[u], j) & pmask) < wlen);
+                        va[4 * u + j] = tab_at<kSmem>(table, quad_at(wa[u], j) >> pbits);
+                    }
 #pragma unroll
                 for (int u = 0; u < U; u++)
 #pragma unroll
@@ -1259,7 +1297,10 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
                 const uint4 wq = ld_stream(wp + (int64_t)q * 32, pol);
                 double va[4], xa[4];
 #pragma unroll
-                for (int j = 0; j < 4; j++) va[j] = tab_at<kSmem>(table, quad_at(wq, j) >> pbits);
+                for (int j = 0; j < 4; j++) {
+                    AMG_DCHECK((int)(quad_at(wq, j) >> pbits) < nvals && (int)(quad_at(wq, j) & pmask) < wlen);
+                    va[j] = tab_at<kSmem>(table, quad_at(wq, j) >> pbits);
+                }
 #pragma unroll
                 for (int j = 0; j < 4; j++) xa[j] = xb[quad_at(wq, j) & pmask];
                 s0 = fma(va[0], xa[0], s0);

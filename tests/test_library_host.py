@@ -26,6 +26,12 @@ def test_library_exports_every_header_symbol():
     for name in sorted(declared):
         assert hasattr(L, name), name
     assert declared == set(_lib.EXPORTED)
+    # the checked build (device-side invariant checks, tests/test_gpu_checked.py) exports the same ABI
+    chk = os.path.join(ROOT, "paper_2511_21268_b200", "libamg_b200_checked.so")
+    if os.path.exists(chk):
+        Lc = C.CDLL(chk)
+        for name in sorted(declared):
+            assert hasattr(Lc, name), name
 
 
 def test_errors_are_reported_not_raised_through_abi():
