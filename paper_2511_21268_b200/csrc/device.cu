@@ -366,13 +366,15 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     }
     // Windowed variant (k_sellviw): blocks of kWinSlices consecutive slices; the union of a block's
     // columns as runs of even length starting at even columns (gaps of <= kWinGap columns are staged
-    // rather than split), each entry's word = its column's position in the block's window.  Single-GPU
-    // layout only (the staged vector must be 16-B aligned at column 0; the distributed vectors carry
-    // ghost slots before the owned block).  AMG_SELLVI_WIN=0 keeps the plain SELL-VI words.
-    bool win = D.nranks <= 1 && A.ncols == n;
+    // rather than split), each entry's word = its column's position in the block's window.  Every
+    // vector it may gather is 16-B aligned at column 0 (the lower ghost areas of the distributed
+    // vectors have even length).  AMG_SELLVI_WIN=0 keeps the plain SELL-VI words.
+    bool win = true;
     if (const char *e = std::getenv("AMG_SELLVI_WIN"))
         if (std::atoi(e) == 0) win = false;
     const int64_t nblk = (nsl + kWinSlices - 1) / kWinSlices;
+    int64_t win_max = kWinMax;  // AMG_WIN_MAX: experiments with wider windows (fewer CTAs per SM)
+    if (const char *e = std::getenv("AMG_WIN_MAX")) win_max = std::max<int64_t>(256, std::min<int64_t>(20000, std::atoll(e)));
     std::vector<std::vector<int4>> bruns;
     int64_t wmax = 0;
     if (win) {
@@ -406,7 +408,7 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
                 k = j;
             }
             wmax = std::max<int64_t>(wmax, tot);
-            ok = ok && tot <= kWinMax;
+            ok = ok && tot <= win_max;
         }
         if (!ok || wmax == 0) win = false;
     }
@@ -445,6 +447,27 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
         }
         out.win = true;
         out.pbits = pbits;
+        if (8 * ((tab.size() <= (size_t)kSellviSmemVals ? ((int64_t)tab.size() + 1) & ~1 : 0) + 2 * ((wmax + 1) & ~1)) > 227 * 1024)
+            out.nbuf = 1;
+        // tail split of the last round (k_sellviw): against the nominal 3 CTAs per SM (U = 4, one
+        // window: the usual choice), the leftover blocks are split in 2 or 4 items so the last round
+        // is short; AMG_SELLVIW_SPLIT=k forces 2^k items for every block (tests), 0 disables
+        {
+            // only where the tail is a large share (<= 4 full rounds: the multi-GPU shares); at C3 on one
+            // GPU (8 rounds) the split items' duplicated window copies and idle warps cost more than the
+            // shorter tail saves (228 vs 221 µs, run r2i)
+            const int64_t cnom = 3 * (int64_t)D.nsm, tail = nblk % cnom;
+            const bool few = nblk / cnom <= 4;
+            int wl = 0;
+            while (few && tail > 0 && wl < 2 && (tail << (wl + 1)) <= cnom) wl++;
+            int64_t wwhole = nblk - tail;
+            if (const char *e = std::getenv("AMG_SELLVIW_SPLIT")) {
+                wl = std::max(0, std::min(3, std::atoi(e)));
+                wwhole = 0;
+            }
+            out.wl = wl;
+            out.wwhole = wl ? wwhole : nblk;
+        }
         out.wmax = (int)((wmax + 1) & ~1);
         out.nruns = (int64_t)runs.size();
         out.binfo = D.alloc_n<int4>(nblk);
@@ -736,6 +759,9 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
         int bu = A.U, bb = A.nbuf;
         for (int nb : {2, 1}) {
             if (nb == 1 && !A.win) continue;
+            // two windows must fit the 227 KB of shared memory a CTA may have (next to the table)
+            const int64_t tabn = A.nvals <= kSellviSmemVals ? (A.nvals + 1) & ~1 : 0;
+            if (nb == 2 && A.win && 8 * (tabn + 2 * (int64_t)A.wmax) > 227 * 1024) continue;
             for (int U : {1, 2, 4}) {
                 A.U = U;
                 A.nbuf = nb;
@@ -1209,7 +1235,7 @@ void build_gorder(DevState &D, DCsr &A) {
     if (A.bnd.empty() || (A.fmt != 0 && A.fmt != 2)) return;
     if (const char *e = std::getenv("AMG_P2P_INTERIOR"))  // 0: every kernel waits at its start (debug)
         if (std::atoi(e) == 0) return;
-    const int64_t G = A.G, ng = (A.nrows + G - 1) / G;
+    const int64_t G = order_granule(A), ng = (A.nrows + G - 1) / G;
     std::vector<int> order, tail;
     order.reserve(ng);
     for (int64_t g = 0; g < ng; g++) {
@@ -1602,6 +1628,7 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                     big = std::max(big, std::max(A->nrows, A->ncols));
                     if (A->halo) lomax = std::max(lomax, -A->lo_base);
                 }
+            lomax = (lomax + 1) & ~(int64_t)1;  // keep sx 16-B aligned (the windowed SELL-VI copies)
             double *scr = nullptr;  // x (with room for negative ghost columns), y1, y2, y3 scratch vectors
             CUDA_OK(cudaMalloc(&scr, sizeof(double) * (big * 4 + lomax)));
             // non-trivial data (not zeros): data-dependent power draw changes the clocks under the cap
@@ -2068,6 +2095,9 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
         if ((A.win ? !(kernel == 1 || kernel == 2) : kernel != 0) || G != 32 || !(U == 1 || U == 2 || U == 4))
             throw Error{AMG_EINVAL, "SELL-VI operator: kernel 0 (windowed: 1 or 2), G 32 and U 1, 2 or 4"};
         CUDA_OK(cudaDeviceSynchronize());
+        if (A.win && kernel == 2 &&
+            8 * ((A.nvals <= kSellviSmemVals ? (A.nvals + 1) & ~1 : 0) + 2 * (int64_t)A.wmax) > 227 * 1024)
+            throw Error{AMG_EINVAL, "windowed SELL-VI: two windows exceed the shared memory of a CTA"};
         A.U = U;
         if (A.win) A.nbuf = kernel;
         A.tuned_us = 0.f;

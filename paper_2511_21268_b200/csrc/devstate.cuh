@@ -86,6 +86,8 @@ struct DCsr {
     int4 *binfo = nullptr;
     int4 *wruns = nullptr;
     int nbuf = 2;  // windows staged per CTA: 2 (double-buffered) or 1 (autotuned with U)
+    int64_t wwhole = 0;  // blocks processed whole; the later ones are split into 2^wl items (k_sellviw)
+    int wl = 0;
     // SELL-VI: the slices of the last (partial) round — slice positions >= nwhole — are split into
     // 2^lparts parts of consecutive quads, one warp each, so the tail round is short; partial = the
     // parts' two chains per row, sticket = per-slice arrival counters (zero between launches)
@@ -241,9 +243,12 @@ inline dev::P2P p2p_of(const DevState &D, bool part, unsigned mask = ~0u) {
 inline dev::P2P p2p_of(const DevState &D, const DCsr &A) { return p2p_of(D, A.part, A.wmask); }
 // The CSR cores on A: with A's boundary-first group order (mid-kernel publication).  ONLY for kernels
 // that implement the group order — a plain kernel handed a group order would never publish.
+// rows per unit of the boundary-first order: the row group (CSR), the slice (SELL-VI), the 8-slice
+// block of the windowed SELL-VI core
+inline int64_t order_granule(const DCsr &A) { return A.fmt == 2 && A.win ? 32 * kWinSlices : A.G; }
 inline dev::P2P p2p_csr(const DevState &D, const DCsr &A) {
     dev::P2P p = p2p_of(D, A.part, A.wmask);
-    if (p.nranks > 0 && (A.fmt == 0 || A.fmt == 2) && A.gorder && A.gorder_G == A.G) {
+    if (p.nranks > 0 && (A.fmt == 0 || A.fmt == 2) && A.gorder && A.gorder_G == order_granule(A)) {
         p.gorder = A.gorder;
         p.nbnd = A.nbnd;
     }

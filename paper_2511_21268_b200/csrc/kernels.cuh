@@ -185,6 +185,27 @@ __device__ __forceinline__ void peer_signal_warp(const P2P &pp) {
     __syncwarp();
 }
 
+// Early publication of the windowed SELL-VI core (block-granular boundary-first order): each CTA checks
+// in once, after the barrier that ended its last boundary item (every thread's pushes issued); the
+// last CTA of the grid publishes the new count.  Counts CTAs on the same bticket as the warp version.
+__device__ __forceinline__ void peer_signal_cta(const P2P &pp) {
+    if (pp.nranks == 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned t = atomicAdd(pp.bticket, 1u);
+        if (t == gridDim.x - 1) {
+            __threadfence_system();
+            const unsigned long long e = *(volatile unsigned long long *)pp.epoch + 1ull;
+            *(volatile unsigned long long *)pp.epoch = e;
+            *(volatile unsigned *)pp.bticket = 0u;
+            for (int q = 0; q < pp.nranks; q++)
+                st_release_sys(reinterpret_cast<unsigned long long *>(pp.base[q] + pp.flags_off) + pp.rank, e);
+        }
+    }
+    __syncthreads();
+}
+
 // Kernel epilogue (every CTA, after all its stores): the last CTA to finish publishes the new count.
 __device__ __forceinline__ void peer_signal(const P2P &pp) {
     if (pp.nranks == 0 || pp.gorder) return;  // boundary-first kernels published early
@@ -1200,11 +1221,16 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
 // every copy is 16-B aligned (the vector must be 16-B aligned: single-GPU layout).  Summation order
 // is k_sellvi's (chain k & 1 per entry k of a row), so results are bitwise those of k_sellvi on
 // whole (unsplit) slices.
+// Tail: the blocks of the last round (positions >= nwhole, counted against the nominal 3·n_SM CTAs so
+// the choice depends on the operator alone) are split into 2^wl work items of 8 >> wl consecutive
+// slices each; the item's CTA stages the block's whole window and its first 8 >> wl warps take one
+// slice each.  Slices stay whole, so the split changes timing, never results.
 template <int U, class Epi, int NBUF, bool kSmem>
 __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ soff, const uint4 *__restrict__ w,
                                                     const int4 *__restrict__ binfo, const int4 *__restrict__ runs,
                                                     const double *__restrict__ gtable, int nvals, int pbits, int wmax,
-                                                    const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc) {
+                                                    const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc,
+                                                    int64_t nwhole, int wl, P2P pp) {
     constexpr int WPB = kBlock / 32;  // warps per CTA = slices per block
     extern __shared__ __align__(16) double wsm[];
     __shared__ __align__(8) uint64_t bar[NBUF];
@@ -1225,31 +1251,59 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
     }
     __syncthreads();
     const double *table = kSmem ? tab : gtable;
-    // warp 0 stages block `b` into buffer `buf`: lane 0 arms the barrier with the window's bytes, then
-    // the lanes issue one bulk copy per run
-    auto stage = [&](int64_t b, int buf) {
-        const int4 bi = __ldg(binfo + b);
+    // P2P (multi-GPU shares): without a block order every CTA waits for the neighbours at its start
+    // and the kernel publishes at its end; with one (pp.gorder: the block positions of BOUNDARY blocks
+    // — a row reads a ghost value or pushes one — first, pp.nbnd of them) warp 0 waits only before
+    // staging a boundary block's window, and each CTA checks in once it is past its boundary items;
+    // the last CTA to check in publishes the new count while the interior items still run
+    if (!pp.gorder) peer_wait(pp);
+    bool signalled = pp.gorder == nullptr || pp.nranks == 0;
+    const int64_t nbnd_pos = pp.gorder ? pp.nbnd : 0;  // boundary block POSITIONS
+    auto blk_at = [&](int64_t pos) { return pp.gorder ? (int64_t)__ldg(pp.gorder + pos) : pos; };
+    bool waited = signalled, cwaited = signalled;
+    // warp 0 stages the block at position `pos` into buffer `buf`: lane 0 arms the barrier with the
+    // window's bytes, then the lanes issue one bulk copy per run
+    auto stage = [&](int64_t pos, int buf) {
+        if (!waited && pos < nbnd_pos) {  // ghost values are read by the copies below
+            peer_wait_warp(pp);
+            waited = true;
+        }
+        const int4 bi = __ldg(binfo + blk_at(pos));
         if (lane == 0) mbar_arrive_expect_tx(&bar[buf], (uint32_t)bi.z * 8u);
         __syncwarp();
         AMG_DCHECK(bi.x <= bi.y && bi.z >= 0 && bi.z <= wmax);
         for (int r = bi.x + lane; r < bi.y; r += 32) {
             const int4 ru = __ldg(runs + r);
-            AMG_DCHECK(ru.y > 0 && (ru.x & 1) == 0 && (ru.y & 1) == 0 && (ru.z & 1) == 0 && ru.z + ru.y <= bi.z &&
-                       ru.x >= 0 && (int64_t)ru.x + ru.y <= nrows + 1);
+            AMG_DCHECK(ru.y > 0 && (ru.x & 1) == 0 && (ru.y & 1) == 0 && (ru.z & 1) == 0 && ru.z + ru.y <= bi.z);
             bulk_g2s(xw + (int64_t)buf * wmax + ru.z, g + ru.x, (uint32_t)ru.y * 8u, &bar[buf], keep_policy());
         }
     };
     typename Epi::Acc dacc{};
-    int64_t blk = blockIdx.x;
-    if (wib == 0 && blk < nblk) stage(blk, 0);
-    for (int it = 0; blk < nblk; blk += gridDim.x, it++) {
+    const int64_t nitems = nwhole + ((nblk - nwhole) << wl);
+    auto block_of = [&](int64_t item) { return item < nwhole ? item : nwhole + ((item - nwhole) >> wl); };
+    int64_t item = blockIdx.x;
+    if (wib == 0 && item < nitems) stage(block_of(item), 0);
+    const int64_t nbnd_items = nbnd_pos <= nwhole ? nbnd_pos : nwhole + ((nbnd_pos - nwhole) << wl);
+    for (int it = 0; item < nitems; item += gridDim.x, it++) {
+        if (!signalled && item >= nbnd_items) {  // past this CTA's boundary items (all their pushes issued)
+            peer_signal_cta(pp);
+            signalled = true;
+        }
         const int buf = NBUF == 2 ? (it & 1) : 0;
-        if (NBUF == 2 && wib == 0 && blk + gridDim.x < nblk) stage(blk + gridDim.x, buf ^ 1);
-        const int64_t sl = blk * WPB + wib;
+        if (NBUF == 2 && wib == 0 && item + gridDim.x < nitems) stage(block_of(item + gridDim.x), buf ^ 1);
+        const int64_t blk = blk_at(block_of(item));
+        // this item's slices: the whole block, or part (item − nwhole) mod 2^wl of WPB >> wl slices
+        const int per = item < nwhole ? WPB : WPB >> wl;
+        const int first = item < nwhole ? 0 : (int)((item - nwhole) & ((1 << wl) - 1)) * per;
+        const int64_t sl = wib < per ? blk * WPB + first + wib : nslices;  // warps beyond `per` idle
         const int64_t row = (sl << 5) + lane;
         typename Epi::Pre pre{};
         if (sl < nslices && row < nrows) pre = epi.load(row);  // epilogue inputs in flight with the stream
         mbar_wait(&bar[buf], (uint32_t)((it / NBUF) & 1));
+        if (!cwaited && item < nbnd_items) {  // every warp acquires the neighbours' flags itself before
+            peer_wait_warp(pp);               // its first boundary item (its pushes overwrite ghost slots)
+            cwaited = true;
+        }
         if (sl < nslices) {
             const double *xb = xw + (int64_t)buf * wmax;
 #ifdef AMG_CHECKS
@@ -1311,12 +1365,14 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
             if (row < nrows) acc_add(dacc, epi(row, s0 + s1, pre));
         }
         __syncthreads();  // every warp is done with `buf`: it may be refilled
-        if (NBUF == 1 && wib == 0 && blk + gridDim.x < nblk) {
+        if (NBUF == 1 && wib == 0 && item + gridDim.x < nitems) {
             fence_proxy_async();
-            stage(blk + gridDim.x, 0);
+            stage(block_of(item + gridDim.x), 0);
         }
     }
+    if (!signalled) peer_signal_cta(pp);
     if constexpr (Epi::kDot) block_dot_finalize(dacc, dc);
+    peer_signal(pp);
 }
 
 // Non-template kernels are defined in device.cu only (AMGB_PLAIN_KERNELS); the inst_*.cu units see

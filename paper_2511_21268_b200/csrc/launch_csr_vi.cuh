@@ -24,10 +24,12 @@ void launch_sellviw(DevState &D, const DCsr &A, const double *g, Epi epi, cudaSt
     const int tabn = kSmem ? (int)((A.nvals + 1) & ~1) : 0;
     const int smem = 8 * (tabn + NBUF * A.wmax);
     const int per_sm = resident_ctas((const void *)dev::k_sellviw<U, Epi, NBUF, kSmem>, dev::kBlock, smem, smem);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)per_sm * D.nsm));
+    const int64_t nitems = A.wwhole + ((nblk - A.wwhole) << A.wl);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nitems, (int64_t)per_sm * D.nsm));
     dev::k_sellviw<U, Epi, NBUF, kSmem><<<grid, dev::kBlock, smem, st>>>(
         A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.binfo, A.wruns, A.vtab, (int)A.nvals, A.pbits, A.wmax, g,
-        A.nrows, epi, dotctx(D, dotkind));
+        A.nrows, epi, dotctx(D, dotkind), A.wwhole, A.wl,
+        (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
 }
 
 template <int U, class Epi, bool kSmem>

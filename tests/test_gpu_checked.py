@@ -58,7 +58,8 @@ def _need():
         pytest.fail("checked build missing: python -m paper_2511_21268_b200.build --checked")
 
 
-@pytest.mark.parametrize("variant", [{}, {"AMG_SELLVI_WIN": "0", "AMG_SELLVI_PARTS": "2"}, {"AMG_SELLVI_WIN": "0"}])
+@pytest.mark.parametrize("variant", [{}, {"AMG_SELLVIW_SPLIT": "2"}, {"AMG_SELLVI_WIN": "0", "AMG_SELLVI_PARTS": "2"},
+                                     {"AMG_SELLVI_WIN": "0"}])
 def test_checked_build_matches_product(variant):
     chk = _run(dict(variant, AMG_LIB="checked"))
     prod = _run(dict(variant))
@@ -71,5 +72,5 @@ def test_checked_build_matches_product(variant):
         for f in ("u", "z"):
             a, b = np.array(c[f]), np.array(p[f])
             assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max(), (key, f)
-    if not variant:
+    if variant.get("AMG_SELLVI_WIN") != "0":
         assert chk["C2_6"]["l0"] == "sellviw"  # the windowed core ran with its checks armed

@@ -26,8 +26,9 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg", fmt=0):
+def _worker(rank, world, port, case, rep_nnz, transport, q, solver="pcg", fmt=0, env=None):
     try:
+        os.environ.update(env or {})
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         os.environ["AMG_REPLICATE_NNZ"] = str(rep_nnz)
@@ -155,6 +156,35 @@ def test_distributed_sellvi(transport):
         assert np.linalg.norm(u8 - u1_8) <= 1e-10 * np.linalg.norm(u1_8)
 
 
+def test_distributed_checked_build():
+    """The checked build (device-side invariant checks: window copies and positions, value indices,
+    split tickets, ghost-push destination ranks) on the P2P path at 2 GPUs, the windowed level-0 layout
+    with every block split into items (AMG_SELLVIW_SPLIT=1): the distributed solve matches the 1-GPU
+    one and no check fires."""
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    env = {"AMG_LIB": "checked", "AMG_SELLVIW_SPLIT": "1"}
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (3, 2, 32), 200000, "p2p", q, "pcg", 0, env))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, out, ref, N = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert status == "ok", out
+    zv = np.zeros(N)
+    for b, e, zl in out["vcycle"]:
+        zv[b:e] = zl
+    assert np.abs(zv - ref["vcycle"]).max() <= 1e-12 * np.abs(ref["vcycle"]).max()
+    for name in ("sine", "random"):
+        it, st, hist, parts = out[name]
+        assert st == 0 and abs(it - ref[name][0]) <= 1
+
+
 @pytest.mark.parametrize("case", [(3, 3, 12), (3, 3, 8, 2)])
 @pytest.mark.parametrize("transport", ["p2p", "nccl"])
 def test_distributed_paper_experiment(transport, case):
@@ -192,16 +222,22 @@ def test_distributed_paper_experiment(transport, case):
         assert np.linalg.norm(u8 - u1_8) <= 1e-6 * np.linalg.norm(u1_8), name
 
 
-def _stress_worker(rank, world, port, lparts, reps, q):
-    """P2P transport with every SELL-VI slice split into 2^lparts quad ranges (AMG_SELLVI_PARTS): the
-    boundary items of split slices are where the round-1 race lived.  `reps` V-cycles and solves on
-    each rank must be bitwise identical run to run; rank 0 also runs the same forced split on 1 GPU."""
+def _stress_worker(rank, world, port, mode, lparts, reps, q):
+    """P2P transport with every SELL-VI slice split into 2^lparts quad ranges (mode "plain":
+    AMG_SELLVI_PARTS, the plain layout) or every windowed block split into 2^lparts items (mode
+    "windowed": AMG_SELLVIW_SPLIT): the boundary items of split work are where the round-1 race
+    lived.  `reps` V-cycles and solves on each rank must be bitwise identical run to run; rank 0 also
+    runs the same forced split on 1 GPU."""
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         os.environ["AMG_REPLICATE_NNZ"] = "200000"
         os.environ["AMG_TRANSPORT"] = "p2p"
-        os.environ["AMG_SELLVI_PARTS"] = str(lparts)
+        if mode == "plain":
+            os.environ["AMG_SELLVI_WIN"] = "0"
+            os.environ["AMG_SELLVI_PARTS"] = str(lparts)
+        else:
+            os.environ["AMG_SELLVIW_SPLIT"] = str(lparts)
         torch.cuda.set_device(rank)
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
         import paper_2511_21268_b200 as amg
@@ -209,7 +245,10 @@ def _stress_worker(rank, world, port, lparts, reps, q):
         K, F = amg.iga_poisson(3, 2, 32)
         prm = amg.params(2, format=6)
         H = amg.Hierarchy(K, prm, dist=amg.make_dist(rank, world, device=rank))
-        assert H.op_config(0, 0)["sellvi_parts"] == 1 << lparts
+        if mode == "plain":
+            assert H.op_config(0, 0)["sellvi_parts"] == 1 << lparts
+        else:
+            assert H.op_config(0, 0)["layout"] == "sellviw"
         b, e = H.local_rows()
         rv = torch.from_numpy(np.ascontiguousarray(amg_inputs.uniform_pm1(K.shape[0], seed=23)[b:e])).cuda()
         Fl = torch.from_numpy(np.ascontiguousarray(F[b:e])).cuda()
@@ -236,19 +275,20 @@ def _stress_worker(rank, world, port, lparts, reps, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("lparts", [1, 2])
+@pytest.mark.parametrize("mode,lparts", [("plain", 1), ("plain", 2), ("windowed", 1), ("windowed", 3)])
 @pytest.mark.parametrize("world", [2, 4])
-def test_p2p_split_slices_stress(world, lparts):
-    """Regression/stress for the P2P ghost protocol with split SELL-VI slices: forced
-    splits on every slice (not only where 24·n_SM warps happen to leave a tail), 4 repeats per rank,
-    bitwise run-to-run identical, and equal to the 1-GPU solve with the same split (V-cycle 1e-12, the
-    6-iteration PCG iterate 1e-10)."""
+def test_p2p_split_slices_stress(world, mode, lparts):
+    """Regression/stress for the P2P ghost protocol with split work items: forced splits
+    on every slice of the plain layout, or on every block of the windowed one (its block-granular
+    boundary-first order and per-CTA early publication), 4 repeats per rank, bitwise run-to-run
+    identical, and equal to the 1-GPU solve with the same split (V-cycle 1e-12, the 6-iteration PCG
+    iterate 1e-10)."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_stress_worker, args=(r, world, port, lparts, 4, q)) for r in range(world)]
+    procs = [ctx.Process(target=_stress_worker, args=(r, world, port, mode, lparts, 4, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     status, parts, z1, u1 = q.get(timeout=300)

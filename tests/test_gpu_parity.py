@@ -197,18 +197,22 @@ def test_sellvi_layout(windowed, monkeypatch):
 def test_sellvi_windowed_bitwise_equals_plain(monkeypatch):
     """The windowed core (x staged in shared memory, window positions in the words) sums every row in
     the plain SELL-VI order: y = A·x on every level and one V-cycle are BITWISE those of the plain
-    layout (AMG_SELLVI_WIN=0), for the bench's format 0 and for format 6.  (The plain layout's tail
+    layout (AMG_SELLVI_WIN=0), for the bench's format 0 and for format 6, also with the windowed tail
+    items forced to single slices (AMG_SELLVIW_SPLIT=3: slices stay whole).  (The plain layout's tail
     split — on at C2's few slices per warp — sums a row's parts separately, so it is switched off:
     AMG_SELLVI_PARTS=0; the split against the unsplit sum is test_sellvi_split_slices.)"""
     amg = _amg()
     dim, p, n = CASES["C2"]
     monkeypatch.setenv("AMG_SELLVI_PARTS", "0")
-    for fmt in (0, 6):
+    for fmt, split in ((0, None), (6, None), (0, "3")):
         Hs = {}
         for wnd in (0, 1):
             monkeypatch.setenv("AMG_SELLVI_WIN", str(wnd))
+            if split is not None and wnd == 1:  # windowed tail items of 1 slice for every block
+                monkeypatch.setenv("AMG_SELLVIW_SPLIT", split)
             K, F = amg.iga_poisson(dim, p, n)
             Hs[wnd] = amg.Hierarchy(K, amg.params(p, format=fmt))
+            monkeypatch.delenv("AMG_SELLVIW_SPLIT", raising=False)
         assert Hs[1].op_config(0, 0)["layout"] == "sellviw" and Hs[0].op_config(0, 0)["layout"] == "sellvi"
         info = Hs[0].info()
         rng = np.random.default_rng(31)
