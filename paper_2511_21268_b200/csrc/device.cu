@@ -903,7 +903,7 @@ struct ProfScope {
 void halo(DevState &D, const DCsr &A, double *x, cudaStream_t st) {
     if (!A.halo || D.p2p) return;
     if (A.nsend > 0) {
-        dev::k_pack<<<grid_for(D, A.nsend), dev::kBlock, 0, st>>>(A.nsend, A.sidx, x, A.sbuf);
+        launch_k(dev::k_pack, grid_for(D, A.nsend), dev::kBlock, 0, st, A.nsend, A.sidx, x, A.sbuf);
         D.launches_total++;
     }
     NCCL_OK(ncclGroupStart());
@@ -920,7 +920,7 @@ void allreduce_dot(DevState &D, int dotkind, cudaStream_t st) {
     if (D.nranks == 1) return;
     const int kind = dotkind & 255, kind2 = dotkind >> 8;
     if (D.p2p) {
-        dev::k_dot_collect<<<1, 32, 0, st>>>(kind, kind2, D.S, p2p_of(D, true));
+        launch_k(dev::k_dot_collect, 1, 32, 0, st, kind, kind2, D.S, p2p_of(D, true));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
         return;
@@ -967,14 +967,14 @@ void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStrea
             const int staged2 = full2 <= 200 * 1024 ? 1 : 0;
             const size_t smem2 = staged2 ? full2 : base2;
             if (smem2 > 48 * 1024) (void)resident_ctas((const void *)dev::k_coarse_cg, 1024, (int)smem2, (int)smem2);
-            dev::k_coarse_cg<<<1, 1024, smem2, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.diag, b, x, D.coarse_tol,
+            launch_k(dev::k_coarse_cg, 1, 1024, smem2, st, n, L.K.rp, L.K.ci, L.K.v, L.diag, b, x, D.coarse_tol,
                                                     D.coarse_maxit, staged2, p2p_of(D, first_rep));
             D.launches_total++;
             CUDA_OK(cudaGetLastError());
             return;
         }
         if (smem > 48 * 1024) (void)resident_ctas((const void *)dev::k_coarse_solve, 1024, (int)smem, (int)smem);
-        dev::k_coarse_solve<<<1, 1024, smem, st>>>(n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps, staged,
+        launch_k(dev::k_coarse_solve, 1, 1024, smem, st, n, L.K.rp, L.K.ci, L.K.v, L.invd, b, x, D.sweeps, staged,
                                                   p2p_of(D, first_rep));
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
@@ -986,7 +986,7 @@ void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStrea
     // --- pre-smoothing from x = 0: d0 = c0·b·invd (level 0 and the first replicated level; other
     //     coarse levels: restriction epilogue)
     if (l == 0 || first_rep) {
-        dev::k_cheb_first<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, b, L.invd, L.d[0], kC0,
+        launch_k(dev::k_cheb_first, grid_for(D, L.n), dev::kBlock, 0, st, L.n, b, L.invd, L.d[0], kC0,
                                                                    push_of(D, L.K, L.d[0]),
                                                                    p2p_of(D, l == 0 || first_rep,
                                                                           first_rep ? ~0u : L.K.wmask));
@@ -1045,11 +1045,11 @@ void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStrea
         e.c0 = kC0;
         launch_csr(D, L.R, L.r, e, st);
         NCCL_OK(ncclAllGather(D.ag_send, D.ag_recv, (size_t)D.ag_stride, ncclFloat64, D.comm, st));
-        dev::k_unpack_allgather<<<grid_for(D, D.ag_stride), dev::kBlock, 0, st>>>(D.nranks, D.ag_stride,
+        launch_k(dev::k_unpack_allgather, grid_for(D, D.ag_stride), dev::kBlock, 0, st, D.nranks, D.ag_stride,
                                                                                 D.ag_bounds, D.ag_recv, C.b);
         D.launches_total++;
         if (!coarse_is_last) {
-            dev::k_cheb_first<<<grid_for(D, C.n), dev::kBlock, 0, st>>>(C.n, C.b, C.invd, C.d[0], kC0, dev::Push{},
+            launch_k(dev::k_cheb_first, grid_for(D, C.n), dev::kBlock, 0, st, C.n, C.b, C.invd, C.d[0], kC0, dev::Push{},
                                                                        dev::P2P{});
             D.launches_total++;
         }
@@ -1112,7 +1112,7 @@ void vcycle_level_body(DevState &D, int l, const double *b, double *x, cudaStrea
         cur ^= 1;
     }
     if (m == 1) {
-        dev::k_axpy1<<<grid_for(D, L.n), dev::kBlock, 0, st>>>(L.n, L.d[0], x);
+        launch_k(dev::k_axpy1, grid_for(D, L.n), dev::kBlock, 0, st, L.n, L.d[0], x);
         D.launches_total++;
         CUDA_OK(cudaGetLastError());
     }
@@ -1128,7 +1128,7 @@ static void vcycle(DevState &D, const double *b, double *x, cudaStream_t st, int
     const bool fused = dotkind != dev::DOT_NONE && D.m > 1 && D.nlevels > 1;
     vcycle_level(D, 0, b, x, st, fused ? dotkind : dev::DOT_NONE, bdot);
     if (dotkind != dev::DOT_NONE && !fused) {
-        dev::k_dot<<<grid_for(D, n0), dev::kBlock, 0, st>>>(n0, bdot ? bdot : b, x, dotctx(D, dotkind));
+        launch_k(dev::k_dot, grid_for(D, n0), dev::kBlock, 0, st, n0, bdot ? bdot : b, x, dotctx(D, dotkind));
         D.launches_total++;
     }
     if (dotkind != dev::DOT_NONE) allreduce_dot(D, dotkind, st);
@@ -1635,6 +1635,9 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
             dev::k_fill_pattern<<<grid_for(*D, big * 4 + lomax), dev::kBlock>>>(big * 4 + lomax, scr);
             CUDA_OK(cudaGetLastError());
             double *sx = scr + lomax, *y1 = sx + big, *y2 = sx + 2 * big, *y3 = sx + 3 * big;
+            // a rank whose autotuning fails must not leave the others waiting in the NCCL collectives
+            // of the P2P setup: the ranks agree on the outcome first and all fail together
+            Error failed{AMG_OK, ""};
             try {
                 for (int l = 0; l < D->nlevels; l++) {
                     autotune_op(*D, D->lev[l].K, l, 0, sx, y1, y2, y3);
@@ -1643,11 +1646,18 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                         autotune_op(*D, D->lev[l].R, l, 2, sx, y1, y2, y3);
                     }
                 }
+            } catch (const Error &e) {
+                failed = e;
             } catch (...) {
-                cudaFree(scr);
-                throw;
+                failed = Error{AMG_ECUDA, "autotuning failed"};
             }
             cudaFree(scr);
+            if (want_p2p) {
+                const std::vector<int64_t> all = nccl_allgather_i64(*D, std::vector<int64_t>(1, failed.st != AMG_OK));
+                for (int q = 0; q < nr && failed.st == AMG_OK; q++)
+                    if (all[q]) failed = Error{AMG_EINVAL, "setup failed on rank " + std::to_string(q)};
+            }
+            if (failed.st != AMG_OK) throw failed;
         }
         // dominant kernel (level-0 fused Chebyshev step): the operator's streamed bytes in its chosen
         // format + 56 B/row of vectors (d_old, r in/out, x in/out, invd, d_new)
@@ -1702,9 +1712,9 @@ static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st, d
     const int flex = D.krylov == 1;
     if (flex) vcycle(D, D.r, D.z, st, dev::DOT_ZQ, D.q);  // FCG: zᵀq_prev (all-reduced)
     else vcycle(D, D.r, D.z, st, dev::DOT_RZ);            // CG: ρ = rᵀz (all-reduced)
-    dev::k_p_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.z, D.p, D.S, kind == 0 ? 1 : 0, flex,
+    launch_k(dev::k_p_update, grid_for(D, n), dev::kBlock, 0, st, n, D.z, D.p, D.S, kind == 0 ? 1 : 0, flex,
                                                            push_of(D, L0.K, D.p), p2p_of(D, L0.K), ctl);
-    dev::k_roll_rho<<<1, 1, 0, st>>>(D.S);
+    launch_k(dev::k_roll_rho, 1, 1, 0, st, D.S);
     D.launches_total += 2;
     {
         halo(D, L0.K, D.p, st);
@@ -1718,7 +1728,7 @@ static void enqueue_segment(DevState &D, int kind, double *u, cudaStream_t st, d
             allreduce_dot(D, dev::DOT_PQ, st);
         }
     }
-    dev::k_pcg_update<<<grid_for(D, n), dev::kBlock, 0, st>>>(n, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR), flex);
+    launch_k(dev::k_pcg_update, grid_for(D, n), dev::kBlock, 0, st, n, D.p, D.q, u, D.r, dotctx(D, dev::DOT_RR), flex);
     D.launches_total++;
     allreduce_dot(D, dev::DOT_RR, st);
     CUDA_OK(cudaGetLastError());
@@ -1754,7 +1764,7 @@ static void run_device_loop(DevState &D, double *u, cudaStream_t st) {
             CUDA_OK(cudaStreamBeginCaptureToGraph(D.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
             try {
                 enqueue_segment(D, 1, u, D.cap, D.ctl);
-                dev::k_loop_ctl<<<1, 1, 0, D.cap>>>(D.S, D.ctl, D.krylov == 1 ? 1 : 0, h);
+                launch_k(dev::k_loop_ctl, 1, 1, 0, D.cap, D.S, D.ctl, D.krylov == 1 ? 1 : 0, h);
                 CUDA_OK(cudaGetLastError());
             } catch (...) {
                 cudaGraph_t gb;
@@ -1835,13 +1845,13 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
     *relres = 0.0;
     CUDA_OK(cudaMemsetAsync(D.S, 0, sizeof(dev::Scalars), st));
     // ‖F‖²
-    dev::k_dot<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, F, F, dotctx(D, dev::DOT_FF));
+    launch_k(dev::k_dot, grid_for(D, N), dev::kBlock, 0, st, N, F, F, dotctx(D, dev::DOT_FF));
     D.launches_total++;
     allreduce_dot(D, dev::DOT_FF, st);
     // r = F − K u ; ‖r‖²   (u is copied into z, which has the ghost slots K_0 gathers)
     {
         if (D.p2p) {
-            dev::k_copy_push<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, u, D.z, push_of(D, L0.K, D.z), p2p_of(D, L0.K));
+            launch_k(dev::k_copy_push, grid_for(D, N), dev::kBlock, 0, st, N, u, D.z, push_of(D, L0.K, D.z), p2p_of(D, L0.K));
             D.launches_total++;
         } else {
             CUDA_OK(cudaMemcpyAsync(D.z, u, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
@@ -1850,7 +1860,7 @@ static amg_status pcg(DevState &D, const double *F, double *u, double rtol, int 
         dev::EpiResidualFrom e{F, D.r, nullptr, nullptr};
         launch_csr(D, L0.K, D.z, e, st);
     }
-    dev::k_dot<<<grid_for(D, N), dev::kBlock, 0, st>>>(N, D.r, D.r, dotctx(D, dev::DOT_RR));
+    launch_k(dev::k_dot, grid_for(D, N), dev::kBlock, 0, st, N, D.r, D.r, dotctx(D, dev::DOT_RR));
     D.launches_total++;
     allreduce_dot(D, dev::DOT_RR, st);
     CUDA_OK(cudaMemcpyAsync(D.hS, D.S, sizeof(dev::Scalars), cudaMemcpyDeviceToHost, st));

@@ -7,6 +7,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -21,6 +23,33 @@ namespace amgb {
         if (e_ != cudaSuccess)                                                                     \
             throw Error{AMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};            \
     } while (0)
+
+// Programmatic dependent launch of the solve-path kernels (kernels.cuh pdl_enter): each may be
+// scheduled while its predecessor drains.  OFF by default (AMG_PDL=1 turns it on): measured on B200 it
+// slows the solve — C3 7.26 vs 6.98 ms per iteration, C2 0.286 vs 0.257 ms (run r2n) — since the
+// persistent one-wave grids leave no launch gap to hide and the early-resident successor CTAs only
+// crowd the predecessor's tail.
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("AMG_PDL");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+template <class... KArgs, class... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 struct DevBuf {
     void *p = nullptr;

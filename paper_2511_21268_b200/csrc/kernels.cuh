@@ -38,6 +38,16 @@ constexpr int kBlock = 256;
 #define AMG_DCHECK(c) ((void)0)
 #endif
 
+// Programmatic dependent launch (PDL, opt-in with AMG_PDL=1; devstate.cuh launch_k): a solve-path kernel
+// launched with programmatic stream serialization may be scheduled while its predecessor drains.  It
+// starts with griddepcontrol.wait — full completion and memory flush of the predecessor, before any
+// global access — and then lets its own successor launch (launch_dependents after the wait: at most two
+// grids overlap).  Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Device scalar block.  Reductions only deposit sums (per rank; the multi-GPU path all-reduces the
 // slot right after the kernel); consumers derive α = ρ/pᵀq and β = ρ/ρ_prev themselves, so the
 // same kernels serve 1 and N GPUs.  The host reads the whole block once per iteration.
@@ -688,6 +698,7 @@ template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlock) k_csr2(const int64_t *__restrict__ rp, Cols cols,
                                                  const double *__restrict__ v, const double *__restrict__ g,
                                                  int64_t nrows, Epi epi, DotCtx dc, P2P pp, int pf) {
+    pdl_enter();
     if (!pp.gorder) peer_wait(pp);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -830,6 +841,7 @@ template <int G, int U, class Epi, class Cols>
 __global__ void __launch_bounds__(kBlockT) k_csr4t(const int64_t *__restrict__ rp, Cols cols,
                                                    const double *__restrict__ v, const double *__restrict__ g,
                                                    int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
+    pdl_enter();
     if (!pp.gorder) peer_wait(pp);
     using C = TmaCfg<U, Cols::kIdxBytes>;
     constexpr int NS = C::NS;
@@ -977,6 +989,7 @@ template <class Epi>
 __global__ void __launch_bounds__(kBlock) k_sell2(const int64_t *__restrict__ soff, const int2 *__restrict__ ci2,
                                                   const double2 *__restrict__ v2, const double *__restrict__ g,
                                                   int64_t nrows, Epi epi, DotCtx dc, P2P pp) {
+    pdl_enter();
     peer_wait(pp);
     constexpr int U = 4;
     const int lane = threadIdx.x & 31;
@@ -1067,6 +1080,7 @@ __global__ void __launch_bounds__(kBlock) k_sellvi(const int64_t *__restrict__ s
                                                    int nvals, int obits, const double *__restrict__ g, int64_t nrows,
                                                    Epi epi, DotCtx dc, P2P pp, int64_t nwhole, int lparts,
                                                    double2 *partial, unsigned *sticket) {
+    pdl_enter();
     const unsigned omask = (1u << obits) - 1u;
     const double *table = gtable;
     if constexpr (kSmem) {
@@ -1231,6 +1245,7 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
                                                     const double *__restrict__ gtable, int nvals, int pbits, int wmax,
                                                     const double *__restrict__ g, int64_t nrows, Epi epi, DotCtx dc,
                                                     int64_t nwhole, int wl, P2P pp) {
+    pdl_enter();
     constexpr int WPB = kBlock / 32;  // warps per CTA = slices per block
     extern __shared__ __align__(16) double wsm[];
     __shared__ __align__(8) uint64_t bar[NBUF];
@@ -1384,6 +1399,7 @@ __global__ void __launch_bounds__(kBlock) k_sellviw(const int64_t *__restrict__ 
 __global__ void __launch_bounds__(kBlock) k_cheb_first(int64_t n, const double *__restrict__ b,
                                                         const double *__restrict__ invd, double *__restrict__ d0,
                                                         double c0, Push push, P2P pp) {
+    pdl_enter();
     peer_wait(pp);
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double d = c0 * (b[i] * invd[i]);
@@ -1396,6 +1412,7 @@ __global__ void __launch_bounds__(kBlock) k_cheb_first(int64_t n, const double *
 // y = x (owned rows) and the ghost push of y (P2P: the initial residual's copy of u)
 __global__ void __launch_bounds__(kBlock) k_copy_push(int64_t n, const double *__restrict__ x, double *__restrict__ y,
                                                        Push push, P2P pp) {
+    pdl_enter();
     peer_wait(pp);
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double v = x[i];
@@ -1408,6 +1425,7 @@ __global__ void __launch_bounds__(kBlock) k_copy_push(int64_t n, const double *_
 // P2P all-reduce of one dot product: every rank deposited its sum in dslot[kind][q] of every rank
 // (block_dot_finalize); each rank adds them in rank order (identical on every rank).
 __global__ void k_dot_collect(int kind, int kind2, Scalars *S, P2P pp) {
+    pdl_enter();
     peer_wait(pp);
     if (threadIdx.x == 0) {
         const int kinds[2] = {kind, kind2};
@@ -1429,6 +1447,7 @@ __global__ void __launch_bounds__(kBlock) k_fill_pattern(int64_t n, double *__re
 }
 
 __global__ void __launch_bounds__(kBlock) k_axpy1(int64_t n, const double *__restrict__ d, double *__restrict__ x) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
         x[i] = x[i] + d[i];
 }
@@ -1436,6 +1455,7 @@ __global__ void __launch_bounds__(kBlock) k_axpy1(int64_t n, const double *__res
 // dot(a, b) -> scalar of kind dc.kind
 __global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
                                                  DotCtx dc) {
+    pdl_enter();
     peer_wait(dc.pp);
     double s = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
@@ -1448,6 +1468,7 @@ __global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const double *__restr
 __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *__restrict__ p,
                                                         const double *__restrict__ q, double *__restrict__ u,
                                                         double *__restrict__ r, DotCtx dc, int flex) {
+    pdl_enter();
     peer_wait(dc.pp);
     const double alpha = (flex ? dc.S->pr : dc.S->rz) / dc.S->pq;  // FCG: pᵀr / pᵀq; CG: ρ / pᵀq
     double s = 0.0;
@@ -1465,6 +1486,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double *
 __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                                                       const Scalars *__restrict__ S, int first_, int flex, Push push,
                                                       P2P pp, const LoopCtl *__restrict__ ctl) {
+    pdl_enter();
     peer_wait(pp);
     const int first = ctl ? ctl->first : first_;  // device loop: the first iteration is decided on the device
     // CG: β = ρ/ρ_prev; FCG(1): β = −zᵀq_prev / pᵀq_prev (S->pq still holds the previous iteration's)
@@ -1478,13 +1500,17 @@ __global__ void __launch_bounds__(kBlock) k_p_update(int64_t n, const double *__
 }
 
 // end of a PCG iteration: ρ_prev <- ρ (one thread; after every consumer of ρ in this iteration)
-__global__ void k_roll_rho(Scalars *S) { S->rz_prev = S->rz; }
+__global__ void k_roll_rho(Scalars *S) {
+    pdl_enter();
+    S->rz_prev = S->rz;
+}
 
 // Device loop control, after iteration k's ‖r‖² (c.19 stopping test, as the host loop takes it):
 // breakdown (CG: rᵀz <= 0; pᵀKp <= 0), ‖r_k‖ <= rtol·‖F‖, or k == maxit end the WHILE loop.  Every
 // rank holds the same all-reduced scalars, so every rank takes the same decision.
 __global__ void k_loop_ctl(const Scalars *__restrict__ S, LoopCtl *__restrict__ c, int flex,
                            cudaGraphConditionalHandle h) {
+    pdl_enter();
     const int k = c->k + 1;
     c->k = k;
     c->first = 0;
@@ -1509,6 +1535,7 @@ __global__ void k_loop_ctl(const Scalars *__restrict__ S, LoopCtl *__restrict__ 
 // gather/scatter helpers of the multi-GPU path
 __global__ void __launch_bounds__(kBlock) k_pack(int64_t n, const int *__restrict__ idx, const double *__restrict__ x,
                                                   double *__restrict__ buf) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
         buf[i] = x[idx[i]];
 }
@@ -1517,6 +1544,7 @@ __global__ void __launch_bounds__(kBlock) k_unpack_allgather(int nranks, int64_t
                                                               const int64_t *__restrict__ bounds,
                                                               const double *__restrict__ recv,
                                                               double *__restrict__ full) {
+    pdl_enter();
     for (int q = 0; q < nranks; q++) {
         const int64_t b = bounds[q], c = bounds[q + 1] - b;
         for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < c; i += (int64_t)gridDim.x * kBlock)
@@ -1532,6 +1560,7 @@ __global__ void __launch_bounds__(1024) k_coarse_solve(int n, const int64_t *__r
                                                         const int *__restrict__ ci, const double *__restrict__ v,
                                                         const double *__restrict__ invd, const double *__restrict__ b,
                                                         double *__restrict__ x, int sweeps, int staged, P2P pp) {
+    pdl_enter();
     peer_wait(pp);
     extern __shared__ double sm[];
     double *xa = sm, *xb = sm + n, *sb = sm + 2 * n, *sd = sm + 3 * n;
@@ -1593,6 +1622,7 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(int n, const int64_t *__rest
                                                      const double *__restrict__ v, const double *__restrict__ diag,
                                                      const double *__restrict__ b, double *__restrict__ x, double tol,
                                                      int maxit, int staged, P2P pp) {
+    pdl_enter();
     peer_wait(pp);
     extern __shared__ double sm[];
     __shared__ double red[32];

@@ -14,7 +14,7 @@ void launch_csr4t_gu(DevState &D, const DCsr &A, const Cols &cols, const double 
     const int per_sm = resident_ctas((const void *)dev::k_csr4t<G, U, Epi, Cols>, dev::kBlockT, smem, smem);
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-    dev::k_csr4t<G, U, Epi, Cols><<<grid, dev::kBlockT, smem, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
+    launch_k(dev::k_csr4t<G, U, Epi, Cols>, grid, dev::kBlockT, smem, st, A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
                                                                       (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
 }
 
@@ -27,7 +27,7 @@ void launch_csr2_gu(DevState &D, const DCsr &A, const Cols &cols, const double *
     // one wave: every CTA resident, warps stride over the row groups
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((ngroups + warps_per_block - 1) / warps_per_block, (int64_t)per_sm * D.nsm));
-    dev::k_csr2<G, U, Epi, Cols><<<grid, dev::kBlock, 0, st>>>(A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
+    launch_k(dev::k_csr2<G, U, Epi, Cols>, grid, dev::kBlock, 0, st, A.rp, cols, A.v, g, A.nrows, epi, dotctx(D, dotkind),
                                                                (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)),
                                                                (A.mult >= 8 ? A.pf : 0) | (A.l2keep ? 2 : 0));
 }
@@ -75,7 +75,7 @@ void launch_csr(DevState &D, const DCsr &A, const double *g, Epi epi, cudaStream
         const int64_t wpb = dev::kBlock / 32;
         const int per_sm = resident_ctas((const void *)dev::k_sell2<Epi>, dev::kBlock, 0);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-        dev::k_sell2<Epi><<<grid, dev::kBlock, 0, st>>>(A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind),
+        launch_k(dev::k_sell2<Epi>, grid, dev::kBlock, 0, st, A.soff, ci2, v2, g, A.nrows, epi, dotctx(D, dotkind),
                                                          (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_of(D, A)));
     } else if (A.kern & 8) {
         launch_csr_vi(D, A, g, epi, st, dotkind);  // instantiated in inst_vi_*.cu

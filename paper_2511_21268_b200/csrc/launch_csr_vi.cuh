@@ -26,7 +26,7 @@ void launch_sellviw(DevState &D, const DCsr &A, const double *g, Epi epi, cudaSt
     const int per_sm = resident_ctas((const void *)dev::k_sellviw<U, Epi, NBUF, kSmem>, dev::kBlock, smem, smem);
     const int64_t nitems = A.wwhole + ((nblk - A.wwhole) << A.wl);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nitems, (int64_t)per_sm * D.nsm));
-    dev::k_sellviw<U, Epi, NBUF, kSmem><<<grid, dev::kBlock, smem, st>>>(
+    launch_k(dev::k_sellviw<U, Epi, NBUF, kSmem>, grid, dev::kBlock, smem, st, 
         A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.binfo, A.wruns, A.vtab, (int)A.nvals, A.pbits, A.wmax, g,
         A.nrows, epi, dotctx(D, dotkind), A.wwhole, A.wl,
         (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)));
@@ -48,7 +48,7 @@ void launch_sellvi_us(DevState &D, const DCsr &A, const double *g, Epi epi, cuda
     const int64_t nwhole = lparts ? A.nwhole : nsl;
     const int64_t nitems = nwhole + ((nsl - nwhole) << lparts);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nitems + wpb - 1) / wpb, (int64_t)per_sm * D.nsm));
-    dev::k_sellvi<U, Epi, kSmem><<<grid, dev::kBlock, smem, st>>>(
+    launch_k(dev::k_sellvi<U, Epi, kSmem>, grid, dev::kBlock, smem, st, 
         A.soff, reinterpret_cast<const uint4 *>(A.vpk), A.rbase, A.vtab, (int)A.nvals, A.obits, g, A.nrows, epi,
         dotctx(D, dotkind), (dotkind != dev::DOT_NONE ? p2p_of(D, A.part) : p2p_csr(D, A)),
         nwhole, lparts, A.partial, A.sticket);
