@@ -268,7 +268,7 @@ amg_status amg_operator_config(amg_hierarchy *H, int level, int op, amg_op_confi
  * and a value table (built at setup for format 0 operators with >= 2e6 stored entries, >= 4 entries per
  * distinct value and <= 2^21 distinct values, unless env AMG_VALUE_INDEX=0); a SELL-VI operator
  * (layout 2) takes kernel 0, G 32 and U in {1, 2, 4} only, a windowed one (layout 3) kernel 1 or 2 (windows
- * staged per CTA), G 32 and U in {1, 2, 4}; G in {1,4,8,32}, U in {2,4,6,8}.  Every configuration
+ * staged per CTA), G 32 and U in {1, 2, 4}; G in {1,2,4,8,32}, U in {2,4,6,8}.  Every configuration
  * sums each row in the same order, so results are bitwise unchanged.  Drops captured PCG graphs.
  * AMG_EINVAL for a bad level/op or an unavailable configuration. */
 amg_status amg_operator_set_config(amg_hierarchy *H, int level, int op, int kernel, int G, int U);

@@ -782,7 +782,7 @@ void autotune_op(DevState &D, DCsr &A, int level, int role, double *x, double *y
         tune_store(key, A);
         return;
     }
-    const int Gs[] = {1, 4, 8, 32};
+    const int Gs[] = {1, 2, 4, 8, 32};  // G = 2: long rows, few of them (C3's K2: 7,383 pairs for 3,552 warps)
     const int Us[] = {2, 4, 6, 8};
     float best = 1e30f;
     int bk = A.kern, bg = A.G, bu = A.U, bp = A.pf;
@@ -2119,8 +2119,8 @@ extern "C" amg_status amg_operator_set_config(amg_hierarchy *H, int level, int o
         ((kernel & 8) && ((kernel & 1) || !A.vtab)))
         throw Error{AMG_EINVAL, "kernel not available for this operator"};
     if ((kernel & 1) && (A.mult < 8 || U > 4)) throw Error{AMG_EINVAL, "TMA core needs rows padded to 8 and U <= 4"};
-    if (!(G == 1 || G == 4 || G == 8 || G == 32) || !(U == 2 || U == 4 || U == 6 || U == 8))
-        throw Error{AMG_EINVAL, "G must be 1, 4, 8 or 32 and U 2, 4, 6 or 8"};
+    if (!(G == 1 || G == 2 || G == 4 || G == 8 || G == 32) || !(U == 2 || U == 4 || U == 6 || U == 8))
+        throw Error{AMG_EINVAL, "G must be 1, 2, 4, 8 or 32 and U 2, 4, 6 or 8"};
     CUDA_OK(cudaDeviceSynchronize());
     A.kern = kernel & 11;
     A.pf = (kernel >> 2) & 1;

@@ -50,7 +50,7 @@ void launch_csr_cols(DevState &D, const DCsr &A, const Cols &cols, const double 
         }                                                                                       \
         break;
 #define CASES_G(GG) CASE(GG, 2) CASE(GG, 4) CASE(GG, 6) CASE(GG, 8)
-        CASES_G(1) CASES_G(4) CASES_G(8) CASES_G(32)
+        CASES_G(1) CASES_G(2) CASES_G(4) CASES_G(8) CASES_G(32)
 #undef CASES_G
 #undef CASE
         default: throw Error{AMG_EINVAL, "bad CSR kernel configuration"};

@@ -110,7 +110,7 @@ def test_kernel_configs_bitwise_equal(case):
             if keep["n_values"]:  # bit 3: value index (CSR-VI), register core
                 kerns += [8, 10, 12, 14]
             for kern in kerns:
-                for G in (1, 4, 8, 32):
+                for G in (1, 2, 4, 8, 32):
                     for U in (2, 4, 6, 8):
                         if (kern & 1) and U > 4:
                             continue

@@ -55,7 +55,7 @@ def main():
             sellvi = chosen["layout"] in ("sellvi", "sellviw")
             sk = [1, 2] if chosen["layout"] == "sellviw" else [0]  # windowed: windows staged per CTA
             for kern in (sk if sellvi else kerns):
-                for G in ((32,) if sellvi else (1, 4, 8, 32)):
+                for G in ((32,) if sellvi else (1, 2, 4, 8, 32)):
                     for U in ((1, 2, 4) if sellvi else (2, 4, 6, 8)):
                         if (kern & 1) and U > 4:
                             continue
