@@ -369,7 +369,9 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     // rather than split), each entry's word = its column's position in the block's window.  Every
     // vector it may gather is 16-B aligned at column 0 (the lower ghost areas of the distributed
     // vectors have even length).  AMG_SELLVI_WIN=0 keeps the plain SELL-VI words.
-    bool win = true;
+    // only with the value table in shared memory: P̄₀ at C3 (17.9 K values, global table) ran 54.9 µs
+    // windowed against 43.9 µs plain (run r2p)
+    bool win = (int64_t)tab.size() <= kSellviSmemVals;
     if (const char *e = std::getenv("AMG_SELLVI_WIN"))
         if (std::atoi(e) == 0) win = false;
     const int64_t nblk = (nsl + kWinSlices - 1) / kWinSlices;

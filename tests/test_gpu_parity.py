@@ -166,8 +166,10 @@ def test_sellvi_layout(windowed, monkeypatch):
             c = H.op_config(l, op)
             if c["layout"] not in ("sellvi", "sellviw"):
                 continue
-            if op == 0:
-                assert c["layout"] == layout, (l, op, c)  # every square K_l of C2 admits the windows
+            if op == 0 and l == 0:
+                assert c["layout"] == layout, (l, op, c)  # K_0 (159 values, table in shared memory) is windowed
+            if c["layout"] == "sellviw":
+                assert c["n_values"] <= 8192  # windows only with the value table in shared memory
             seen += 1
             A = A.tocsr()
             bits = np.unique(np.concatenate([A.data.view(np.uint64), np.zeros(1, np.uint64)]))
