@@ -367,6 +367,30 @@ def test_host_pointer_entry_matches_device_entry():
     assert it == it2 and np.array_equal(u_dev.cpu().numpy(), u_host)
 
 
+@pytest.mark.parametrize("krylov", [0, 1])
+def test_device_loop_equals_host_loop(krylov, monkeypatch):
+    """The Krylov loop on the device (one graph with a conditional WHILE node, k_loop_ctl deciding) gives
+    BITWISE the iterate, the iteration count, the status and the residual history of the per-iteration
+    graphs with the host's stopping test (AMG_DEVICE_LOOP=0): converged, cut at maxit, rtol = 0, and a
+    zero right-hand side; PCG and FCG with the §5.1 coarse CG."""
+    amg = _amg()
+    dim, p, n = CASES["C2"]
+    Hs = {}
+    for dl in (0, 1):
+        monkeypatch.setenv("AMG_DEVICE_LOOP", str(dl))
+        K, F = amg.iga_poisson(dim, p, n, rhs=2 if krylov else 0)
+        Hs[dl] = amg.Hierarchy(K, amg.params(p, krylov=krylov, coarse_solver=krylov))
+    Fd = dev(F)
+    for rtol, maxit, rhs in ((1e-8, 200, Fd), (1e-8, 3, Fd), (0.0, 5, Fd), (1e-6, 50, torch.zeros_like(Fd))):
+        out = []
+        for dl in (0, 1):
+            u, it, rr, hist, st = Hs[dl].solve(rhs, rtol=rtol, maxit=maxit)
+            out.append((u.cpu().numpy(), it, rr, np.asarray(hist), st))
+        (u0, i0, r0, h0, s0), (u1, i1, r1, h1, s1) = out
+        assert (i0, s0) == (i1, s1) and np.array_equal(u0, u1), (rtol, maxit, i0, i1, s0, s1)
+        assert r0 == r1 and np.array_equal(h0, h1, equal_nan=True)
+
+
 def test_deterministic_runs():
     K, F, H, Ho = build("cube12p3")
     a = H.solve(dev(F))[0].cpu().numpy()

@@ -302,7 +302,7 @@ def _study():
 def test_opc_tie_order_study(table1):
     """PAPER pin of the tie-order reading (DESIGN.md c.8t) on the committed study (written by the
     oracle-only oracle/scripts/opc_study.py; oracle/sizes_C3.json for the canonical k = 96 setup):
-    Table 1c at (24,3), (48,3), (96,3) lies between the two kinds of tie order — the
+    Table 1c at (24,3), (48,3), (96,3) and (96,4) lies between the two kinds of tie order — the
     pseudo-random order (3 seeds) within ±0.015 of the paper (printed to 2 decimals) at every k, the
     index orders (canonical, and preferring the larger index) at most 0.035 below it and never above
     it by more than 0.005."""
@@ -316,6 +316,12 @@ def test_opc_tie_order_study(table1):
         for n in ("canonical", "tie_larger_index"):
             assert paper - 0.035 <= r[n]["opc"] <= paper + 0.005, (k, n, r[n]["opc"], paper)
         assert r["canonical"]["N"][0] == table1[(k, 3)][0]
+    # (96,4): the same picture with a wider tie spread at p = 4 (1.258 index order, 1.301 pseudo-random,
+    # paper 1.30)
+    r, paper = st["k96_p4"], table1[(96, 4)][1]
+    assert abs(r["tie_hashed"]["opc"] - paper) <= 0.015, r["tie_hashed"]["opc"]
+    assert paper - 0.045 <= r["canonical"]["opc"] <= paper + 0.005, r["canonical"]["opc"]
+    assert r["canonical"]["N"][0] == table1[(96, 4)][0]
 
 
 @pytest.mark.slow
