@@ -117,7 +117,7 @@ def main():
             times += [(time.perf_counter() - stamps[0]) / max(it, 1)] * max(it, 1)
     timed = times[args.warmup:]
     s_iter = sum(timed) / max(len(timed), 1)
-    out = dict(config=args.config, problem=args.problem, krylov="FCG(1)" if paper else "PCG",
+    out = dict(config=args.config, problem="paper" if paper else "manufactured", krylov="FCG(1)" if paper else "PCG",
                N=H.levels[0].N, levels=H.nlevels, opc=round(H.opc(), 4),
                assemble_s=round(t_asm, 2), setup_s=round(t_setup, 2), step_s=[round(t, 4) for t in timed],
                warmup=args.warmup, steps=args.steps, s_per_iter=round(s_iter, 4), full_solve=full,
