@@ -210,11 +210,13 @@ def run_gpu(args) -> None:
     if rank == 0:
         # torchrun sets OMP_NUM_THREADS=1 per process; the generator runs alone on rank 0
         amg.set_num_threads(len(os.sched_getaffinity(0)))
+        # keep_c + take below: K stays the library's array and the setup takes it over (no numpy copy and
+        # no setup copy of K: what lets C5 at 4 GPUs fit the box's host RAM)
         if geom == 1 and not paper:  # quarter ring, manufactured-style run: seeded random right-hand side
-            K, _ = amg.iga_poisson(dim, p, n, rhs=1, geometry=1)
+            K, _ = amg.iga_poisson(dim, p, n, rhs=1, geometry=1, keep_c=True)
             F = amg_inputs.uniform_pm1(K.shape[0], seed=amg_inputs.SEED)
         else:
-            K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0, geometry=geom)
+            K, F = amg.iga_poisson(dim, p, n, rhs=2 if paper else 0, geometry=geom, keep_c=True)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     prm = amg.params(p, format=args.format, krylov=1 if paper else 0, coarse_solver=1 if paper else 0)
@@ -222,9 +224,9 @@ def run_gpu(args) -> None:
         # one host setup on rank 0 with all host cores; every rank receives its share (local operators,
         # halo plans, replicated levels) over gloo and builds its device state from it
         gl = dist.new_group(backend="gloo")
-        H = amg.setup_distributed(K, prm, rank, world, device=local, group=gl)
+        H = amg.setup_distributed(K, prm, rank, world, device=local, group=gl, take=True)
     else:
-        H = amg.Hierarchy(K, prm)
+        H = amg.Hierarchy(K, prm, take=True)
     del K
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0

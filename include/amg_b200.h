@@ -186,6 +186,13 @@ amg_status amg_local_rows(amg_hierarchy *H, int64_t *row_begin, int64_t *row_end
  * *H is released with amg_hierarchy_free. */
 amg_status amg_setup(const amg_csr *K, const amg_params *prm, const amg_dist *dist, amg_hierarchy **H);
 
+/* amg_setup without the copy of K: the hierarchy takes K's three arrays over (they must come from the
+ * library, e.g. amg_iga_poisson, i.e. be malloc'd) and K itself is released with amg_csr_free — in
+ * every case, also on error; the caller must not touch K afterwards.  For the largest workloads, whose
+ * K₀ alone is tens of GB (C5 at 4 GPUs: 94 GB of host RAM): it saves one copy of K at the setup's
+ * peak.  Same parameters, results (bitwise) and errors as amg_setup. */
+amg_status amg_setup_take(amg_csr *K, const amg_params *prm, const amg_dist *dist, amg_hierarchy **H);
+
 /* PCG (c.19) preconditioned by one V-cycle per iteration (c.18).
  * F, u: DEVICE pointers (fp64, N = K->n_rows); u holds the initial guess on entry and the solution on
  * exit.  Stops when ‖r_k‖₂ <= rtol·‖F‖₂ (recurrence residual) or k == maxit; iteration count = number
@@ -310,8 +317,10 @@ amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist
  * export (NULL dist = rank 0 of 1): the result behaves like amg_setup's for that rank — same device
  * state, same kernels, bitwise the same solve — except that amg_hierarchy_export is unavailable
  * (AMG_EINVAL: the global operators are not held).  host_only = 1 skips the device part (for
- * amg_dist_view_get / amg_hierarchy_info).  The blob is borrowed (copied); AMG_EINVAL on a truncated or
- * corrupt blob. */
+ * amg_dist_view_get / amg_hierarchy_info); with host_only = 0 the host copies of this rank's operators
+ * are freed once the device holds them (amg_dist_view_get then returns AMG_EINVAL; amg_hierarchy_info and
+ * amg_local_rows keep working).  The blob is borrowed (copied); AMG_EINVAL on a truncated or corrupt
+ * blob. */
 amg_status amg_share_export(const amg_hierarchy *H, int rank, int nranks, void **share, int64_t *bytes);
 amg_status amg_setup_from_share(const void *share, int64_t bytes, const amg_dist *dist, int host_only,
                                 amg_hierarchy **H);

@@ -47,14 +47,60 @@ def _from_c(ptr) -> HostCsr:
     return HostCsr(rp, ci, v, shape)
 
 
-def iga_poisson(dim: int, p: int, n: int, dirichlet_sides: int = 0b000111, rhs: int = 0, geometry: int = 0):
+class LibCsr:
+    """A library-owned amg_csr (from amg_iga_poisson with keep_c=True), for the largest workloads: no
+    numpy copy of K; `Hierarchy(K, ..., take=True)` hands its arrays to amg_setup_take, after which K
+    only keeps its shape.  The array views (indptr, indices, data) are valid while K is neither taken
+    nor garbage-collected."""
+
+    def __init__(self, ptr):
+        self._p = ptr
+        c = ptr.contents
+        self.shape = (c.n_rows, c.n_cols)
+        self._nnz = c.nnz
+
+    @property
+    def nnz(self) -> int:
+        return self._nnz
+
+    def _arrays(self):
+        if self._p is None:
+            raise ValueError("K was taken over by amg_setup_take")
+        c = self._p.contents
+        n, nnz = c.n_rows, c.nnz
+        return (np.ctypeslib.as_array(c.row_ptr, shape=(n + 1,)),
+                np.ctypeslib.as_array(c.col, shape=(max(nnz, 1),))[:nnz],
+                np.ctypeslib.as_array(c.val, shape=(max(nnz, 1),))[:nnz])
+
+    indptr = property(lambda self: self._arrays()[0])
+    indices = property(lambda self: self._arrays()[1])
+    data = property(lambda self: self._arrays()[2])
+
+    def to_scipy(self):  # a copy (the views die with K)
+        return HostCsr(*(a.copy() for a in self._arrays()), self.shape).to_scipy()
+
+    def take(self):
+        p, self._p = self._p, None
+        if p is None:
+            raise ValueError("K was already taken")
+        return p
+
+    def __del__(self):
+        if getattr(self, "_p", None) is not None:
+            lib().amg_csr_free(self._p)
+            self._p = None
+
+
+def iga_poisson(dim: int, p: int, n: int, dirichlet_sides: int = 0b000111, rhs: int = 0, geometry: int = 0,
+                keep_c: bool = False):
     """amg_iga_poisson: (K as HostCsr, F as numpy fp64).  geometry 1 = the thick quarter ring (dim 3),
-    geometry 2 = the three-patch L-shape (dim 3; rhs 0: f = 1, 1: F = 0, 2: its paper data)."""
+    geometry 2 = the three-patch L-shape (dim 3; rhs 0: f = 1, 1: F = 0, 2: its paper data).
+    keep_c: K stays the library's array (LibCsr; no numpy copy) for Hierarchy(K, take=True)."""
     d = _lib.amg_iga_desc(dim, p, n, dirichlet_sides, rhs, geometry)
     Kp = C.POINTER(_lib.amg_csr)()
     Fp = C.POINTER(C.c_double)()
     check(lib().amg_iga_poisson(C.byref(d), C.byref(Kp), C.byref(Fp)))
-    K = _from_c(Kp)
+    K = LibCsr(Kp) if keep_c else _from_c(Kp)
     F = np.ctypeslib.as_array(Fp, shape=(K.shape[0],)).copy()
     lib().amg_free(Fp)
     return K, F
@@ -181,20 +227,25 @@ class Share:
 class Hierarchy:
     """amg_setup / amg_pcg_solve / amg_vcycle / amg_level_apply / export / info on one handle."""
 
-    def __init__(self, K, prm: _lib.amg_params | None = None, dist: _lib.amg_dist | None = None):
+    def __init__(self, K, prm: _lib.amg_params | None = None, dist: _lib.amg_dist | None = None,
+                 take: bool = False):
+        """amg_setup; take=True with a LibCsr K: amg_setup_take (K's arrays become the hierarchy's)."""
         if K is None:  # from_share
             self._h = C.c_void_p()
             return
-        c, keep = _borrow(K)
         self._h = C.c_void_p()
         if prm is None:
             prm = params(2)
         if not prm.host_only:
             use_torch_allocator()
-        check(lib().amg_setup(C.byref(c), C.byref(prm), C.byref(dist) if dist is not None else None,
-                              C.byref(self._h)))
+        dp = C.byref(dist) if dist is not None else None
+        if take and isinstance(K, LibCsr):
+            check(lib().amg_setup_take(K.take(), C.byref(prm), dp, C.byref(self._h)))
+        else:
+            c, keep = _borrow(K)
+            check(lib().amg_setup(C.byref(c), C.byref(prm), dp, C.byref(self._h)))
+            del keep
         self.prm = prm
-        del keep
 
     @classmethod
     def from_share(cls, share, dist: _lib.amg_dist | None = None, host_only: bool = False) -> "Hierarchy":
@@ -367,7 +418,7 @@ class Hierarchy:
 
 def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: int = 0, group=None,
                       nccl_id: bytes | None = None, host_only: bool = False,
-                      chunk_bytes: int = 1 << 28) -> Hierarchy:
+                      chunk_bytes: int = 1 << 28, take: bool = False) -> Hierarchy:
     """One host setup for the whole job: rank 0 builds the hierarchy of K once
     (amg_setup, host_only), exports every rank's share (amg_share_export) and sends it over `group`
     (a gloo group of torch.distributed; created when None); every rank then creates its device state
@@ -399,10 +450,12 @@ def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: i
         hp = _lib.amg_params()
         C.memmove(C.byref(hp), C.byref(prm), C.sizeof(hp))
         hp.host_only = 1
-        G = Hierarchy(K, hp)
+        G = Hierarchy(K, hp, take=take)  # take: K's arrays become G's level 0 (one copy of K₀ less)
         lap("host_setup")
-        mine = None
-        for q in range(nranks):
+        # the other ranks' shares first, one at a time; rank 0's own last, after which the global
+        # hierarchy is freed before rank 0's device setup (host RAM holds at most G + one share + the
+        # receiving rank's upload at any time)
+        for q in list(range(1, nranks)) + [0]:
             sh = G.export_share(q, nranks)
             lap("export")
             ph["share_bytes"] = ph.get("share_bytes", 0) + sh.nbytes

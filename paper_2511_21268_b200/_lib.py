@@ -20,7 +20,7 @@ STATUS = {0: "AMG_OK", 1: "AMG_NOT_CONVERGED", -1: "AMG_EINVAL", -2: "AMG_ENOMEM
 
 # every symbol declared in include/amg_b200.h
 EXPORTED = ["amg_iga_poisson", "amg_iga_tables", "amg_csr_free", "amg_free", "amg_params_default",
-            "amg_set_allocator", "amg_setup", "amg_pcg_solve", "amg_pcg_solve_host", "amg_vcycle",
+            "amg_set_allocator", "amg_setup", "amg_setup_take", "amg_pcg_solve", "amg_pcg_solve_host", "amg_vcycle",
             "amg_level_apply", "amg_hierarchy_info", "amg_hierarchy_export", "amg_set_profiling",
             "amg_get_kernel_stats", "amg_operator_config", "amg_operator_set_config", "amg_get_level_times", "amg_nccl_unique_id", "amg_local_rows",
             "amg_dist_view_get", "amg_share_export", "amg_setup_from_share", "amg_set_num_threads",
@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
         "amg_params_default": ([P(amg_params), C.c_int], C.c_int),
         "amg_set_allocator": ([vp, vp], C.c_int),
         "amg_setup": ([P(amg_csr), P(amg_params), P(amg_dist), P(vp)], C.c_int),
+        "amg_setup_take": ([P(amg_csr), P(amg_params), P(amg_dist), P(vp)], C.c_int),
         "amg_pcg_solve": ([vp, vp, vp, C.c_double, C.c_int, vp, ip, dp, dp], C.c_int),
         "amg_pcg_solve_host": ([vp, dp, dp, C.c_double, C.c_int, vp, ip, dp, dp], C.c_int),
         "amg_vcycle": ([vp, vp, vp, vp], C.c_int),

@@ -39,6 +39,14 @@ int64_t replicate_nnz() {  // replicate levels below ~7e6 non-zeros (SURVEY §8(
     return rep;
 }
 
+void check_params(const amg_params &prm) {
+    if (prm.agg_steps < 1 || prm.cheb_degree < 1 || prm.coarse_sweeps < 0 || prm.max_levels < 1 ||
+        prm.coarse_size < 1 || !(prm.filter_theta >= 0.0) || prm.krylov < 0 || prm.krylov > 1 ||
+        prm.coarse_solver < 0 || prm.coarse_solver > 1 || !(prm.coarse_tol >= 0.0) || prm.coarse_maxit < 0 ||
+        prm.format < 0 || prm.format > 6)
+        throw Error{AMG_EINVAL, "bad parameter"};
+}
+
 amg_csr *export_csr(const HCsr &A) {
     amg_csr *c = static_cast<amg_csr *>(std::calloc(1, sizeof(amg_csr)));
     if (!c) throw Error{AMG_ENOMEM, "host allocation failed"};
@@ -107,7 +115,15 @@ amg_status amg_iga_poisson(const amg_iga_desc *d, amg_csr **K, double **F) {
     HCsr A;
     Buf<double> f;
     iga_assemble(*d, A, f);
-    amg_csr *c = export_csr(A);
+    // hand the assembled arrays over (no second copy of K: C5's K₀ alone is 94 GB at 4 GPUs)
+    amg_csr *c = static_cast<amg_csr *>(std::calloc(1, sizeof(amg_csr)));
+    if (!c) throw Error{AMG_ENOMEM, "host allocation failed"};
+    c->n_rows = A.nrows;
+    c->n_cols = A.ncols;
+    c->nnz = A.nnz();
+    c->row_ptr = A.rp.release();
+    c->col = A.ci.release();
+    c->val = A.v.release();
     double *fo = static_cast<double *>(std::malloc(sizeof(double) * (A.nrows > 0 ? A.nrows : 1)));
     if (!fo) {
         amg_csr_free(c);
@@ -150,11 +166,7 @@ amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist 
     amg_params prm;
     if (prm_in) prm = *prm_in;
     else amg_params_default(&prm, 2);
-    if (prm.agg_steps < 1 || prm.cheb_degree < 1 || prm.coarse_sweeps < 0 || prm.max_levels < 1 ||
-        prm.coarse_size < 1 || !(prm.filter_theta >= 0.0) || prm.krylov < 0 || prm.krylov > 1 ||
-        prm.coarse_solver < 0 || prm.coarse_solver > 1 || !(prm.coarse_tol >= 0.0) || prm.coarse_maxit < 0 ||
-        prm.format < 0 || prm.format > 6)
-        throw Error{AMG_EINVAL, "bad parameter"};
+    check_params(prm);
     if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
         throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
     amg_hierarchy *H = new amg_hierarchy();
@@ -172,6 +184,50 @@ amg_status amg_setup(const amg_csr *K, const amg_params *prm_in, const amg_dist 
     *Hout = H;
     return AMG_OK;
     API_END
+}
+
+amg_status amg_setup_take(amg_csr *K, const amg_params *prm_in, const amg_dist *dist, amg_hierarchy **Hout) {
+    // as amg_setup, with K's arrays taken over by the hierarchy instead of copied; K is released in
+    // every case (its arrays are owned by the hierarchy or freed)
+    if (!K) {
+        set_error("NULL argument");
+        return AMG_EINVAL;
+    }
+    amg_status st = AMG_OK;
+    try {
+        if (!Hout || !K->row_ptr || (K->nnz && (!K->col || !K->val))) throw Error{AMG_EINVAL, "NULL argument"};
+        if (K->n_rows < 1 || K->n_rows > INT32_MAX) throw Error{AMG_EINVAL, "n_rows out of range"};
+        amg_params prm;
+        if (prm_in) prm = *prm_in;
+        else amg_params_default(&prm, 2);
+        check_params(prm);
+        if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+            throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
+        amg_hierarchy *H = new amg_hierarchy();
+        try {
+            build_hierarchy_take(*K, prm, H->host);
+            if (dist && dist->nranks > 1) {
+                build_dist_plan(H->host, dist->rank, dist->nranks, replicate_nnz(), H->plan);
+                H->distributed = true;
+            }
+            if (!prm.host_only) H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
+        } catch (...) {
+            delete H;
+            throw;
+        }
+        *Hout = H;
+    } catch (const Error &e) {
+        set_error(e.msg);
+        st = e.st;
+    } catch (const std::bad_alloc &) {
+        set_error("out of host memory");
+        st = AMG_ENOMEM;
+    } catch (...) {
+        set_error("unknown internal error");
+        st = AMG_EINVAL;
+    }
+    amg_csr_free(K);  // arrays already taken over are NULL here
+    return st;
 }
 
 amg_status amg_share_export(const amg_hierarchy *H, int rank, int nranks, void **share, int64_t *bytes) {
@@ -196,7 +252,26 @@ amg_status amg_setup_from_share(const void *share, int64_t bytes, const amg_dist
         share_import(share, bytes, rank, nranks, H->host, H->plan);
         H->host.prm.host_only = host_only ? 1 : 0;
         H->distributed = nranks > 1;
-        if (!host_only) H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
+        if (!host_only) {
+            H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
+            // the device holds everything the solve needs: free this rank's host operators (the ranks of
+            // one job share one host, whose RAM is what bounds the largest runs); the sizes, nnz counts
+            // and row bounds stay for amg_hierarchy_info / amg_local_rows
+            auto drop = [](HCsr &A) {
+                A.ci = Buf<int32_t>();
+                A.v = Buf<double>();
+            };
+            for (int l = 0; l < H->host.nlevels; l++) {
+                HLevel &L = H->host.lev[l];
+                drop(L.K);
+                drop(L.P);
+                drop(L.R);
+                drop(H->plan.lev[l].K.A);
+                drop(H->plan.lev[l].P.A);
+                drop(H->plan.lev[l].R.A);
+            }
+            H->host.released = true;
+        }
     } catch (...) {
         delete H;
         throw;
@@ -263,6 +338,7 @@ amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist
     if (!H || !v || !H->distributed) throw Error{AMG_EINVAL, "hierarchy is not distributed"};
     if (level < 0 || level >= H->host.nlevels || op < 0 || op > 2) throw Error{AMG_EINVAL, "bad level/op"};
     if (op > 0 && level == H->host.nlevels - 1) throw Error{AMG_EINVAL, "no transfer operator on the coarsest level"};
+    if (H->host.released) throw Error{AMG_EINVAL, "host operators released after the device upload (use host_only)"};
     const DistLevel &D = H->plan.lev[level];
     std::memset(v, 0, sizeof(*v));
     v->nranks = H->plan.nranks;

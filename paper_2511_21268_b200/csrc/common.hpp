@@ -48,6 +48,18 @@ struct Buf {
         return *this;
     }
     ~Buf() { std::free(p); }
+    // hand the malloc'd array over (to an amg_csr the caller frees) / take one over (from an amg_csr)
+    T *release() {
+        T *q = p;
+        p = nullptr;
+        n = 0;
+        return q;
+    }
+    void adopt(T *q, int64_t count) {
+        std::free(p);
+        p = q;
+        n = count;
+    }
     T &operator[](int64_t i) { return p[i]; }
     const T &operator[](int64_t i) const { return p[i]; }
     T *data() { return p; }
@@ -80,6 +92,7 @@ struct HHierarchy {
     amg_params prm{};
     int nlevels = 0;
     bool thin = false;  // built from one rank's share (share.cpp): distributed levels held as LocalOps
+    bool released = false;  // thin + device: the host operators were freed once uploaded (amg_setup_from_share)
     HLevel lev[32];
 };
 
@@ -132,6 +145,8 @@ void iga_assemble(const amg_iga_desc &d, HCsr &K, Buf<double> &F);
 
 // setup.cpp
 void build_hierarchy(const amg_csr &K, const amg_params &prm, HHierarchy &H);
+// The same, taking K's arrays over instead of copying them (amg_setup_take): K's pointers are nulled.
+void build_hierarchy_take(amg_csr &K, const amg_params &prm, HHierarchy &H);
 
 // device.cu
 struct DevState;

@@ -443,12 +443,22 @@ void validate(const HCsr &A) {
         }
     }
     if (bad) throw Error{AMG_EINVAL, "K: columns must be in range and strictly ascending per row"};
-    HCsr T;
-    transpose(A, T);
-    bool same = std::memcmp(T.rp.data(), A.rp.data(), sizeof(int64_t) * (A.nrows + 1)) == 0 &&
-                std::memcmp(T.ci.data(), A.ci.data(), sizeof(int32_t) * A.nnz()) == 0 &&
-                std::memcmp(T.v.data(), A.v.data(), sizeof(double) * A.nnz()) == 0;
-    if (!same) throw Error{AMG_EINVAL, "K must be exactly (bitwise) symmetric"};
+    // exact (bitwise) symmetry: every stored (i, j) has a stored (j, i) with the same bits — found by
+    // binary search in row j (ascending columns), so no transposed copy of K is built (K₀ of C5 at 4
+    // GPUs is 94 GB); (i, j) ↦ (j, i) is then an involution of the stored entries, i.e. K == Kᵀ bitwise
+    std::atomic<int> asym{0};
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < A.nrows; i++) {
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1] && !asym; k++) {
+            const int32_t j = A.ci[k];
+            const int32_t *b = A.ci.data() + A.rp[j], *e = A.ci.data() + A.rp[j + 1];
+            const int32_t *f = std::lower_bound(b, e, (int32_t)i);
+            if (f == e || *f != i ||
+                std::memcmp(&A.v[k], &A.v[A.rp[j] + (f - b)], sizeof(double)) != 0)
+                asym = 1;
+        }
+    }
+    if (asym) throw Error{AMG_EINVAL, "K must be exactly (bitwise) symmetric"};
     Buf<double> d;
     diagonal(A, d);  // throws AMG_ENOTSPD on a missing or non-positive diagonal entry
 }
@@ -458,12 +468,32 @@ void validate(const HCsr &A) {
 // Hierarchy (c.6-c.15): level l is the coarsest if N_l <= coarse_size, l+1 == max_levels, or the
 // composite aggregation does not reduce N_l.  w^(0) = 1 (c.6); the test vector is carried through the
 // pairwise steps (w_{s+1} = ‖w_e‖) and on to the next level.
+static void build_levels(const amg_params &prm, HHierarchy &H);
+
 void build_hierarchy(const amg_csr &Kin, const amg_params &prm, HHierarchy &H) {
     if (prm.num_threads > 0) omp_set_num_threads(prm.num_threads);
+    copy_in(Kin, H.lev[0].K);
+    build_levels(prm, H);
+}
+
+void build_hierarchy_take(amg_csr &Kin, const amg_params &prm, HHierarchy &H) {
+    if (prm.num_threads > 0) omp_set_num_threads(prm.num_threads);
+    HCsr &A = H.lev[0].K;
+    A.nrows = Kin.n_rows;
+    A.ncols = Kin.n_cols;
+    A.rp.adopt(Kin.row_ptr, Kin.n_rows + 1);
+    A.ci.adopt(Kin.col, Kin.nnz);
+    A.v.adopt(Kin.val, Kin.nnz);
+    Kin.row_ptr = nullptr;
+    Kin.col = nullptr;
+    Kin.val = nullptr;
+    build_levels(prm, H);
+}
+
+static void build_levels(const amg_params &prm, HHierarchy &H) {
     H.prm = prm;
     H.nlevels = 0;
     HLevel &L0 = H.lev[0];
-    copy_in(Kin, L0.K);
     validate(L0.K);
     L0.N = L0.K.nrows;
     Buf<double> w(L0.N);

@@ -53,6 +53,30 @@ def test_errors_are_reported_not_raised_through_abi():
         amg.Hierarchy(A, amg.params(2, host_only=1))
 
 
+def test_setup_take_equals_setup():
+    """amg_setup_take (the hierarchy takes the generator's arrays over, no copy of K) builds bitwise the
+    hierarchy amg_setup builds from a copy; K is consumed (a second take fails)."""
+    K, _ = amg.iga_poisson(3, 3, 8)
+    Kc, _ = amg.iga_poisson(3, 3, 8, keep_c=True)
+    assert isinstance(Kc, amg.LibCsr) and Kc.nnz == K.nnz
+    assert np.array_equal(Kc.to_scipy().data.view(np.uint64), K.to_scipy().data.view(np.uint64))
+    H = amg.Hierarchy(K, amg.params(3, host_only=1))
+    Ht = amg.Hierarchy(Kc, amg.params(3, host_only=1), take=True)
+    with pytest.raises(ValueError):
+        Kc.take()
+    assert Kc.shape == K.shape
+    for l in range(H.info()["levels"]):
+        a, b = H.export(l), Ht.export(l)
+        assert _bitwise(a["K"].to_scipy(), b["K"].to_scipy())
+        if a["P"] is not None:
+            assert _bitwise(a["P"].to_scipy(), b["P"].to_scipy())
+    # the symmetry check without a transposed copy still rejects a non-symmetric K (one value flipped)
+    Kn, _ = amg.iga_poisson(2, 2, 4, keep_c=True)
+    Kn.data[1] = Kn.data[1] * 0.5
+    with pytest.raises(amg.AmgError, match="symmetric"):
+        amg.Hierarchy(Kn, amg.params(2, host_only=1), take=True)
+
+
 def test_solve_without_device_part_fails_loudly():
     K, F = amg.iga_poisson(2, 2, 4)
     H = amg.Hierarchy(K.to_scipy(), amg.params(2, host_only=1))
