@@ -18,6 +18,8 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <vector>
@@ -59,9 +61,60 @@ struct Chunk {
     std::vector<double> v;
 };
 
+// Two-pass assembly for the largest levels (fine levels of C5-sized problems, or AMG_SETUP_LEAN=1):
+// every row is computed twice, once to count and once straight into the exactly-sized output, so the
+// peak holds the output once instead of the chunk buffers (with vector growth slack) plus the output.
+// The rows are the same computation both times, so the result is bitwise the single-pass one.
+inline bool lean_rows(int64_t nrows) {
+    static const int forced = [] {
+        const char *e = std::getenv("AMG_SETUP_LEAN");
+        return e ? std::atoi(e) : -1;
+    }();
+    return forced >= 0 ? forced != 0 : nrows >= 8000000;
+}
+
 // fn(row, spa, out_ci, out_v): append the row's entries (ascending columns) to out_ci/out_v.
 template <class Fn>
 void build_rows(int64_t nrows, int64_t ncols, HCsr &out, Fn fn) {
+    out.nrows = nrows;
+    out.ncols = ncols;
+    if (lean_rows(nrows)) {
+        out.rp.alloc(nrows + 1);
+        out.rp[0] = 0;
+#pragma omp parallel
+        {
+            Spa spa;
+            spa.init(ncols);
+            std::vector<int32_t> ci;
+            std::vector<double> v;
+#pragma omp for schedule(dynamic, 2048)
+            for (int64_t r = 0; r < nrows; r++) {
+                ci.clear();
+                v.clear();
+                fn(r, spa, ci, v);
+                out.rp[r + 1] = (int64_t)ci.size();
+            }
+        }
+        for (int64_t r = 0; r < nrows; r++) out.rp[r + 1] += out.rp[r];
+        out.ci.alloc(out.rp[nrows]);
+        out.v.alloc(out.rp[nrows]);
+#pragma omp parallel
+        {
+            Spa spa;
+            spa.init(ncols);
+            std::vector<int32_t> ci;
+            std::vector<double> v;
+#pragma omp for schedule(dynamic, 2048)
+            for (int64_t r = 0; r < nrows; r++) {
+                ci.clear();
+                v.clear();
+                fn(r, spa, ci, v);
+                std::memcpy(out.ci.data() + out.rp[r], ci.data(), ci.size() * sizeof(int32_t));
+                std::memcpy(out.v.data() + out.rp[r], v.data(), v.size() * sizeof(double));
+            }
+        }
+        return;
+    }
     const int64_t CH = 2048;
     const int64_t nch = (nrows + CH - 1) / CH;
     std::vector<Chunk> chunks(nch);
@@ -81,8 +134,6 @@ void build_rows(int64_t nrows, int64_t ncols, HCsr &out, Fn fn) {
             }
         }
     }
-    out.nrows = nrows;
-    out.ncols = ncols;
     out.rp.alloc(nrows + 1);
     out.rp[0] = 0;
     std::vector<int64_t> base(nch + 1, 0);
@@ -490,11 +541,32 @@ void build_hierarchy_take(amg_csr &Kin, const amg_params &prm, HHierarchy &H) {
     build_levels(prm, H);
 }
 
+// AMG_SETUP_TRACE=1: resident host memory (GB) and seconds at every phase boundary of the setup, to
+// stderr (the largest runs are bounded by the host RAM of the box)
+static void trace(const char *what, int l) {
+    static const bool on = [] {
+        const char *e = std::getenv("AMG_SETUP_TRACE");
+        return e && std::atoi(e) != 0;
+    }();
+    if (!on) return;
+    long rss = 0;
+    if (FILE *f = std::fopen("/proc/self/statm", "r")) {
+        long sz = 0;
+        if (std::fscanf(f, "%ld %ld", &sz, &rss) != 2) rss = 0;
+        std::fclose(f);
+    }
+    static const auto t0 = std::chrono::steady_clock::now();
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[setup] %-18s level %d  rss %.2f GB  t %.1f s\n", what, l, rss * 4096.0 / 1e9, sec);
+}
+
 static void build_levels(const amg_params &prm, HHierarchy &H) {
+    trace("start", 0);
     H.prm = prm;
     H.nlevels = 0;
     HLevel &L0 = H.lev[0];
     validate(L0.K);
+    trace("validated", 0);
     L0.N = L0.K.nrows;
     Buf<double> w(L0.N);
     for (int64_t i = 0; i < L0.N; i++) w[i] = 1.0;
@@ -525,11 +597,13 @@ static void build_levels(const amg_params &prm, HHierarchy &H) {
                 pt[i] = pt[i] * pvs[a];
                 agg[i] = aggs[a];
             }
+            trace("pairwise", l);
             if (s + 1 < prm.agg_steps) {
                 HCsr Ac;
                 galerkin_pairwise(*Acur, aggs, pvs, ncs, Ac);
                 A = std::move(Ac);
                 Acur = &A;
+                trace("galerkin_pairwise", l);
             }
             wc = std::move(wn);
             nc = ncs;
@@ -547,14 +621,18 @@ static void build_levels(const amg_params &prm, HHierarchy &H) {
             for (int64_t i = 0; i < N; i++) { L.P.ci[i] = agg[i]; L.P.v[i] = pt[i]; }
             L.omega = 0.0;
         }
+        trace("prolongator", l);
         L.agg = std::move(agg);
         L.ptent = std::move(pt);
         transpose(L.P, L.R);
         HCsr AP, Kc;
         spgemm(L.K, L.P, AP);
+        trace("AP", l);
         spgemm(L.R, AP, Kc);
+        trace("RAP", l);
         { HCsr tmp = std::move(AP); }
         symmetrize(Kc);
+        trace("symmetrized", l);
         HLevel &C = H.lev[l + 1];
         C.K = std::move(Kc);
         C.N = nc;

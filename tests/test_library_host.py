@@ -77,6 +77,33 @@ def test_setup_take_equals_setup():
         amg.Hierarchy(Kn, amg.params(2, host_only=1), take=True)
 
 
+def test_lean_two_pass_setup_bitwise():
+    """The two-pass row assembly of the largest levels (AMG_SETUP_LEAN=1: count, then fill the exact
+    output; automatic from 8 M rows) builds bitwise the single-pass hierarchy."""
+    import hashlib
+    import subprocess
+    import sys
+    code = (
+        "import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2511_21268_b200 as amg\n"
+        "K, _ = amg.iga_poisson(3, 2, 14)\n"
+        "H = amg.Hierarchy(K, amg.params(2, host_only=1))\n"
+        "h = hashlib.sha256()\n"
+        "for l in range(H.info()['levels']):\n"
+        "    e = H.export(l)\n"
+        "    for M in (e['K'], e['P']):\n"
+        "        if M is not None:\n"
+        "            for a in (M.indptr, M.indices, M.data): h.update(np.ascontiguousarray(a).tobytes())\n"
+        "print(h.hexdigest())\n") % ROOT
+    out = {}
+    for lean in ("0", "1"):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           env=dict(os.environ, AMG_SETUP_LEAN=lean), timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[lean] = r.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["1"]
+
+
 def test_solve_without_device_part_fails_loudly():
     K, F = amg.iga_poisson(2, 2, 4)
     H = amg.Hierarchy(K.to_scipy(), amg.params(2, host_only=1))
