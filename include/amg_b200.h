@@ -324,6 +324,13 @@ amg_status amg_dist_view_get(const amg_hierarchy *H, int level, int op, amg_dist
 amg_status amg_share_export(const amg_hierarchy *H, int rank, int nranks, void **share, int64_t *bytes);
 amg_status amg_setup_from_share(const void *share, int64_t bytes, const amg_dist *dist, int host_only,
                                 amg_hierarchy **H);
+/* amg_setup_from_share that takes the blob over: it is freed (std::free) as soon as it is imported —
+ * in every case, also on error — so a rank does not hold the blob and its imported copy through the
+ * device setup.  The blob must come from amg_malloc (or amg_share_export). */
+amg_status amg_setup_from_share_take(void *share, int64_t bytes, const amg_dist *dist, int host_only,
+                                     amg_hierarchy **H);
+/* Host allocation the library may free (receive buffers for amg_setup_from_share_take); NULL on failure. */
+void *amg_malloc(int64_t bytes);
 
 void amg_hierarchy_free(amg_hierarchy *H);
 

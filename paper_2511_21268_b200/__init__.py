@@ -211,6 +211,19 @@ class Share:
         self._p, self.nbytes = ptr, nbytes
         self.array = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(nbytes,))
 
+    @classmethod
+    def alloc(cls, nbytes: int) -> "Share":
+        """A library-allocated buffer (amg_malloc) to receive a share into, for from_share(take=True)."""
+        p = lib().amg_malloc(nbytes)
+        if not p:
+            raise MemoryError(f"amg_malloc({nbytes})")
+        return cls(C.c_void_p(p), nbytes)
+
+    def take(self) -> C.c_void_p:
+        """Hand the buffer over (amg_setup_from_share_take frees it); this Share is empty afterwards."""
+        p, self._p, self.array = self._p, C.c_void_p(), None
+        return p
+
     def close(self) -> None:
         if getattr(self, "_p", None) and self._p.value:
             self.array = None
@@ -248,15 +261,21 @@ class Hierarchy:
         self.prm = prm
 
     @classmethod
-    def from_share(cls, share, dist: _lib.amg_dist | None = None, host_only: bool = False) -> "Hierarchy":
-        """amg_setup_from_share: this rank's hierarchy from its blob (a Share, or any uint8 buffer)."""
-        arr = share.array if isinstance(share, Share) else np.ascontiguousarray(share, dtype=np.uint8)
+    def from_share(cls, share, dist: _lib.amg_dist | None = None, host_only: bool = False,
+                   take: bool = False) -> "Hierarchy":
+        """amg_setup_from_share: this rank's hierarchy from its blob (a Share, or any uint8 buffer).
+        take=True with a Share: amg_setup_from_share_take (the blob is freed once imported)."""
         if not host_only:
             use_torch_allocator()
         H = cls(None)
-        check(lib().amg_setup_from_share(arr.ctypes.data_as(C.c_void_p), arr.size,
-                                         C.byref(dist) if dist is not None else None, int(host_only),
-                                         C.byref(H._h)))
+        dp = C.byref(dist) if dist is not None else None
+        if take and isinstance(share, Share):
+            n = share.nbytes
+            check(lib().amg_setup_from_share_take(share.take(), n, dp, int(host_only), C.byref(H._h)))
+        else:
+            arr = share.array if isinstance(share, Share) else np.ascontiguousarray(share, dtype=np.uint8)
+            check(lib().amg_setup_from_share(arr.ctypes.data_as(C.c_void_p), arr.size, dp, int(host_only),
+                                             C.byref(H._h)))
         H.prm = None
         return H
 
@@ -471,18 +490,18 @@ def setup_distributed(K, prm: _lib.amg_params, rank: int, nranks: int, device: i
             lap("send")
         G.close()
         set_num_threads(max(1, cores // nranks))  # the device setups run side by side
-        H = Hierarchy.from_share(mine, d, host_only=host_only)
-        mine.close()
+        H = Hierarchy.from_share(mine, d, host_only=host_only, take=True)
     else:
         dist.recv(size, 0, group=group)
         lap("wait")
-        buf = torch.empty(int(size[0]), dtype=torch.uint8)
+        sh = Share.alloc(int(size[0]))  # the library frees it once imported (from_share take=True)
+        buf = torch.from_numpy(sh.array)
         for o in range(0, buf.numel(), chunk_bytes):
             dist.recv(buf[o:o + chunk_bytes], 0, group=group)
+        del buf
         lap("recv")
         set_num_threads(max(1, cores // nranks))
-        H = Hierarchy.from_share(buf.numpy(), d, host_only=host_only)
-        del buf
+        H = Hierarchy.from_share(sh, d, host_only=host_only, take=True)
     lap("device_setup")
     H.prm = prm
     H.setup_phases = ph

@@ -23,7 +23,8 @@ EXPORTED = ["amg_iga_poisson", "amg_iga_tables", "amg_csr_free", "amg_free", "am
             "amg_set_allocator", "amg_setup", "amg_setup_take", "amg_pcg_solve", "amg_pcg_solve_host", "amg_vcycle",
             "amg_level_apply", "amg_hierarchy_info", "amg_hierarchy_export", "amg_set_profiling",
             "amg_get_kernel_stats", "amg_operator_config", "amg_operator_set_config", "amg_get_level_times", "amg_nccl_unique_id", "amg_local_rows",
-            "amg_dist_view_get", "amg_share_export", "amg_setup_from_share", "amg_set_num_threads",
+            "amg_dist_view_get", "amg_share_export", "amg_setup_from_share", "amg_setup_from_share_take",
+            "amg_malloc", "amg_set_num_threads",
             "amg_hierarchy_free",
             "amg_last_error"]
 
@@ -118,6 +119,8 @@ def lib() -> C.CDLL:
         "amg_dist_view_get": ([vp, C.c_int, C.c_int, P(amg_dist_view)], C.c_int),
         "amg_share_export": ([vp, C.c_int, C.c_int, P(vp), P(C.c_int64)], C.c_int),
         "amg_setup_from_share": ([vp, C.c_int64, P(amg_dist), C.c_int, P(vp)], C.c_int),
+        "amg_setup_from_share_take": ([vp, C.c_int64, P(amg_dist), C.c_int, P(vp)], C.c_int),
+        "amg_malloc": ([C.c_int64], vp),
         "amg_set_num_threads": ([C.c_int], C.c_int),
         "amg_hierarchy_free": ([vp], None),
         "amg_last_error": ([], C.c_char_p),

@@ -68,6 +68,58 @@ amg_csr *export_csr(const HCsr &A) {
 }
 }  // namespace
 
+namespace {
+// amg_setup_from_share(_take): import the blob (freed right after when `take`), then the device setup,
+// which frees this rank's host operators once they are on the device and before its first collective
+amg_hierarchy *from_share(const void *share, int64_t bytes, const amg_dist *dist, int host_only, void *take) {
+    struct Free {
+        void *p;
+        ~Free() { std::free(p); }
+    } own{take};
+    if (!share) throw Error{AMG_EINVAL, "NULL argument"};
+    if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+        throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
+    const int rank = dist ? dist->rank : 0, nranks = dist ? dist->nranks : 1;
+    amg_hierarchy *H = new amg_hierarchy();
+    try {
+        share_import(share, bytes, rank, nranks, H->host, H->plan);
+        if (take) {  // the imported copy is all that is needed from here on
+            std::free(own.p);
+            own.p = nullptr;
+        }
+        H->host.prm.host_only = host_only ? 1 : 0;
+        H->distributed = nranks > 1;
+        if (!host_only) {
+            // the device holds everything the solve needs: free this rank's host operators (the ranks of
+            // one job share one host, whose RAM is what bounds the largest runs) before the first
+            // collective of the device setup, where a rank waits for the others; the sizes, nnz counts
+            // and row bounds stay for amg_hierarchy_info / amg_local_rows
+            auto release = [H] {
+                auto drop = [](HCsr &A) {
+                    A.ci = Buf<int32_t>();
+                    A.v = Buf<double>();
+                };
+                for (int l = 0; l < H->host.nlevels; l++) {
+                    HLevel &L = H->host.lev[l];
+                    drop(L.K);
+                    drop(L.P);
+                    drop(L.R);
+                    drop(H->plan.lev[l].K.A);
+                    drop(H->plan.lev[l].P.A);
+                    drop(H->plan.lev[l].R.A);
+                }
+                H->host.released = true;
+            };
+            H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr, release);
+        }
+    } catch (...) {
+        delete H;
+        throw;
+    }
+    return H;
+}
+}  // namespace
+
 extern "C" {
 
 const char *amg_last_error(void) { return get_error(); }
@@ -240,46 +292,30 @@ amg_status amg_share_export(const amg_hierarchy *H, int rank, int nranks, void *
     API_END
 }
 
+
 amg_status amg_setup_from_share(const void *share, int64_t bytes, const amg_dist *dist, int host_only,
                                 amg_hierarchy **Hout) {
     API_BEGIN
-    if (!share || !Hout) throw Error{AMG_EINVAL, "NULL argument"};
-    if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
-        throw Error{AMG_EINVAL, "bad amg_dist (rank/nranks)"};
-    const int rank = dist ? dist->rank : 0, nranks = dist ? dist->nranks : 1;
-    amg_hierarchy *H = new amg_hierarchy();
-    try {
-        share_import(share, bytes, rank, nranks, H->host, H->plan);
-        H->host.prm.host_only = host_only ? 1 : 0;
-        H->distributed = nranks > 1;
-        if (!host_only) {
-            H->dev = dev_create(H->host, dist, H->distributed ? &H->plan : nullptr);
-            // the device holds everything the solve needs: free this rank's host operators (the ranks of
-            // one job share one host, whose RAM is what bounds the largest runs); the sizes, nnz counts
-            // and row bounds stay for amg_hierarchy_info / amg_local_rows
-            auto drop = [](HCsr &A) {
-                A.ci = Buf<int32_t>();
-                A.v = Buf<double>();
-            };
-            for (int l = 0; l < H->host.nlevels; l++) {
-                HLevel &L = H->host.lev[l];
-                drop(L.K);
-                drop(L.P);
-                drop(L.R);
-                drop(H->plan.lev[l].K.A);
-                drop(H->plan.lev[l].P.A);
-                drop(H->plan.lev[l].R.A);
-            }
-            H->host.released = true;
-        }
-    } catch (...) {
-        delete H;
-        throw;
-    }
-    *Hout = H;
+    if (!Hout) throw Error{AMG_EINVAL, "NULL argument"};
+    *Hout = from_share(share, bytes, dist, host_only, nullptr);
     return AMG_OK;
     API_END
 }
+
+amg_status amg_setup_from_share_take(void *share, int64_t bytes, const amg_dist *dist, int host_only,
+                                     amg_hierarchy **Hout) {
+    if (!Hout) {
+        std::free(share);
+        set_error("NULL argument");
+        return AMG_EINVAL;
+    }
+    API_BEGIN
+    *Hout = from_share(share, bytes, dist, host_only, share);
+    return AMG_OK;
+    API_END
+}
+
+void *amg_malloc(int64_t bytes) { return std::malloc(bytes > 0 ? (size_t)bytes : 1); }
 
 void amg_hierarchy_free(amg_hierarchy *H) {
     if (!H) return;

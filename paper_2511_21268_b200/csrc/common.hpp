@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -150,7 +151,11 @@ void build_hierarchy_take(amg_csr &K, const amg_params &prm, HHierarchy &H);
 
 // device.cu
 struct DevState;
-DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *plan);
+// release (may be null): called once every operator is on the device, before the first collective
+// (NCCL init): a share-built hierarchy frees its host operators there, so the ranks that wait in the
+// collective for the others do not hold them
+DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *plan,
+                     const std::function<void()> &release = {});
 void dev_destroy(DevState *D);
 
 }  // namespace amgb

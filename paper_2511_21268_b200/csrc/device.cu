@@ -1330,14 +1330,9 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
         D.lev[l].R.wmask = (l == ld) ? ~0u : m;
     }
     // boundary rows (touch a ghost value or are pushed somewhere) of every distributed operator; the
-    // CSR cores run the other row groups before waiting for any peer
-    auto ghost_rows = [&](const LocalOp &op, std::vector<char> &b) {
-        const int64_t nown = op.col_end - op.col_begin;
-        b.assign(op.A.nrows, 0);
-        if (op.full_cols) return;
-        for (int64_t i = 0; i < op.A.nrows; i++)
-            for (int64_t k = op.A.rp[i]; k < op.A.rp[i + 1] && !b[i]; k++) b[i] = op.A.ci[k] < 0 || op.A.ci[k] >= nown;
-    };
+    // CSR cores run the other row groups before waiting for any peer.  The ghost-reading rows were
+    // marked at upload (DCsr::ghostrow; the host operators may be gone by now)
+    auto ghost_rows = [&](const LocalOp &, std::vector<char> &b, const DCsr &A) { b = A.ghostrow; };
     auto add_pushed = [](std::vector<char> &b, const DCsr *A) {
         if (!A) return;
         for (size_t i = 0; i < A->pushed.size() && i < b.size(); i++) b[i] |= A->pushed[i];
@@ -1345,16 +1340,16 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
     for (int l = 0; l <= ld; l++) {
         DLevel &L = D.lev[l];
         const DCsr *Pab = l > 0 ? &D.lev[l - 1].P : nullptr;
-        ghost_rows(plan.lev[l].K, L.K.bnd);
+        ghost_rows(plan.lev[l].K, L.K.bnd, L.K);
         add_pushed(L.K.bnd, &L.K);
         add_pushed(L.K.bnd, &L.R);
         add_pushed(L.K.bnd, Pab);
         build_gorder(D, L.K);
         if (l + 1 < D.nlevels) {
-            ghost_rows(plan.lev[l].P, L.P.bnd);
+            ghost_rows(plan.lev[l].P, L.P.bnd, L.P);
             add_pushed(L.P.bnd, &L.K);
             build_gorder(D, L.P);
-            ghost_rows(plan.lev[l].R, L.R.bnd);
+            ghost_rows(plan.lev[l].R, L.R.bnd, L.R);
             if (l == ld) std::fill(L.R.bnd.begin(), L.R.bnd.end(), 1);  // all-gather: every row pushed
             else add_pushed(L.R.bnd, &D.lev[l + 1].K);
             build_gorder(D, L.R);
@@ -1401,7 +1396,8 @@ void p2p_setup(DevState &D, const DistPlan &plan) {
 }
 }  // namespace
 
-DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *planp) {
+DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *planp,
+                     const std::function<void()> &release) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw Error{AMG_ENODEV, "no CUDA device"};
     if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
@@ -1446,33 +1442,8 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
         D->nranks = nr;
         if (nr > 1 && (!planp || planp->nranks != nr)) throw Error{AMG_EINVAL, "missing distribution plan"};
         const DistPlan &plan = *planp;
-        if (nr > 1) {
-            D->last_dist = plan.last_dist;
-            ncclUniqueId id;
-            static_assert(sizeof(id) == sizeof(dist->nccl_id), "ncclUniqueId size");
-            std::memcpy(&id, dist->nccl_id, sizeof(id));
-            NCCL_OK(ncclCommInitRank(&D->comm, nr, id, D->rank));
-        } else {
-            D->last_dist = H.nlevels - 1;
-        }
+        D->last_dist = nr > 1 ? plan.last_dist : H.nlevels - 1;
         const int fmt = H.prm.format;
-        // transport: P2P peer memory (default) unless AMG_TRANSPORT=nccl, a degree-1 smoother, or a rank
-        // that cannot map its peers — decided collectively so every rank uses the same one
-        bool want_p2p = false;
-        if (nr > 1) {
-            int ok = 1;
-            if (const char *e = std::getenv("AMG_TRANSPORT")) ok = std::strcmp(e, "nccl") != 0;
-            if (H.prm.cheb_degree < 2 || nr > 32) ok = 0;  // wait masks are 32-bit
-            for (int q = 0; q < ndev && ok; q++) {
-                if (q == dev_id) continue;
-                int can = 0;
-                if (cudaDeviceCanAccessPeer(&can, dev_id, q) != cudaSuccess || !can) ok = 0;
-            }
-            std::vector<int64_t> v(1, ok);
-            const std::vector<int64_t> all = nccl_allgather_i64(*D, v);
-            want_p2p = true;
-            for (int q = 0; q < nr; q++) want_p2p = want_p2p && all[q] != 0;
-        }
         std::vector<int64_t> vlo(H.nlevels, 0), vhi(H.nlevels, 0);  // ghost extents of the level vectors
         for (int l = 0; l < H.nlevels; l++) {
             const HLevel &h = H.lev[l];
@@ -1486,7 +1457,18 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                 const DistLevel &P = plan.lev[l];
                 r0 = P.K.row_begin;
                 L.n = P.K.row_end - P.K.row_begin;
+                // rows that read a ghost column (the P2P boundary rows, p2p_setup), taken from the host
+                // operators now: they may be released before p2p_setup runs
+                auto ghost_rows = [](const LocalOp &op, std::vector<char> &b) {
+                    const int64_t nown = op.col_end - op.col_begin;
+                    b.assign(op.A.nrows, 0);
+                    if (op.full_cols) return;
+                    for (int64_t i = 0; i < op.A.nrows; i++)
+                        for (int64_t k = op.A.rp[i]; k < op.A.rp[i + 1] && !b[i]; k++)
+                            b[i] = op.A.ci[k] < 0 || op.A.ci[k] >= nown;
+                };
                 upload_local(*D, P.K, L.K, fmt, 0);
+                ghost_rows(P.K, L.K.ghostrow);
                 if (!coarsest) {
                     // P̄_l's ghosts of the coarse x lie beyond K_{l+1}'s on both sides
                     const LocalOp &Kc = plan.lev[l + 1].K;
@@ -1494,6 +1476,8 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                     const int64_t klo = next_dist ? Kc.nlo : 0, khi = next_dist ? (int64_t)Kc.ghost.size() - Kc.nlo : 0;
                     upload_local(*D, P.P, L.P, fmt, 1, klo, khi);
                     upload_local(*D, P.R, L.R, fmt, 2);
+                    ghost_rows(P.P, L.P.ghostrow);
+                    ghost_rows(P.R, L.R.ghostrow);
                 }
             } else {
                 L.n = h.N;
@@ -1525,6 +1509,32 @@ DevState *dev_create(const HHierarchy &H, const amg_dist *dist, const DistPlan *
                 vlo[l] = std::max(vlo[l], -A->lo_base);
                 vhi[l] = std::max(vhi[l], A->hi_base - A->nown + (A->nghost - A->nlo));
             }
+        }
+        // every operator is on the device: the host copies may go (share-built hierarchies), then the
+        // collectives — NCCL init and the transport decision — with nothing large held while waiting
+        if (release) release();
+        if (nr > 1) {
+            ncclUniqueId id;
+            static_assert(sizeof(id) == sizeof(dist->nccl_id), "ncclUniqueId size");
+            std::memcpy(&id, dist->nccl_id, sizeof(id));
+            NCCL_OK(ncclCommInitRank(&D->comm, nr, id, D->rank));
+        }
+        // transport: P2P peer memory (default) unless AMG_TRANSPORT=nccl, a degree-1 smoother, or a rank
+        // that cannot map its peers — decided collectively so every rank uses the same one
+        bool want_p2p = false;
+        if (nr > 1) {
+            int ok = 1;
+            if (const char *e = std::getenv("AMG_TRANSPORT")) ok = std::strcmp(e, "nccl") != 0;
+            if (H.prm.cheb_degree < 2 || nr > 32) ok = 0;  // wait masks are 32-bit
+            for (int q = 0; q < ndev && ok; q++) {
+                if (q == dev_id) continue;
+                int can = 0;
+                if (cudaDeviceCanAccessPeer(&can, dev_id, q) != cudaSuccess || !can) ok = 0;
+            }
+            std::vector<int64_t> v(1, ok);
+            const std::vector<int64_t> all = nccl_allgather_i64(*D, v);
+            want_p2p = true;
+            for (int q = 0; q < nr; q++) want_p2p = want_p2p && all[q] != 0;
         }
         const int64_t n00 = D->lev[0].n;
         // level vectors b, x, r, d0, d1 and the PCG r, z, p, q: in the P2P slab (same offsets on every

@@ -159,6 +159,8 @@ struct DCsr {
     int2 *push_dst = nullptr;
     std::vector<char> pushed;   // host: owned index i has a push destination
     std::vector<char> bnd;      // host: row i touches a ghost value or is pushed (P2P boundary row)
+    std::vector<char> ghostrow; // host: row i reads a ghost column (computed at upload, before the host
+                                // operators may be released)
     int *gorder = nullptr;      // device: row groups (of the current G) boundary-first
     int64_t nbnd = 0, gorder_G = 0, gorder_cap = 0;
     int *sidx = nullptr;     // device: local owned indices to send, by destination rank
