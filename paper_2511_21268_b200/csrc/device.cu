@@ -375,7 +375,11 @@ bool upload_sellvi(DevState &D, const HCsr &A, DCsr &out, bool rule) {
     if (const char *e = std::getenv("AMG_SELLVI_WIN"))
         if (std::atoi(e) == 0) win = false;
     const int64_t nblk = (nsl + kWinSlices - 1) / kWinSlices;
-    int64_t win_max = kWinMax;  // AMG_WIN_MAX: experiments with wider windows (fewer CTAs per SM)
+    // the largest window: one window and the value table within kWinSmem (two CTAs per SM).  Measured
+    // (run r2k): L3's ≈ 10 K-double windows at 2 CTAs/SM beat the plain layout (22.7 vs 23.3 ms per
+    // iteration); C4's p = 4 windows with its 4,147-value table would leave 1 CTA/SM (1.90 vs 1.33 ms
+    // per level-0 step) and stay plain.  AMG_WIN_MAX overrides (experiments).
+    int64_t win_max = std::min<int64_t>(kWinMax, kWinSmem / 8 - (((int64_t)tab.size() + 1) & ~1));
     if (const char *e = std::getenv("AMG_WIN_MAX")) win_max = std::max<int64_t>(256, std::min<int64_t>(20000, std::atoll(e)));
     std::vector<std::vector<int4>> bruns;
     int64_t wmax = 0;

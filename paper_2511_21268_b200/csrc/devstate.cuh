@@ -66,11 +66,12 @@ struct DevBuf {
 // (C3's K₀: 1,054 values; C4's: 4,147).  At U = 4 the kernel's 80 registers allow 3 CTAs of 256 threads
 // per SM, and 3 × 64 KB still fits the SM's shared memory, so staging never lowers the occupancy there.
 constexpr int64_t kSellviSmemVals = 8192;
-// windowed SELL-VI (k_sellviw): slices per block (= warps per CTA), the largest staged window
-// (doubles; 2 buffers + a 1,054-value table = 104 KB at C3 where the windows are ≤ 5,950), and the
-// column gap below which two runs of a window are merged rather than copied separately
+// windowed SELL-VI (k_sellviw): slices per block (= warps per CTA), the largest staged window (doubles;
+// further bounded by kWinSmem with the table, device.cu; C3's windows are ≤ 5,950), and the column gap
+// below which two runs of a window are merged rather than copied separately
 constexpr int kWinSlices = dev::kBlock / 32;
-constexpr int64_t kWinMax = 7168;
+constexpr int64_t kWinMax = 14336;
+constexpr int64_t kWinSmem = 110 * 1024;  // window + value table of one CTA: 2 CTAs fit an SM
 constexpr int64_t kWinGap = 8;
 
 // Resident CTAs per SM of kernel `fn` at (block, dynamic smem) on the CURRENT device, after raising
