@@ -65,3 +65,18 @@ def test_paper_solution_converges_at_order(p):
         errs.append(cp.l2_error_full(p, n, uf, uD))
     rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert np.all(rates >= p + 0.5), (errs, rates)
+
+
+@pytest.mark.parametrize("k", [12, 24])
+def test_paper_experiment_iterations_against_table1a_p3(k, table1):
+    """The paper's cube experiment at p = 3 (its data, FCG P:L1107, §5.1 coarse CG P:L1114, degree-8
+    Chebyshev P:L1117) against Table 1a: 10 and 11 FCG iterations at k = 12 and 24.  The
+    paper's optimized 1st-kind polynomial is unpublished (the oracle uses Lottes' 4th kind, c.16), so
+    the counts are a band, ±1 — at p = 3 the two smoothers agree this closely (at p ≥ 4 they do not:
+    DESIGN.md §8)."""
+    from oracle import cube_paper
+    K = oracle.assemble(3, 3, k)
+    F, _ = cube_paper.paper_cube_rhs(3, k)
+    H = oracle.setup(K, oracle.OParams.for_degree(3, coarse_solver=1))
+    u, it, rr, hist, rc = oracle.fcg(H, F, rtol=1e-6, maxit=100)
+    assert rc == 0 and abs(it - table1[(k, 3)][2]) <= 1, (it, table1[(k, 3)][2])
