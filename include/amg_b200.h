@@ -198,6 +198,9 @@ amg_status amg_setup_take(amg_csr *K, const amg_params *prm, const amg_dist *dis
  * exit.  Stops when ‖r_k‖₂ <= rtol·‖F‖₂ (recurrence residual) or k == maxit; iteration count = number
  * of K·p products.  F == 0 -> u = 0, *iters = 0.  cuda_stream: cudaStream_t (NULL = legacy default).
  * resid_history: nullable host array of length maxit+1, receives ‖r_k‖/‖F‖.
+ * The iterations run as ONE CUDA graph launch with a conditional WHILE node whose controller kernel
+ * takes the stopping test on the device (env AMG_DEVICE_LOOP=0: one graph per iteration and the test
+ * on the host; bitwise the same results).  The call returns when the solve is complete.
  * Returns AMG_OK, AMG_NOT_CONVERGED, AMG_ENOTSPD (breakdown), AMG_ECUDA, AMG_EINVAL. */
 amg_status amg_pcg_solve(amg_hierarchy *H, const double *F, double *u, double rtol, int maxit,
                          void *cuda_stream, int *iters, double *relres, double *resid_history);
@@ -209,7 +212,9 @@ amg_status amg_pcg_solve_host(amg_hierarchy *H, const double *F, double *u, doub
 /* One V-cycle z = V(r) (c.18) on DEVICE vectors of length N_0. */
 amg_status amg_vcycle(amg_hierarchy *H, const double *r, double *z, void *cuda_stream);
 
-/* y = A x on the device for A = K_l (op 0), P̄_l (op 1, x has N_{l+1} entries) or R_l = P̄_lᵀ (op 2). */
+/* y = A x on the device for A = K_l (op 0), P̄_l (op 1, x has N_{l+1} entries) or R_l = P̄_lᵀ (op 2).
+ * x must be 16-byte aligned (the windowed SELL-VI layout stages it with bulk copies; AMG_EINVAL
+ * otherwise) and readable up to the next 16-byte boundary past its end. */
 amg_status amg_level_apply(amg_hierarchy *H, int level, int op, const double *x, double *y,
                            void *cuda_stream);
 
